@@ -1,0 +1,221 @@
+"""Pins for the oracle's search (Alg. 1 SYCOS_TD, Alg. 2 SYCOS_BU, §6 noise pruning, Alg. 4 chunks).
+
+The control logic is pinned with a table-driven mock MI provider against the
+paper's worked examples and the SPEC examples
+(S:329-341), then against invariants and planted-window
+recovery on the real estimator (cfg1).
+"""
+import numpy as np
+import pytest
+
+import datagen
+
+
+def P(orc, **kw):
+    base = dict(k=2, method=1, noise=0, s_min=16, s_max=16, sigma=0.2, tau_ratio=0.25, p=3, h=5,
+                t_max_idle=3, n_chunks=1, seed=0)
+    base.update(kw)
+    return orc.make_params(**base)
+
+
+# ------------------------------------------------------------------ TD worked examples
+def test_td_worked_example_p238(orc):
+    # w0=[0,16), w1=[4,20) uncorrelated; w2=[8,24) correlated -> S={w2}; partition [ts0, ts2)
+    # passed down; w3 starts at te2 = 24.
+    def fn(t0, t1):
+        return (1.0, 1.0, 1.0) if (t0, t1) == (8, 24) else (0.0, 1.0, 0.0)
+
+    res, st, calls = orc.search_mock(fn, 64, P(orc, s_max=16, s_min=4, sizes=[16, 4]))
+    assert [(r[2], r[3]) for r in res] == [(8, 24)]
+    assert calls[:4] == [(0, 16), (4, 20), (8, 24), (24, 40)]
+    layer2 = [c for c in calls if c[1] - c[0] == 4]
+    covered = set()
+    for (a, b) in layer2:
+        covered.update(range(a, b))
+    assert covered == set(range(0, 8)) | set(range(24, 64))  # partitions [0,8) and [24,64)
+
+
+def test_td_worked_example_p3009(orc):
+    # w1..w4 uncorrelated, w5 correlated -> left-out list [ts1, ts5); w6 starts right after te5.
+    def fn(t0, t1):
+        return (1.0, 1.0, 1.0) if (t0, t1) == (16, 32) else (0.0, 1.0, 0.0)
+
+    res, st, calls = orc.search_mock(fn, 64, P(orc, s_max=16, s_min=4, sizes=[16, 4]))
+    assert [(r[2], r[3]) for r in res] == [(16, 32)]
+    assert calls[:6] == [(0, 16), (4, 20), (8, 24), (12, 28), (16, 32), (32, 48)]
+    layer2 = {c for c in calls if c[1] - c[0] == 4}
+    assert (12, 16) in layer2 and (32, 36) in layer2 and not any(16 <= a < 32 for a, _ in layer2)
+
+
+def test_td_fully_correlated_single_window(orc):
+    # fully correlated pair with s_max = N -> {[0, N)} after layer 1
+    res, st, calls = orc.search_mock(lambda a, b: (2.0, 1.0, 1.0), 256, P(orc, s_max=256, s_min=16))
+    assert [(r[2], r[3]) for r in res] == [(0, 256)] and st["td_windows"] == 1
+
+
+def test_td_independent_empty_and_full_coverage(orc):
+    # independent pair -> {}; every sample ends in a bottom-layer partition
+    res, st, calls = orc.search_mock(lambda a, b: (0.0, 1.0, 0.0), 200, P(orc, s_max=64, s_min=16))
+    assert res == []
+    bottom = [c for c in calls if c[1] - c[0] == 16]
+    covered = set()
+    for a, b in bottom:
+        covered.update(range(a, b))
+    assert covered == set(range(200))
+    # layer schedule: halving 64 -> 32 -> 16; delta = s/4
+    assert {c[1] - c[0] for c in calls} == {64, 32, 16}
+    assert (4, 20) in calls and (8, 40) in calls and (16, 80) in calls
+
+
+def _noise_mock(s, delta, clean_tails=()):
+    # main windows: uncorrelated (nmi 0.1 < sigma), mi 0.5; overlap (size s-delta): mi 0.6 > main;
+    # tail (size delta): nmi 0.01 < tau = 0.05 -> noise, unless listed in clean_tails.
+    def fn(t0, t1):
+        size = t1 - t0
+        if size == s:
+            return (0.5, 1.0, 0.1)
+        if size == s - delta:
+            return (0.6, 1.0, 0.1)
+        if size == delta:
+            return (0.0, 1.0, 0.5 if (t0, t1) in clean_tails else 0.01)
+        return (0.0, 1.0, 0.0)
+    return fn
+
+
+def test_td_noise_p1_skips_immediately(orc):
+    # p=1, verdict noise -> skip past w1
+    res, st, calls = orc.search_mock(_noise_mock(16, 4), 64, P(orc, noise=1, p=1, s_min=16, s_max=16, k=2))
+    mains = [c for c in calls if c[1] - c[0] == 16]
+    assert mains == [(0, 16), (4, 20), (20, 36), (24, 40), (40, 56), (44, 60)]
+    assert st["td_noise_checks"] == 3 and st["td_skips"] == 3 and st["td_windows"] == 6
+
+
+def test_td_noise_streak_p3(orc):
+    res, st, calls = orc.search_mock(_noise_mock(16, 4), 64, P(orc, noise=1, p=3, s_min=16, s_max=16, k=2))
+    mains = [c for c in calls if c[1] - c[0] == 16]
+    # checks at t=4,8,12 -> skip to 28; checks at 32,36,40 -> skip to 56 (56+16 > 64)
+    assert mains == [(0, 16), (4, 20), (8, 24), (12, 28), (28, 44), (32, 48), (36, 52), (40, 56)]
+    assert st["td_skips"] == 2
+
+
+def test_td_noise_streak_reset(orc):
+    # p=3, verdicts noise, noise, clean -> streak reset, no skip at t=12
+    fn = _noise_mock(16, 4, clean_tails={(24, 28)})
+    res, st, calls = orc.search_mock(fn, 64, P(orc, noise=1, p=3, s_min=16, s_max=16, k=2))
+    mains = [c for c in calls if c[1] - c[0] == 16]
+    # t=4 s1, t=8 s2, t=12 clean -> 0, t=16 s1, t=20 s2, t=24 s3 -> skip to 40; 40: no check; 44: s1; 48: s2
+    assert mains[:9] == [(0, 16), (4, 20), (8, 24), (12, 28), (16, 32), (20, 36), (24, 40), (40, 56), (44, 60)]
+    assert st["td_skips"] == 1
+
+
+def test_noise_predicate_stated_values(orc):
+    # S:275-276 with the split reading: tail nmi 0.03 < tau=0.05 and mix mi < base mi -> noise;
+    # tail nmi 0.10 >= tau -> not noise regardless of the mixture.
+    for tail_nmi, expect_skip in ((0.03, True), (0.10, False)):
+        def fn(t0, t1, tail_nmi=tail_nmi):
+            size = t1 - t0
+            if size == 16:
+                return (0.20, 1.0, 0.10)   # mixture w1 (normalized below sigma)
+            if size == 12:
+                return (0.30, 1.0, 0.30)   # base w_o
+            return (0.0, 1.0, tail_nmi)    # extension w_delta
+        res, st, _ = orc.search_mock(fn, 32, P(orc, noise=1, p=1, s_min=16, s_max=16, k=2))
+        assert (st["td_skips"] > 0) == expect_skip
+
+
+# ------------------------------------------------------------------ BU
+def test_bu_constant_landscape_iterations(orc):
+    # constant MI: every iteration rejects (strict '>', G4) -> T_maxIdle+1 iterations per climb
+    for T in (0, 3):
+        res, st, _ = orc.search_mock(lambda a, b: (0.3, 1.0, 0.1), 640,
+                                     P(orc, method=2, s_min=32, s_max=128, t_max_idle=T, k=4))
+        assert res == []
+        assert st["bu_climbs"] == 20                 # lo = 0, 32, ..., 608
+        # S:384 (T=0 stops at the first non-improvement); the last climb [608,640) has an empty
+        # neighbourhood (every delta-neighbour leaves [lo,hi) or the size bounds) and stops at once.
+        assert st["bu_iterations"] == 19 * (T + 1)
+
+
+def test_bu_climbs_to_unimodal_peak(orc):
+    d = 10
+    a, b = 50, 50 + 32 + 3 * d   # peak window; s_min=32, delta_bu=10
+
+    def fn(t0, t1):
+        v = 1.0 - (abs(t0 - a) + abs(t1 - b)) / 1000.0
+        return (v, 1.0, 0.5 if (t0, t1) == (a, b) else 0.05)
+
+    res, st, calls = orc.search_mock(fn, 400, P(orc, method=2, s_min=32, s_max=200, delta_bu=d, k=4))
+    assert [(r[2], r[3]) for r in res] == [(a, b)]
+    assert res[0][1] == 2
+
+
+def test_bu_noise_prunes_right_p1(orc):
+    # smaller windows score higher; every extension is noise (nmi 0 < tau) and every mix (larger)
+    # has lower MI than the base -> with p=1 the applicable direction is pruned after one verdict.
+    fn = lambda t0, t1: (1.0 / (t1 - t0), 1.0, 0.0)
+    base = P(orc, method=2, s_min=32, s_max=128, k=4, t_max_idle=1)
+    _, st0, _ = orc.search_mock(fn, 320, base)
+    _, st1, _ = orc.search_mock(fn, 320, P(orc, method=2, s_min=32, s_max=128, k=4, t_max_idle=1, noise=1, p=1))
+    assert st1["bu_prunes"] >= st1["bu_climbs"] - 1   # the last climb has no neighbourhood
+    assert st1["bu_neighbors"] < st0["bu_neighbors"]
+
+
+def test_bu_seed_determinism(orc):
+    wl = datagen.cfg1()
+    p = orc.make_params(wl.search, method=2)
+    r1, s1 = orc.search(wl.series, wl.pairs, p)
+    r2, s2 = orc.search(wl.series, wl.pairs, p)
+    assert r1 == r2 and s1 == s2
+
+
+# ------------------------------------------------------------------ chunks (Alg. 4)
+def test_chunk_plan_s511(orc):
+    assert orc.chunk_plan(1000, 4, 100) == [(0, 250), (150, 500), (400, 750), (650, 1000)]
+    assert orc.chunk_plan(1000, 1, 100) == [(0, 1000)]
+
+
+def test_chunks_np1_equals_plain(orc):
+    wl = datagen.cfg1()
+    a = orc.search(wl.series, wl.pairs, orc.make_params(wl.search))
+    b = orc.search(wl.series, wl.pairs, orc.make_params(wl.search, n_chunks=1))
+    assert a == b
+
+
+def test_chunks_interior_windows_preserved(orc):
+    # windows far from chunk boundaries appear identically in the n_p=2 run (TD)
+    wl = datagen.cfg1()
+    a, _ = orc.search(wl.series, wl.pairs, orc.make_params(wl.search, method=1))
+    b, _ = orc.search(wl.series, wl.pairs, orc.make_params(wl.search, method=1, n_chunks=2))
+    for w in b:
+        assert all(not (w[2] < q[3] and q[2] < w[3]) or q == w for q in b)  # disjoint
+    interior_a = [w for w in a if w[3] <= 1024 - 512]
+    assert all(w in b for w in interior_a)
+
+
+# ------------------------------------------------------------------ invariants + planted recovery
+def _coverage(res, block):
+    a, b = block
+    cov = set()
+    for r in res:
+        cov.update(range(max(a, r[2]), min(b, r[3])))
+    return len(cov) / (b - a)
+
+
+@pytest.mark.parametrize("noise", [0, 1])
+def test_cfg1_search_invariants_and_recovery(orc, noise):
+    wl = datagen.cfg1()
+    sc = wl.search
+    res, st = orc.search(wl.series, wl.pairs, orc.make_params(sc, noise=noise))
+    x, y = wl.series
+    for method in (1, 2):
+        rs = [r for r in res if r[1] == method]
+        # disjoint, sorted, size bounds, sigma re-verified from scratch
+        for i, r in enumerate(rs):
+            assert sc.s_min <= r[3] - r[2] <= sc.s_max
+            if i:
+                assert rs[i - 1][3] <= r[2]
+            w = orc.window(x[r[2]:r[3]], y[r[2]:r[3]], k=sc.k)
+            assert w.nmi >= sc.sigma and w.mi == r[4] and w.nmi == r[6]
+        # planted recovery: union coverage >= 0.8 per planted block (S:331 form)
+        for (a, b, _) in wl.planted[0]:
+            assert _coverage(rs, (a, b)) >= 0.8, (method, a, b, rs)
