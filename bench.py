@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the iSYCOS hot path on B200 (the driver's contract).
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+the default workload is BASELINE.json configs[1] ("cfg2": one pair, n = 100,000, AR(1) background
+with 4 planted relations, k = 4, scales 32..4096, SYCOS_TD + SYCOS_BU with MI-based noise pruning),
+run through the C ABI (isycos_search) with the series resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2|cfg3|cfg4s]
+
+Metric (BASELINE.json): KSG window compares/s, counting 2*w*(w-1) brute-force-equivalent compares
+(w(w-1) joint-distance + w(w-1) marginal compares) for every distinct window the search consumed;
+windows/s is reported beside it.  N > 1 (torchrun): every rank runs its own replica of the step
+(cfg2 is a single-pair search: "replicas only"); value = all ranks' compares / the
+max over ranks of the device-timed region ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# issue-bound compare roofline: 148 SM x 4 SMSP x 32 lanes x 1 warp-instr/clk
+# at clocks.max.sm = 1965 MHz = 3.72e13 lane-instr/s; the brute-force path needs >= 5 lane
+# instructions per compare (kNN: 2 FADD + FMNMX + compare; count: FADD + FADD + LEA.HI per marginal).
+SMS, SMSP, LANES = 148, 4, 32
+INSTR_PER_COMPARE = 5.0
+
+
+def peak_compares(sm_mhz: float) -> float:
+    return SMS * SMSP * LANES * sm_mhz * 1e6 / INSTR_PER_COMPARE
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str | None):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"]
+        if self.gpu_id:
+            cmd += ["-i", self.gpu_id]
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(cmd, stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------- workloads
+def make_workload(name: str):
+    import datagen
+
+    if name == "cfg2":
+        wl = datagen.cfg2()
+        desc = {"workload": "cfg2", "n": 100_000, "pairs": 1, "k": 4, "scales": "32..4096 (TD halving)",
+                "method": "TD+BU", "noise_pruning": True, "sigma": 0.2, "tau_ratio": 0.25}
+    elif name == "cfg1":
+        wl = datagen.cfg1()
+        desc = {"workload": "cfg1", "n": 2048, "pairs": 1, "k": 4, "scales": "64..512", "method": "TD+BU",
+                "noise_pruning": True}
+    elif name == "cfg4s":
+        wl = datagen.cfg4(n=200_000, n_series=8)
+        wl.search.s_max = 4096
+        desc = {"workload": "cfg4s", "n": 200_000, "series": 8, "pairs": 28, "k": 4, "scales": "64..4096",
+                "method": "TD+BU", "noise_pruning": True, "note": "reduced configs[3] instance"}
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return wl, desc
+
+
+def compares_of(stats):
+    # 2 * sum w(w-1) over the distinct windows the search consumed (brute-force-equivalent compares)
+    return 2.0 * stats["distinct_pairs"]
+
+
+# ----------------------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The oracle (plain single-threaded C++) timed on the host cores: the base contract's reference
+    arm for this tier (no upstream code exists; BASELINE.json 'published' is empty)."""
+    if rank != 0:
+        return 0
+    import oracle
+
+    wl, desc = make_workload(args.workload)
+    n_s = args.ref_prefix
+    series = [s[:n_s] for s in wl.series]
+    params = oracle.make_params(wl.search)
+    times, comps, wins = [], [], []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        res, st = oracle.search(series, wl.pairs, params)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+            comps.append(compares_of(st))
+            wins.append(st["distinct_windows"])
+    tot = sum(times)
+    value = sum(comps) / tot
+    sample = (f"{desc['workload']} prefix [0,{n_s}) of both series ({n_s / len(wl.series[0]):.0%} of the "
+              f"workload), full search with the same parameters, per step")
+    line = {
+        "impl": "reference", "metric": "KSG window compares/s", "value": value, "unit": "compares/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": desc, "windows_per_s": sum(wins) / tot,
+        "cpu_baseline": {"value": value, "unit": "compares/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "compares/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(args, wl, desc):
+    import oracle
+
+    n_s = args.ref_prefix
+    series = [s[:n_s] for s in wl.series]
+    t = time.perf_counter()
+    res, st = oracle.search(series, wl.pairs, oracle.make_params(wl.search))
+    dt = time.perf_counter() - t
+    return {"value": compares_of(st) / dt, "unit": "compares/s", "cores": 1, "kind": "oracle",
+            "sample": f"{desc['workload']} prefix [0,{n_s}) of both series, full TD+BU search, same "
+                      f"parameters ({dt:.1f} s single-threaded)",
+            "windows_per_s": st["distinct_windows"] / dt}
+
+
+# ----------------------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--ref-prefix", type=int, default=25_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lookahead", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2204_09131_b200 import build
+
+    if rank == 0:
+        build.build()
+    if dist:
+        dist.barrier()
+    import paper_2204_09131_b200 as isy
+
+    wl, desc = make_workload(args.workload)
+    stream = torch.cuda.current_stream()
+    dev_series = [torch.from_numpy(s).cuda() for s in wl.series]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    kw = {}
+    if args.lookahead:
+        kw["lookahead"] = args.lookahead
+
+    def step(series, profile=True):
+        return isy.search_workload(wl, series=series, stream=stream, profile=profile, **kw)
+
+    def sync_all():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(dev_series)
+    torch.cuda.synchronize()
+
+    props = torch.cuda.get_device_properties(local)
+    gpu_id = None
+    try:
+        gpu_id = "GPU-" + str(props.uuid) if not str(props.uuid).startswith("GPU-") else str(props.uuid)
+    except Exception:
+        gpu_id = None
+    sampler = ClockSampler(gpu_id)
+    sampler.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ms_total, comps, wins, kms, kpairs, launches, ksg_launches, rounds = 0.0, 0.0, 0, 0.0, 0, 0, 0, 0
+    h2d = d2h = 0
+    results = None
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed iterations (256 MiB > 126 MB L2)
+        sync_all()
+        ev0.record(stream)
+        res, st = step(dev_series)
+        ev1.record(stream)
+        sync_all()
+        ms_total += ev0.elapsed_time(ev1)
+        comps += compares_of(st)
+        wins += st["distinct_windows"]
+        k = st["kernel"]
+        kms += k["kernel_ms"]
+        kpairs += k["point_pairs"]
+        launches += k["launches"]
+        ksg_launches += k["ksg_launches"]
+        rounds += k["rounds"]
+        results = res
+    clocks = sampler.stop()
+
+    # end to end: host (pinned) series through the public API, H2D inside the timed region
+    host_series = [torch.from_numpy(s).pin_memory() for s in wl.series]
+    e2e_ms, e2e_comps = 0.0, 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        sync_all()
+        ev0.record(stream)
+        res, st = step(host_series, profile=False)
+        ev1.record(stream)
+        sync_all()
+        e2e_ms += ev0.elapsed_time(ev1)
+        e2e_comps += compares_of(st)
+        h2d += st["kernel"]["h2d_bytes"]
+        d2h += st["kernel"]["d2h_bytes"] + len(res) * 48
+
+    def agg(v, op):
+        if not dist:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=op)
+        return t.item()
+
+    import torch.distributed as tdist
+
+    ms_max = agg(ms_total, tdist.ReduceOp.MAX) if dist else ms_total
+    comps_all = agg(comps, tdist.ReduceOp.SUM) if dist else comps
+    wins_all = agg(wins, tdist.ReduceOp.SUM) if dist else wins
+    e2e_max = agg(e2e_ms, tdist.ReduceOp.MAX) if dist else e2e_ms
+    e2e_all = agg(e2e_comps, tdist.ReduceOp.SUM) if dist else e2e_comps
+
+    if rank == 0:
+        value = comps_all / (ms_max / 1e3)
+        sm_for_peak = 1965.0
+        peak = peak_compares(sm_for_peak)
+        achieved = (2.0 * kpairs) / (kms / 1e3) if kms > 0 else None
+        line = {
+            "metric": "KSG window compares/s", "value": value, "unit": "compares/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": dict(desc, l2="flushed between steps (256 MiB write)",
+                                                 parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
+            "windows_per_s": wins_all / (ms_max / 1e3),
+            "results_per_step": len(results) if results is not None else None,
+            "roofline": {"bound": "alu", "achieved": achieved / 1e12 if achieved else None,
+                         "peak": peak / 1e12, "unit": "Tcompare/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "kernel": "ksg_small_kernel + ksg_tile_kernel (all KSG launches of the step)",
+                         "peak_basis": "issue-bound: 148 SM x 4 SMSP x 32 lanes x 1965 MHz / 5 lane-instr "
+                                       "per compare (DESIGN.md §Roofline)",
+                         "kernel_share_of_step": (kms / ms_total) if ms_total else None,
+                         "evaluated_compares_per_step": 2.0 * kpairs / args.steps},
+            "e2e": {"value": e2e_all / (e2e_max / 1e3), "unit": "compares/s",
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+            "gpu_launches": launches,
+            "ksg_launches": ksg_launches,
+            "rounds_per_step": rounds / args.steps,
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args, wl, desc)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

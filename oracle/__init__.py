@@ -76,6 +76,13 @@ def lib():
                                     C.POINTER(OStats)]
         L.oracle_search_mock.argtypes = [MIFN, C.c_void_p, C.c_int64, C.POINTER(OParams), C.c_void_p,
                                          C.c_int64, C.POINTER(C.c_int64), C.POINTER(OStats)]
+        L.oracle_point.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                   C.c_void_p, C.c_void_p]
+        L.oracle_point_psi_q.restype = C.c_int64
+        L.oracle_point_psi_q.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        L.oracle_point_log_q.restype = C.c_int64
+        L.oracle_point_log_q.argtypes = [C.c_float]
+        L.oracle_finish.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_void_p]
         L.oracle_chunk_plan.argtypes = [C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_int32]
     return _lib
 
@@ -208,6 +215,30 @@ def search_mock(fn, n: int, params: OParams, cap: int = 1 << 14):
     if rc != 0:
         raise ValueError(f"oracle_search_mock rc={rc}")
     return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS}, calls
+
+
+def point(x, y, i: int, k: int = 4, variant: int = 0):
+    """(eps_i, n_x(i), n_y(i)) of point i of the window (x, y)."""
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.ascontiguousarray(y, np.float32)
+    e = np.zeros(1, np.float32)
+    nn = np.zeros(2, np.int32)
+    rc = lib().oracle_point(_p(x), _p(y), len(x), int(i), k, variant, _p(e), _p(nn))
+    if rc != 0:
+        raise ValueError(f"oracle_point rc={rc}")
+    return float(e[0]), int(nn[0]), int(nn[1])
+
+
+def point_terms(nx: int, ny: int, eps: float, variant: int = 0):
+    """Canonical per-point terms (q(psi) pair sum, q(LN(2 eps)) or 0)."""
+    return lib().oracle_point_psi_q(int(nx), int(ny), variant), lib().oracle_point_log_q(float(eps))
+
+
+def finish(s_psi: int, s_log: int, zeros: int, w: int, k: int = 4, variant: int = 0):
+    """(mi, h, nmi) from the canonical sums (the window finish of §8(c).3)."""
+    o = np.zeros(3)
+    lib().oracle_finish(int(s_psi), int(s_log), int(zeros), int(w), k, variant, _p(o))
+    return float(o[0]), float(o[1]), float(o[2])
 
 
 def chunk_plan(n: int, n_p: int, s_max: int):

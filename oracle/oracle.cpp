@@ -591,6 +591,80 @@ int oracle_search_mock(oracle_mi_fn fn, void* ctx, int64_t n, const OParams* P, 
     return (int64_t)res.size() > cap ? -4 : 0;
 }
 
+// One point i of a window (sampled checks at sizes where the full window is too slow):
+// out_eps = eps_i (KSG-1 radius), out_n = {n_x, n_y} of the chosen variant.
+int oracle_point(const float* x, const float* y, int64_t w, int64_t i, int32_t k, int32_t variant,
+                 float* out_eps, int32_t* out_n) {
+    if (w <= k || k < 1 || i < 0 || i >= w) return -3;
+    std::vector<float> buf;
+    float eps = kth_distance(x, y, w, i, k, 0, buf);
+    int64_t nx = 0, ny = 0;
+    if (variant == 0) {
+        for (int64_t j = 0; j < w; ++j) {
+            if (j == i) continue;
+            if (std::fabs(x[i] - x[j]) < eps) ++nx;
+            if (std::fabs(y[i] - y[j]) < eps) ++ny;
+        }
+    } else {
+        std::vector<std::pair<float, int64_t>> dj;
+        for (int64_t j = 0; j < w; ++j)
+            if (j != i) dj.push_back({dist(x[i], y[i], x[j], y[j]), j});
+        std::sort(dj.begin(), dj.end());
+        float dxk = 0.0f, dyk = 0.0f;
+        for (int m = 0; m < k; ++m) {
+            int64_t j = dj[m].second;
+            dxk = std::max(dxk, std::fabs(x[i] - x[j]));
+            dyk = std::max(dyk, std::fabs(y[i] - y[j]));
+        }
+        for (int64_t j = 0; j < w; ++j) {
+            if (j == i) continue;
+            if (std::fabs(x[i] - x[j]) <= dxk) ++nx;
+            if (std::fabs(y[i] - y[j]) <= dyk) ++ny;
+        }
+    }
+    *out_eps = eps;
+    out_n[0] = (int32_t)nx;
+    out_n[1] = (int32_t)ny;
+    return 0;
+}
+
+// Per-point canonical terms (q(psi(a)) + q(psi(b)), q(LN(2 eps)) or 0) and the window finish
+// from the canonical sums: out3 = {mi, h, nmi}.
+int64_t oracle_point_psi_q(int32_t nx, int32_t ny, int32_t variant) {
+    int64_t a = variant == 0 ? nx + 1 : nx, b = variant == 0 ? ny + 1 : ny;
+    ensure_psi(std::max(a, b));
+    return q32(psi(a)) + q32(psi(b));
+}
+int64_t oracle_point_log_q(float eps) { return eps > 0.0f ? q32(canon_ln(2.0 * (double)eps)) : 0; }
+
+int oracle_finish(int64_t s_psi, int64_t s_log, int32_t zeros, int64_t w, int32_t k, int32_t variant,
+                  double* out3) {
+    ensure_psi(w + 1);
+    double dw = (double)w;
+    double mean_q = ((double)s_psi * kTwoPowMinus32) / dw;
+    double mi;
+    if (variant == 0) {
+        double a = psi(k) + psi(w);
+        mi = a - mean_q;
+    } else {
+        double a = psi(k) - 1.0 / (double)k;
+        a = a + psi(w);
+        mi = a - mean_q;
+    }
+    double h;
+    if (zeros > 0) {
+        h = -INFINITY;
+    } else {
+        double a = psi(w) - psi(k);
+        double m = ((double)s_log * kTwoPowMinus32) / dw;
+        h = a + 2.0 * m;
+    }
+    out3[0] = mi;
+    out3[1] = h;
+    out3[2] = normalized(mi, h, zeros);
+    return 0;
+}
+
 int oracle_chunk_plan(int64_t n, int32_t n_p, int64_t s_max, int64_t* out, int32_t cap) {
     auto c = chunk_plan(n, n_p, s_max);
     for (int32_t i = 0; i < (int32_t)c.size() && i < cap; ++i) { out[2 * i] = c[i].first; out[2 * i + 1] = c[i].second; }

@@ -1,0 +1,317 @@
+// C ABI of libisycos.so (include/isycos.h): validation, host/device pointer handling, error codes.
+// All arithmetic of the path runs in ksg_kernels.cu; this file only marshals.
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "engine.h"
+
+using namespace isy;
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear: unregistered host memory on some drivers
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int fail(const Status& s) {
+    set_last_error(s);
+    return s.code;
+}
+
+int ok() {
+    set_last_error(Status{});
+    return ISYCOS_OK;
+}
+
+// A series resident on the device in the layout the kernels need (16-B aligned, readable up to a
+// multiple of 4 floats).  Caller-owned device series that already satisfy this are used in place.
+struct DevSeries {
+    DevSeries() = default;
+    DevSeries(const DevSeries&) = delete;
+    DevSeries& operator=(const DevSeries&) = delete;
+    Engine* eng = nullptr;
+    const float* ptr = nullptr;
+    float* owned = nullptr;
+    ~DevSeries() {
+        if (owned) eng->free_series(owned);
+    }
+    Status make(Engine* e, const float* src, int64_t n, cudaStream_t st, BatchStats* bs) {
+        eng = e;
+        const bool dev = is_device_ptr(src);
+        if (dev && (reinterpret_cast<uintptr_t>(src) % 16 == 0) && (n % 4 == 0)) {
+            ptr = src;
+            return Status{};
+        }
+        Status s = e->upload_series(src, n, dev, &owned, st, bs);
+        ptr = owned;
+        return s;
+    }
+};
+
+// copy `bytes` from a host buffer to a caller pointer that may be host or device
+Status put_out(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!dst || bytes == 0) return Status{};
+    if (is_device_ptr(dst)) {
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return cuda_err(e, "copy output to device");
+    }
+    std::memcpy(dst, src, bytes);
+    return Status{};
+}
+
+}  // namespace
+
+extern "C" int isycos_abi_version(void) { return ISYCOS_ABI_VERSION; }
+
+extern "C" int isycos_release_cache(void) {
+    release_engine_for_current_device();
+    return ok();
+}
+
+extern "C" int isycos_mi_batch_ex(const float* x, const float* y, int64_t n, const isycos_window* windows,
+                                  int64_t n_windows, int32_t k, const isycos_mi_opts* opts, double* out_mi) {
+    if (!x || !y || (!windows && n_windows > 0) || (!out_mi && n_windows > 0))
+        return fail(make_err(ISYCOS_E_INVAL, "null pointer argument"));
+    if (n < 2) return fail(make_err(ISYCOS_E_INVAL, "n must be >= 2"));
+    if (k < 1 || k > ISYCOS_MAX_K) return fail(make_err(ISYCOS_E_INVAL, "k must be in [1, 16]"));
+    if (n_windows < 0) return fail(make_err(ISYCOS_E_INVAL, "n_windows < 0"));
+    isycos_mi_opts o{};
+    if (opts) o = *opts;
+    if (o.variant != 0)
+        return fail(make_err(ISYCOS_E_INVAL, "variant 1 (KSG-2) has no GPU kernel in this build (oracle only)"));
+    if (n_windows == 0) return ok();
+
+    Status s;
+    Engine* eng = engine_for_current_device(&s);
+    if (!eng) return fail(s);
+    cudaStream_t st = o.stream ? static_cast<cudaStream_t>(o.stream) : eng->own_stream();
+    BatchStats bs;
+
+    // windows to host
+    std::vector<isycos_window> wh(n_windows);
+    if (is_device_ptr(windows)) {
+        cudaError_t e = cudaMemcpyAsync(wh.data(), windows, n_windows * sizeof(isycos_window),
+                                        cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(cuda_err(e, "copy windows to host"));
+        bs.d2h_bytes += n_windows * (int64_t)sizeof(isycos_window);
+    } else {
+        std::memcpy(wh.data(), windows, n_windows * sizeof(isycos_window));
+    }
+    int64_t total_pts = 0;
+    for (int64_t i = 0; i < n_windows; ++i) {
+        const int64_t t0 = wh[i].t0, t1 = wh[i].t1;
+        if (t0 < 0 || t1 > n || t0 >= t1)
+            return fail(make_err(ISYCOS_E_RANGE, "window " + std::to_string(i) + " = [" + std::to_string(t0) + ", " +
+                                                     std::to_string(t1) + ") outside [0, n)"));
+        if (t1 - t0 > ISYCOS_MAX_W) return fail(make_err(ISYCOS_E_RANGE, "window larger than ISYCOS_MAX_W"));
+        if (t1 - t0 <= k)
+            return fail(make_err(ISYCOS_E_TOO_FEW, "window " + std::to_string(i) + " has w <= k"));
+        total_pts += t1 - t0;
+    }
+
+    DevSeries dx, dy;
+    if (!(s = dx.make(eng, x, n, st, &bs)).ok()) return fail(s);
+    if (!(s = dy.make(eng, y, n, st, &bs)).ok()) return fail(s);
+    bool fin_x = false, fin_y = false;
+    if (!(s = eng->check_finite(dx.ptr, n, st, &fin_x)).ok()) return fail(s);
+    if (!(s = eng->check_finite(dy.ptr, n, st, &fin_y)).ok()) return fail(s);
+    bs.launches += 2;
+    if (!fin_x || !fin_y) return fail(make_err(ISYCOS_E_INVAL, "non-finite sample in x or y"));
+
+    // debug outputs: kernels write device memory; stage through device temporaries if needed
+    const bool want_dbg = o.dbg_eps || o.dbg_nx || o.dbg_ny;
+    DebugOut dbg;
+    std::vector<void*> tmp_dev;
+    auto dev_target = [&](void* user, size_t elem, void** devp) -> Status {
+        if (!user) {
+            *devp = nullptr;
+            return Status{};
+        }
+        if (is_device_ptr(user)) {
+            *devp = user;
+            return Status{};
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, total_pts * elem);
+        if (e != cudaSuccess) return cuda_err(e, "cudaMalloc debug buffer");
+        tmp_dev.push_back(p);
+        *devp = p;
+        return Status{};
+    };
+    void *de = nullptr, *dnx = nullptr, *dny = nullptr;
+    auto cleanup = [&] {
+        for (void* p : tmp_dev) cudaFree(p);
+    };
+    if (want_dbg) {
+        if (!(s = dev_target(o.dbg_eps, 4, &de)).ok() || !(s = dev_target(o.dbg_nx, 4, &dnx)).ok() ||
+            !(s = dev_target(o.dbg_ny, 4, &dny)).ok()) {
+            cleanup();
+            return fail(s);
+        }
+        dbg.eps = static_cast<float*>(de);
+        dbg.nx = static_cast<int32_t*>(dnx);
+        dbg.ny = static_cast<int32_t*>(dny);
+    }
+
+    PairPtrs pp{dx.ptr, dy.ptr};
+    std::vector<KsgWin> wins(n_windows);
+    int64_t off = 0;
+    for (int64_t i = 0; i < n_windows; ++i) {
+        const int32_t w = (int32_t)(wh[i].t1 - wh[i].t0);
+        wins[i] = KsgWin{wh[i].t0, w, 0, want_dbg ? off : -1};
+        off += w;
+    }
+    std::vector<KsgRec> recs(n_windows);
+    s = eng->evaluate(&pp, 1, wins.data(), n_windows, k, o.variant, recs.data(), dbg, st,
+                      (o.flags & ISYCOS_F_PROFILE) != 0, &bs);
+    if (!s.ok()) {
+        cleanup();
+        return fail(s);
+    }
+    // debug arrays back to host targets
+    auto dbg_back = [&](void* user, void* devp) -> Status {
+        if (!user || user == devp) return Status{};
+        cudaError_t e = cudaMemcpyAsync(user, devp, total_pts * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return cuda_err(e, "copy debug output");
+    };
+    if (want_dbg) {
+        if (!(s = dbg_back(o.dbg_eps, de)).ok() || !(s = dbg_back(o.dbg_nx, dnx)).ok() ||
+            !(s = dbg_back(o.dbg_ny, dny)).ok()) {
+            cleanup();
+            return fail(s);
+        }
+    }
+    cleanup();
+
+    std::vector<double> col(n_windows);
+    auto put_d = [&](double* dst, auto getter) -> Status {
+        if (!dst) return Status{};
+        for (int64_t i = 0; i < n_windows; ++i) col[i] = getter(recs[i]);
+        return put_out(dst, col.data(), n_windows * sizeof(double), st);
+    };
+    if (!(s = put_d(out_mi, [](const KsgRec& r) { return r.mi; })).ok()) return fail(s);
+    if (!(s = put_d(o.out_h, [](const KsgRec& r) { return r.h; })).ok()) return fail(s);
+    if (!(s = put_d(o.out_nmi, [](const KsgRec& r) { return r.nmi; })).ok()) return fail(s);
+    if (o.out_sum_psi_q || o.out_sum_log_q) {
+        std::vector<int64_t> c(n_windows);
+        if (o.out_sum_psi_q) {
+            for (int64_t i = 0; i < n_windows; ++i) c[i] = recs[i].s_psi;
+            if (!(s = put_out(o.out_sum_psi_q, c.data(), n_windows * 8, st)).ok()) return fail(s);
+        }
+        if (o.out_sum_log_q) {
+            for (int64_t i = 0; i < n_windows; ++i) c[i] = recs[i].s_log;
+            if (!(s = put_out(o.out_sum_log_q, c.data(), n_windows * 8, st)).ok()) return fail(s);
+        }
+    }
+    if (o.out_zero_eps) {
+        std::vector<int32_t> c(n_windows);
+        for (int64_t i = 0; i < n_windows; ++i) c[i] = recs[i].zero_eps;
+        if (!(s = put_out(o.out_zero_eps, c.data(), n_windows * 4, st)).ok()) return fail(s);
+    }
+    if (o.stats) bs.add_to(o.stats);
+    return ok();
+}
+
+extern "C" int isycos_mi_batch(const float* x, const float* y, int64_t n, const isycos_window* windows,
+                               int64_t n_windows, int32_t k, double* out_mi) {
+    return isycos_mi_batch_ex(x, y, n, windows, n_windows, k, nullptr, out_mi);
+}
+
+extern "C" int isycos_search(const float* const* series, int32_t n_series, int64_t n, const isycos_pair* pairs,
+                             int32_t n_pairs, const isycos_scales* scales, int32_t k, const isycos_noise* noise,
+                             const isycos_search_opts* opts, isycos_result_window* out_windows,
+                             int64_t out_capacity, int64_t* out_count, isycos_search_stats* out_stats) {
+    if (!series || !pairs || !scales || !opts || !out_count || (!out_windows && out_capacity > 0))
+        return fail(make_err(ISYCOS_E_INVAL, "null pointer argument"));
+    if (n_series < 1 || n_pairs < 0 || n < 2) return fail(make_err(ISYCOS_E_INVAL, "bad n_series / n_pairs / n"));
+    SearchParams P;
+    P.k = k;
+    P.variant = opts->variant;
+    P.method = opts->method;
+    P.s_min = scales->s_min;
+    P.s_max = scales->s_max;
+    if (scales->sizes && scales->n_sizes > 0) P.sizes.assign(scales->sizes, scales->sizes + scales->n_sizes);
+    P.noise = noise && noise->enabled;
+    P.tau_ratio = noise ? noise->tau_ratio : 0.25;
+    P.p = noise ? noise->p : 3;
+    P.sigma = opts->sigma;
+    P.delta_td = opts->delta_td;
+    P.delta_bu = opts->delta_bu;
+    P.t_max_idle = opts->t_max_idle;
+    P.h = opts->h;
+    P.n_chunks = opts->n_chunks;
+    P.lookahead = opts->lookahead > 0 ? opts->lookahead : 256;
+    P.seed = opts->seed;
+    P.profile = (opts->flags & ISYCOS_F_PROFILE) != 0;
+    auto bad = [&](const char* m) { return fail(make_err(ISYCOS_E_INVAL, m)); };
+    if (k < 1 || k > ISYCOS_MAX_K) return bad("k must be in [1, 16]");
+    if (P.variant != 0) return bad("variant 1 (KSG-2) has no GPU kernel in this build (oracle only)");
+    if (P.s_min < 2 || P.s_min > P.s_max || P.s_max > n) return bad("need 2 <= s_min <= s_max <= n");
+    if (P.s_max > ISYCOS_MAX_W) return bad("s_max > ISYCOS_MAX_W");
+    if (k >= P.s_min) return bad("need k < s_min");
+    if (!(P.sigma > 0.0 && P.sigma <= 1.0)) return bad("need 0 < sigma <= 1");
+    if (!(P.tau_ratio >= 0.0 && P.tau_ratio < 1.0)) return bad("need 0 <= tau_ratio < 1");
+    if (P.h < 1 || P.p < 1 || P.t_max_idle < 0) return bad("need h >= 1, p >= 1, t_max_idle >= 0");
+    if (P.method < 1 || P.method > 3) return bad("method must be 1 (TD), 2 (BU) or 3 (both)");
+    if (P.n_chunks < 1) return bad("n_chunks must be >= 1");
+    if (P.delta_td < 0 || P.delta_bu < 0) return bad("delta must be >= 0");
+    for (size_t i = 0; i < P.sizes.size(); ++i) {
+        if (P.sizes[i] <= k || P.sizes[i] > P.s_max || P.sizes[i] < P.s_min || (i && P.sizes[i] >= P.sizes[i - 1]))
+            return bad("sizes must be strictly decreasing within [s_min, s_max] and > k");
+    }
+    for (int32_t i = 0; i < n_pairs; ++i) {
+        if (pairs[i].xs < 0 || pairs[i].ys < 0 || pairs[i].xs >= n_series || pairs[i].ys >= n_series)
+            return bad("pair index out of range");
+    }
+
+    Status s;
+    Engine* eng = engine_for_current_device(&s);
+    if (!eng) return fail(s);
+    cudaStream_t st = opts->stream ? static_cast<cudaStream_t>(opts->stream) : eng->own_stream();
+    BatchStats bs;
+
+    // series used by any pair -> device layout; finiteness checked on the device
+    std::vector<char> used(n_series, 0);
+    for (int32_t i = 0; i < n_pairs; ++i) used[pairs[i].xs] = used[pairs[i].ys] = 1;
+    std::vector<DevSeries> dev(n_series);
+    for (int32_t i = 0; i < n_series; ++i) {
+        if (!used[i]) continue;
+        if (!series[i]) return bad("null series pointer");
+        if (!(s = dev[i].make(eng, series[i], n, st, &bs)).ok()) return fail(s);
+        bool fin = false;
+        if (!(s = eng->check_finite(dev[i].ptr, n, st, &fin)).ok()) return fail(s);
+        bs.launches += 1;
+        if (!fin) return fail(make_err(ISYCOS_E_INVAL, "non-finite sample in series " + std::to_string(i)));
+    }
+    std::vector<PairPtrs> pp(n_pairs);
+    std::vector<int32_t> ids(n_pairs);
+    for (int32_t i = 0; i < n_pairs; ++i) {
+        pp[i] = PairPtrs{dev[pairs[i].xs].ptr, dev[pairs[i].ys].ptr};
+        ids[i] = pairs[i].id;
+    }
+    std::vector<isycos_result_window> res;
+    isycos_search_stats local{};
+    s = run_search(eng, pp, ids, n, P, st, &res, &local);
+    if (!s.ok()) return fail(s);
+    bs.add_to(&local.kernel);
+    if (out_stats) *out_stats = local;
+    *out_count = (int64_t)res.size();
+    const int64_t m = std::min<int64_t>(out_capacity, (int64_t)res.size());
+    if (m > 0) std::memcpy(out_windows, res.data(), m * sizeof(isycos_result_window));
+    if ((int64_t)res.size() > out_capacity)
+        return fail(make_err(ISYCOS_E_TRUNC, "out_capacity too small: need " + std::to_string(res.size())));
+    return ok();
+}

@@ -1,0 +1,362 @@
+// Per-device engine: digamma tables, batch buffers, batch evaluation, profiling.
+//
+// A batch is a list of windows over one or more series pairs.  Host work per batch is only
+// marshalling: bin windows into size classes, pack descriptors into one
+// pinned buffer, one H2D copy, one launch per non-empty class, one D2H copy of the records.
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "engine.h"
+
+namespace isy {
+
+// ---------------------------------------------------------------- errors
+namespace {
+thread_local std::string g_last_error;
+}
+
+Status make_err(int code, const std::string& msg) {
+    Status s;
+    s.code = code;
+    s.msg = msg;
+    return s;
+}
+
+Status cuda_err(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return Status{};
+    return make_err(e == cudaErrorMemoryAllocation ? ISYCOS_E_NOMEM : ISYCOS_E_CUDA,
+                    std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+void set_last_error(const Status& s) { g_last_error = s.ok() ? std::string() : s.msg; }
+
+}  // namespace isy
+
+extern "C" const char* isycos_last_error(void) { return isy::g_last_error.c_str(); }
+
+namespace isy {
+
+#define ISY_CK(expr)                                          \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_err(_e, #expr);    \
+    } while (0)
+
+void BatchStats::add_to(isycos_kernel_stats* s) const {
+    if (!s) return;
+    s->windows += windows;
+    s->point_pairs += point_pairs;
+    s->launches += launches;
+    s->ksg_launches += ksg_launches;
+    s->rounds += rounds;
+    s->kernel_ms += kernel_ms;
+    s->h2d_bytes += h2d_bytes;
+    s->d2h_bytes += d2h_bytes;
+}
+
+// ---------------------------------------------------------------- engine registry (one per device)
+namespace {
+std::mutex g_mu;
+std::map<int, std::unique_ptr<Engine>> g_engines;
+}  // namespace
+
+Engine* engine_for_current_device(Status* st) {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        *st = cuda_err(e, "cudaGetDevice (no CUDA device?)");
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_engines.find(dev);
+    if (it != g_engines.end()) return it->second.get();
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) {
+        *st = cuda_err(e, "cudaGetDeviceProperties");
+        return nullptr;
+    }
+    if (prop.major != 10) {
+        *st = make_err(ISYCOS_E_CUDA, "libisycos is built for sm_100a (B200); device " + std::to_string(dev) +
+                                          " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+        return nullptr;
+    }
+    auto eng = std::make_unique<Engine>();
+    Status s = eng->init(dev);
+    if (!s.ok()) {
+        *st = s;
+        return nullptr;
+    }
+    Engine* p = eng.get();
+    g_engines[dev] = std::move(eng);
+    return p;
+}
+
+void release_engine_for_current_device() {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_engines.erase(dev);
+}
+
+Status Engine::init(int dev) {
+    dev_ = dev;
+    ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
+    return Status{};
+}
+
+Engine::~Engine() {
+    cudaFree(psi_);
+    cudaFree(psiq_);
+    cudaFree(acc_);
+    cudaFree(dstage_);
+    cudaFree(drec_);
+    cudaFree(dflag_);
+    cudaFreeHost(hstage_);
+    cudaFreeHost(hrec_);
+    for (auto e : events_) cudaEventDestroy(e);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+Status Engine::ensure_psi(int64_t w_max, cudaStream_t st) {
+    if (psi_max_ >= w_max) return Status{};
+    int64_t m = std::max<int64_t>(w_max, 65537);
+    m = std::min<int64_t>(std::max<int64_t>(m, psi_max_ * 2), ISYCOS_MAX_W + 1);
+    double *psi = nullptr, *inv = nullptr;
+    long long* psiq = nullptr;
+    ISY_CK(cudaMalloc(&psi, (m + 1) * sizeof(double)));
+    ISY_CK(cudaMalloc(&inv, (m + 1) * sizeof(double)));
+    ISY_CK(cudaMalloc(&psiq, (m + 1) * sizeof(long long)));
+    ISY_CK(launch_psi_tables(psi, psiq, inv, m, st));
+    ISY_CK(cudaStreamSynchronize(st));
+    cudaFree(inv);
+    cudaFree(psi_);
+    cudaFree(psiq_);
+    psi_ = psi;
+    psiq_ = psiq;
+    psi_max_ = m;
+    return Status{};
+}
+
+Status Engine::ensure_capacity(int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists) {
+    if (acc_cap_ < n_wins) {
+        int64_t c = std::max<int64_t>(n_wins, acc_cap_ * 2);
+        cudaFree(acc_);
+        acc_ = nullptr;
+        ISY_CK(cudaMalloc(&acc_, c * sizeof(KsgAcc)));
+        ISY_CK(cudaMemset(acc_, 0, c * sizeof(KsgAcc)));
+        acc_cap_ = c;
+    }
+    if (drec_cap_ < n_wins) {
+        int64_t c = std::max<int64_t>(n_wins, drec_cap_ * 2);
+        cudaFree(drec_);
+        drec_ = nullptr;
+        ISY_CK(cudaMalloc(&drec_, c * sizeof(KsgRec)));
+        drec_cap_ = c;
+    }
+    if (hrec_cap_ < n_wins) {
+        int64_t c = std::max<int64_t>(n_wins, hrec_cap_ * 2);
+        cudaFreeHost(hrec_);
+        hrec_ = nullptr;
+        ISY_CK(cudaMallocHost(&hrec_, c * sizeof(KsgRec)));
+        hrec_cap_ = c;
+    }
+    const int64_t bytes = 64 + n_pairs * (int64_t)sizeof(PairPtrs) + n_wins * (int64_t)sizeof(KsgWin) +
+                          n_lists * 4 + n_items * (int64_t)sizeof(KsgItem) + 4 * 64;
+    if (dstage_cap_ < bytes) {
+        int64_t c = std::max<int64_t>(bytes, dstage_cap_ * 2);
+        cudaFree(dstage_);
+        dstage_ = nullptr;
+        ISY_CK(cudaMalloc(&dstage_, c));
+        dstage_cap_ = c;
+    }
+    if (hstage_cap_ < bytes) {
+        int64_t c = std::max<int64_t>(bytes, hstage_cap_ * 2);
+        cudaFreeHost(hstage_);
+        hstage_ = nullptr;
+        ISY_CK(cudaMallocHost(&hstage_, c));
+        hstage_cap_ = c;
+    }
+    return Status{};
+}
+
+static int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
+
+Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
+                        int32_t variant, KsgRec* recs_host, const DebugOut& dbg, cudaStream_t st, bool profile,
+                        BatchStats* bs) {
+    if (n <= 0) return Status{};
+    if (n > INT32_MAX / 2) return make_err(ISYCOS_E_INVAL, "batch too large");
+    int64_t w_max = 0;
+    for (int64_t i = 0; i < n; ++i) w_max = std::max<int64_t>(w_max, wins[i].w);
+    {
+        Status s = ensure_psi(w_max + 1, st);
+        if (!s.ok()) return s;
+    }
+    // bin windows: small classes R = 1,2,4,8; tile classes R = 2,4
+    std::vector<int32_t> small[4];
+    std::vector<int32_t> tile[2];
+    int64_t n_items = 0;
+    int64_t pp = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int w = wins[i].w;
+        pp += (int64_t)w * (w - 1);
+        const int R = small_class_R(w);
+        if (R) {
+            small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
+        } else {
+            const int tr = tile_R(w);
+            tile[tr == 2 ? 0 : 1].push_back((int32_t)i);
+            n_items += (w + kTileThreads * tr - 1) / (kTileThreads * tr);
+        }
+    }
+    int64_t n_lists = 0;
+    for (auto& v : small) n_lists += (int64_t)v.size();
+    {
+        Status s = ensure_capacity(n, n_items, n_pairs, n_lists);
+        if (!s.ok()) return s;
+    }
+    // pack [pairs | wins | lists | items] into the pinned stage
+    int64_t off_pairs = 0;
+    int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
+    int64_t off_lists = align64(off_wins + n * (int64_t)sizeof(KsgWin));
+    int64_t off_items = align64(off_lists + n_lists * 4);
+    int64_t total = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
+    std::memcpy(hstage_ + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
+    std::memcpy(hstage_ + off_wins, wins, n * sizeof(KsgWin));
+    int64_t list_off[4];
+    {
+        int32_t* lp = reinterpret_cast<int32_t*>(hstage_ + off_lists);
+        int64_t c = 0;
+        for (int s = 0; s < 4; ++s) {
+            list_off[s] = c;
+            std::memcpy(lp + c, small[s].data(), small[s].size() * 4);
+            c += (int64_t)small[s].size();
+        }
+    }
+    int64_t item_off[2];
+    {
+        KsgItem* ip = reinterpret_cast<KsgItem*>(hstage_ + off_items);
+        int64_t c = 0;
+        for (int s = 0; s < 2; ++s) {
+            item_off[s] = c;
+            const int tr = s == 0 ? 2 : 4;
+            for (int32_t q : tile[s]) {
+                const int w = wins[q].w;
+                for (int i0 = 0; i0 < w; i0 += kTileThreads * tr) ip[c++] = KsgItem{q, i0};
+            }
+        }
+    }
+    ISY_CK(cudaMemcpyAsync(dstage_, hstage_, total, cudaMemcpyHostToDevice, st));
+    if (bs) bs->h2d_bytes += total;
+
+    KsgLaunch L;
+    L.pairs = reinterpret_cast<const PairPtrs*>(dstage_ + off_pairs);
+    L.wins = reinterpret_cast<const KsgWin*>(dstage_ + off_wins);
+    L.psi = psi_;
+    L.psiq = psiq_;
+    L.acc = acc_;
+    L.out = drec_;
+    L.dbg_eps = dbg.eps;
+    L.dbg_nx = dbg.nx;
+    L.dbg_ny = dbg.ny;
+    L.k = k;
+    L.variant = variant;
+    const int32_t* dlists = reinterpret_cast<const int32_t*>(dstage_ + off_lists);
+    const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dstage_ + off_items);
+
+    // launches: biggest work first so the small classes fill the tail
+    int n_launch = 0;
+    auto ev_pair = [&](int i) -> std::pair<cudaEvent_t, cudaEvent_t> {
+        while ((int)events_.size() < 2 * (i + 1)) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            events_.push_back(e);
+        }
+        return {events_[2 * i], events_[2 * i + 1]};
+    };
+    auto launch = [&](auto&& fn) -> Status {
+        std::pair<cudaEvent_t, cudaEvent_t> ev{};
+        if (profile) {
+            ev = ev_pair(n_launch);
+            ISY_CK(cudaEventRecord(ev.first, st));
+        }
+        ISY_CK(fn());
+        if (profile) ISY_CK(cudaEventRecord(ev.second, st));
+        ++n_launch;
+        return Status{};
+    };
+    for (int s = 1; s >= 0; --s) {
+        if (tile[s].empty()) continue;
+        int64_t cnt = 0;
+        for (int32_t q : tile[s]) {
+            const int tr = s == 0 ? 2 : 4;
+            cnt += (wins[q].w + kTileThreads * tr - 1) / (kTileThreads * tr);
+        }
+        const int R = s == 0 ? 2 : 4;
+        const KsgItem* ip = ditems + item_off[s];
+        Status r = launch([&] { return launch_ksg_tile(L, ip, (int32_t)cnt, R, st); });
+        if (!r.ok()) return r;
+    }
+    for (int s = 3; s >= 0; --s) {
+        if (small[s].empty()) continue;
+        const int R = 1 << s;
+        const int32_t* lp = dlists + list_off[s];
+        const int32_t cnt = (int32_t)small[s].size();
+        Status r = launch([&] { return launch_ksg_small(L, lp, cnt, R, st); });
+        if (!r.ok()) return r;
+    }
+    if (recs_host) {
+        ISY_CK(cudaMemcpyAsync(hrec_, drec_, n * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
+        if (bs) bs->d2h_bytes += n * (int64_t)sizeof(KsgRec);
+    }
+    ISY_CK(cudaStreamSynchronize(st));
+    if (recs_host) std::memcpy(recs_host, hrec_, n * sizeof(KsgRec));
+    if (bs) {
+        bs->windows += n;
+        bs->point_pairs += pp;
+        bs->launches += n_launch;
+        bs->ksg_launches += n_launch;
+        bs->rounds += 1;
+        if (profile) {
+            for (int i = 0; i < n_launch; ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, events_[2 * i], events_[2 * i + 1]);
+                bs->kernel_ms += ms;
+            }
+        }
+    }
+    return Status{};
+}
+
+Status Engine::upload_series(const float* src, int64_t n, bool src_is_device, float** dev_out, cudaStream_t st,
+                             BatchStats* bs) {
+    const int64_t npad = ((n + 3) & ~int64_t(3)) + 4;
+    float* d = nullptr;
+    ISY_CK(cudaMalloc(&d, npad * sizeof(float)));
+    ISY_CK(cudaMemsetAsync(d, 0, npad * sizeof(float), st));
+    ISY_CK(cudaMemcpyAsync(d, src, n * sizeof(float),
+                           src_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (bs && !src_is_device) bs->h2d_bytes += n * (int64_t)sizeof(float);
+    *dev_out = d;
+    return Status{};
+}
+
+void Engine::free_series(float* p) { cudaFree(p); }
+
+Status Engine::check_finite(const float* dev, int64_t n, cudaStream_t st, bool* finite) {
+    ISY_CK(cudaMemsetAsync(dflag_, 0, sizeof(int), st));
+    ISY_CK(launch_nonfinite_scan(dev, n, dflag_, st));
+    int h = 0;
+    ISY_CK(cudaMemcpyAsync(&h, dflag_, sizeof(int), cudaMemcpyDeviceToHost, st));
+    ISY_CK(cudaStreamSynchronize(st));
+    *finite = (h == 0);
+    return Status{};
+}
+
+}  // namespace isy

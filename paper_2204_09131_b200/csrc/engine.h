@@ -1,0 +1,171 @@
+// Internal interfaces of libisycos (not part of the C ABI; see include/isycos.h).
+//
+// Layering:
+//   capi.cpp     validation, pointer classification, error codes  (C ABI)
+//   search.cpp   batched SYCOS_TD / SYCOS_BU / noise / chunk driver (host state machines)
+//   engine.cu    per-device context: digamma tables, buffers, batch evaluation, profiling
+//   ksg_kernels.cu  the sm_100a KSG window kernels (a2-a6 of SURVEY §8(a))
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "isycos.h"
+
+namespace isy {
+
+// ---------------------------------------------------------------- device-visible records
+struct PairPtrs {            // device pointers of one series pair (16-B aligned, padded to 4 floats)
+    const float* x;
+    const float* y;
+};
+
+struct KsgWin {              // one window of a batch (24 B)
+    int64_t t0;
+    int32_t w;
+    int32_t pair;            // index into the batch's PairPtrs table
+    int64_t dbg_off;         // offset of this window's points in the debug arrays, or -1
+};
+
+struct KsgItem {             // one (window, i-tile) work item of the tile kernel
+    int32_t win;
+    int32_t i0;
+};
+
+struct KsgRec {              // per-window result (48 B)
+    double mi, h, nmi;
+    long long s_psi, s_log;
+    int32_t zero_eps;
+    int32_t pad;
+};
+
+struct KsgAcc {              // self-cleaning accumulator of a multi-tile window
+    unsigned long long s_psi, s_log;
+    unsigned int zero, done;
+    unsigned long long pad;
+};
+
+struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
+    const PairPtrs* pairs;
+    const KsgWin* wins;
+    const double* psi;       // psi[m], m = 0..w_max
+    const long long* psiq;   // q(psi[m]) = rint(psi[m] * 2^32)
+    KsgAcc* acc;
+    KsgRec* out;
+    float* dbg_eps;
+    int32_t* dbg_nx;
+    int32_t* dbg_ny;
+    int32_t k;
+    int32_t variant;
+};
+
+// Size classes.  Small: one warp per window, R = points per lane.
+constexpr int kSmallWarps = 8;           // warps per CTA of the small kernel
+constexpr int kTileThreads = 256;        // threads per CTA of the tile kernel
+constexpr int kTileJ = 4096;             // j-tile (points) staged per cp.async.bulk round
+int small_class_R(int w);                // 1,2,4,8 for w <= 256; 0 => tile kernel
+int tile_R(int w);                       // points per thread of the tile kernel
+
+// Launchers (ksg_kernels.cu).  Return cudaGetLastError().
+cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
+cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st);
+cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, cudaStream_t st);
+cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st);
+
+// ---------------------------------------------------------------- errors
+struct Status {
+    int code = ISYCOS_OK;
+    std::string msg;
+    bool ok() const { return code == ISYCOS_OK; }
+};
+Status make_err(int code, const std::string& msg);
+Status cuda_err(cudaError_t e, const char* what);
+void set_last_error(const Status& s);
+
+// ---------------------------------------------------------------- engine
+struct DebugOut {
+    float* eps = nullptr;     // device pointers (engine writes directly), or nullptr
+    int32_t* nx = nullptr;
+    int32_t* ny = nullptr;
+};
+
+struct BatchStats {
+    int64_t windows = 0, point_pairs = 0, launches = 0, ksg_launches = 0, rounds = 0;
+    double kernel_ms = 0.0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
+    void add_to(isycos_kernel_stats* s) const;
+};
+
+class Engine;
+Engine* engine_for_current_device(Status* st);
+void release_engine_for_current_device();
+
+class Engine {
+public:
+    // Evaluate windows of a batch.  pairs: host array of device pointer pairs.  Results are
+    // written to recs_host (pinned or pageable host memory) or, if recs_dev != nullptr, left in
+    // device memory at recs_dev (caller-owned device buffer of n KsgRec).
+    Status evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
+                    int32_t variant, KsgRec* recs_host, const DebugOut& dbg, cudaStream_t st,
+                    bool profile, BatchStats* bs);
+
+    // Device copy of a series (padded to a multiple of 4 floats, 16-B aligned).
+    Status upload_series(const float* src, int64_t n, bool src_is_device, float** dev_out, cudaStream_t st,
+                         BatchStats* bs);
+    Status check_finite(const float* dev, int64_t n, cudaStream_t st, bool* finite);
+    void free_series(float* p);
+
+    cudaStream_t own_stream() const { return stream_; }
+    int device() const { return dev_; }
+    ~Engine();
+
+    Status init(int dev);
+
+private:
+    Status ensure_psi(int64_t w_max, cudaStream_t st);
+    Status ensure_capacity(int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists);
+
+    int dev_ = -1;
+    cudaStream_t stream_ = nullptr;
+    // digamma tables
+    double* psi_ = nullptr;
+    long long* psiq_ = nullptr;
+    int64_t psi_max_ = 0;
+    // batch buffers (device) and pinned staging (host)
+    KsgAcc* acc_ = nullptr;
+    int64_t acc_cap_ = 0;
+    char* dstage_ = nullptr;       // packed [pairs | wins | lists | items]
+    int64_t dstage_cap_ = 0;
+    char* hstage_ = nullptr;       // pinned mirror of dstage_
+    int64_t hstage_cap_ = 0;
+    KsgRec* drec_ = nullptr;
+    int64_t drec_cap_ = 0;
+    KsgRec* hrec_ = nullptr;       // pinned
+    int64_t hrec_cap_ = 0;
+    int* dflag_ = nullptr;
+    std::vector<cudaEvent_t> events_;
+};
+
+// ---------------------------------------------------------------- search driver
+struct SearchParams {
+    int32_t k = 4, variant = 0, method = 3;
+    int64_t s_min = 64, s_max = 512;
+    std::vector<int64_t> sizes;
+    bool noise = true;
+    double tau_ratio = 0.25;
+    int32_t p = 3;
+    double sigma = 0.2;
+    int64_t delta_td = 0, delta_bu = 0;
+    int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 256;
+    uint64_t seed = 0;
+    bool profile = false;
+};
+
+Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std::vector<int32_t>& pair_ids,
+                  int64_t n, const SearchParams& P, cudaStream_t st, std::vector<isycos_result_window>* out,
+                  isycos_search_stats* stats);
+
+}  // namespace isy

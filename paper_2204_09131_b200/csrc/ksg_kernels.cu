@@ -1,0 +1,502 @@
+// sm_100a KSG window kernels — steps a2-a6 of SURVEY §8(a).
+//
+// Per window W = [t0, t1) of w points of a series pair (Def 4.2):
+//   a2  stage x[t0:t1], y[t0:t1] into shared memory (cp.async.bulk + mbarrier for the tile
+//       kernel; coalesced loads for the warp-per-window kernel), 16-B aligned superset with
+//       +inf sentinels in the pad slots so every inner loop reads float4 (LDS.128 broadcast)
+//   a3  k-NN radius: eps_i = (k+1)-th smallest of { d_ij : all j in W } including d_ii = 0,
+//       i.e. the k-th smallest over j != i  (multiset order statistic; Kraskov alg. 1)
+//       kept per point in registers (sorted top-(k+1), min/max insertion network)
+//   a4  marginal counts n_x(i) = #{j : |fl(x_i - x_j)| < eps_i} - [eps_i > 0]  (strict; self
+//       removed), via the sign bit of fl(|dx| - eps) — exact for finite floats without FTZ
+//   a5  per-point digamma terms as int64 fixed point (table q(psi[m]), Q = 2^32) and
+//       q(LN(2 eps_i)) for the entropy; warp shuffle + CTA + int64 atomics (exact, order free)
+//   a6  canonical fp64 finalize -> I (KSG-1), H (KL), normalized I (Eq. 12)
+//
+// No tensor cores: this is compare/count ALU work, not a contraction (north star).
+// Compile with -fmad=false is NOT required: every fp64 op below is an explicit _rn
+// intrinsic, and the fp32 inner loops contain no multiply-add.
+
+#include <cmath>
+
+#include "engine.h"
+
+namespace isy {
+
+int small_class_R(int w) {
+    if (w <= 32) return 1;
+    if (w <= 64) return 2;
+    if (w <= 128) return 4;
+    if (w <= 256) return 8;
+    return 0;
+}
+
+int tile_R(int w) { return w <= 2 * kTileThreads ? 2 : 4; }
+
+namespace {
+
+constexpr float kInf = __builtin_huge_valf();
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ------------------------------------------------------------------ mbarrier / bulk copy (TMA engine)
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+// ------------------------------------------------------------------ canonical fp64 numerics (§8(c).3)
+__device__ __forceinline__ long long q32(double v) { return __double2ll_rn(__dmul_rn(v, 4294967296.0)); }
+
+// LN(v), v > 0 normal: frexp -> [sqrt(1/2), sqrt(2)) -> 2 atanh(s) series to s^19, fixed op order.
+__device__ double canon_ln(double v) {
+    const long long bits = __double_as_longlong(v);
+    int e = (int)((bits >> 52) & 0x7FF) - 1022;
+    double m = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FE0000000000000LL);  // [0.5, 1)
+    if (m < 0.70710678118654752440) {
+        m = __dmul_rn(m, 2.0);
+        e -= 1;
+    }
+    const double s = __ddiv_rn(__dsub_rn(m, 1.0), __dadd_rn(m, 1.0));
+    const double z = __dmul_rn(s, s);
+    double p = __ddiv_rn(1.0, 19.0);
+#pragma unroll
+    for (int j = 8; j >= 1; --j) p = __dadd_rn(__dmul_rn(p, z), __ddiv_rn(1.0, (double)(2 * j + 1)));
+    const double two_s = __dmul_rn(2.0, s);
+    const double tail = __dmul_rn(__dmul_rn(two_s, z), p);
+    const double r = __dadd_rn(two_s, tail);
+    return __dadd_rn(__dmul_rn((double)e, 0.69314718055994530942), r);
+}
+
+__device__ void finalize(const KsgLaunch& L, int w, long long s_psi, long long s_log, int zero, KsgRec* o) {
+    const double kQ = 2.3283064365386962890625e-10;  // 2^-32
+    const double dw = (double)w;
+    double a;
+    if (L.variant == 0) {
+        a = __dadd_rn(L.psi[L.k], L.psi[w]);
+    } else {
+        a = __dsub_rn(L.psi[L.k], __ddiv_rn(1.0, (double)L.k));
+        a = __dadd_rn(a, L.psi[w]);
+    }
+    const double mean_q = __ddiv_rn(__dmul_rn(__ll2double_rn(s_psi), kQ), dw);
+    const double mi = __dsub_rn(a, mean_q);
+    double h;
+    if (zero > 0) {
+        h = -__builtin_huge_val();
+    } else {
+        const double a2 = __dsub_rn(L.psi[w], L.psi[L.k]);
+        const double m2 = __ddiv_rn(__dmul_rn(__ll2double_rn(s_log), kQ), dw);
+        h = __dadd_rn(a2, __dmul_rn(2.0, m2));
+    }
+    double nmi;
+    if (zero > 0 || !(h > 1e-6)) {
+        nmi = mi > 1e-6 ? 1.0 : 0.0;
+    } else {
+        nmi = __ddiv_rn(mi, h);
+        nmi = nmi < 0.0 ? 0.0 : (nmi > 1.0 ? 1.0 : nmi);
+    }
+    o->mi = mi;
+    o->h = h;
+    o->nmi = nmi;
+    o->s_psi = s_psi;
+    o->s_log = s_log;
+    o->zero_eps = zero;
+    o->pad = 0;
+}
+
+// ------------------------------------------------------------------ inner loops
+// Sorted ascending top list r[0..K1-1]; insert d (exact: r becomes the K1 smallest of r U {d}).
+template <int K1>
+__device__ __forceinline__ void topk_insert(float (&r)[K1], float d) {
+#pragma unroll
+    for (int m = K1 - 1; m >= 1; --m) r[m] = fminf(r[m], fmaxf(r[m - 1], d));
+    r[0] = fminf(r[0], d);
+}
+
+// a3: four candidates j (one float4 of x and of y, broadcast to the warp) against R points.
+template <int K1, int R>
+__device__ __forceinline__ void knn_step(const float (&xi)[R], const float (&yi)[R], float (&rk)[R][K1],
+                                         const float4 X, const float4 Y) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const float d0 = fmaxf(fabsf(xi[r] - X.x), fabsf(yi[r] - Y.x));
+        const float d1 = fmaxf(fabsf(xi[r] - X.y), fabsf(yi[r] - Y.y));
+        const float d2 = fmaxf(fabsf(xi[r] - X.z), fabsf(yi[r] - Y.z));
+        const float d3 = fmaxf(fabsf(xi[r] - X.w), fabsf(yi[r] - Y.w));
+        const float m = fminf(fminf(d0, d1), fminf(d2, d3));
+        if (m < rk[r][K1 - 1]) {
+            if (d0 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d0);
+            if (d1 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d1);
+            if (d2 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d2);
+            if (d3 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d3);
+        }
+    }
+}
+
+// a4: sign bit of fl(|fl(x_i - x_j)| - eps_i) is 1 iff |fl(x_i - x_j)| < eps_i (finite, no FTZ).
+__device__ __forceinline__ unsigned lt_bit(float xi, float xj, float eps) {
+    return __float_as_uint(fabsf(xi - xj) - eps) >> 31;
+}
+
+template <int R>
+__device__ __forceinline__ void count_step(const float (&xi)[R], const float (&yi)[R], const float (&eps)[R],
+                                           unsigned (&cx)[R], unsigned (&cy)[R], const float4 X, const float4 Y) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        cx[r] += lt_bit(xi[r], X.x, eps[r]) + lt_bit(xi[r], X.y, eps[r]) + lt_bit(xi[r], X.z, eps[r]) +
+                 lt_bit(xi[r], X.w, eps[r]);
+        cy[r] += lt_bit(yi[r], Y.x, eps[r]) + lt_bit(yi[r], Y.y, eps[r]) + lt_bit(yi[r], Y.z, eps[r]) +
+                 lt_bit(yi[r], Y.w, eps[r]);
+    }
+}
+
+// a5: per-point terms of the points this thread owns (i = i_first + stride * r).
+template <int R>
+__device__ __forceinline__ void point_terms(const KsgLaunch& L, int w, int64_t dbg_off, int i_first, int stride,
+                                            const float (&eps)[R], const unsigned (&cx)[R],
+                                            const unsigned (&cy)[R], long long& sp, long long& sl, int& z) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = i_first + stride * r;
+        if (i < w) {
+            const int pos = eps[r] > 0.0f ? 1 : 0;
+            const int nx = (int)cx[r] - pos;
+            const int ny = (int)cy[r] - pos;
+            sp += L.psiq[nx + 1] + L.psiq[ny + 1];
+            if (pos)
+                sl += q32(canon_ln(__dmul_rn(2.0, (double)eps[r])));
+            else
+                z += 1;
+            if (dbg_off >= 0) {
+                if (L.dbg_eps) L.dbg_eps[dbg_off + i] = eps[r];
+                if (L.dbg_nx) L.dbg_nx[dbg_off + i] = nx;
+                if (L.dbg_ny) L.dbg_ny[dbg_off + i] = ny;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void warp_sum(long long& a, long long& b, int& c) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+        c += __shfl_down_sync(0xffffffffu, c, off);
+    }
+}
+
+// ------------------------------------------------------------------ small windows: one warp per window
+template <int K1, int R>
+__global__ void __launch_bounds__(kSmallWarps * 32)
+    ksg_small_kernel(const KsgLaunch L, const int32_t* __restrict__ list, int32_t n) {
+    constexpr int CAP = 32 * R + 4;
+    __shared__ __align__(16) float sbuf[kSmallWarps][2][CAP];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int idx = blockIdx.x * kSmallWarps + warp;
+    if (idx >= n) return;  // warp-uniform
+    const int q = list[idx];
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    const int wpad = (w + 3) & ~3;
+    const float* gx = L.pairs[W.pair].x + W.t0;
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    float* sx = sbuf[warp][0];
+    float* sy = sbuf[warp][1];
+    for (int j = lane; j < wpad; j += 32) {  // a2: coalesced loads, +inf sentinels past w
+        sx[j] = j < w ? gx[j] : kInf;
+        sy[j] = j < w ? gy[j] : kInf;
+    }
+    __syncwarp();
+    float xi[R], yi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        xi[r] = i < w ? sx[i] : 0.0f;
+        yi[r] = i < w ? sy[i] : 0.0f;
+    }
+    float rk[R][K1];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < K1; ++m) rk[r][m] = kInf;
+    const float4* sx4 = reinterpret_cast<const float4*>(sx);
+    const float4* sy4 = reinterpret_cast<const float4*>(sy);
+    const int ng = wpad >> 2;
+    for (int g = 0; g < ng; ++g) knn_step<K1, R>(xi, yi, rk, sx4[g], sy4[g]);
+    float eps[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) eps[r] = rk[r][K1 - 1];
+    unsigned cx[R], cy[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
+    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g]);
+    long long sp = 0, sl = 0;
+    int z = 0;
+    point_terms<R>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
+    warp_sum(sp, sl, z);
+    if (lane == 0) finalize(L, w, sp, sl, z, &L.out[q]);
+}
+
+// ------------------------------------------------------------------ large windows: (window, i-tile) per CTA
+// a2 via cp.async.bulk of the 16-B aligned superset [a & ~3, ceil4(a + len)) into SMEM, completion on an
+// mbarrier; series buffers are 16-B aligned and padded to a multiple of 4 floats so the superset is in bounds.
+__device__ __forceinline__ int stage_tile(const float* gx, const float* gy, int64_t a, int len, float* sx,
+                                          float* sy, uint32_t bar, uint32_t& phase) {
+    const int64_t a0 = a & ~int64_t(3);
+    const int64_t a1 = (a + len + 3) & ~int64_t(3);
+    const int nfl = (int)(a1 - a0);
+    const int off = (int)(a - a0);
+    if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bytes = (uint32_t)nfl * 4u;
+        mbar_arrive_expect_tx(bar, 2u * bytes);
+        bulk_g2s(smem_u32(sx), gx + a0, bytes, bar);
+        bulk_g2s(smem_u32(sy), gy + a0, bytes, bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const int t = threadIdx.x;
+    if (t < off) {
+        sx[t] = kInf;
+        sy[t] = kInf;
+    }
+    const int tail0 = off + len;
+    if (t < nfl - tail0) {
+        sx[tail0 + t] = kInf;
+        sy[tail0 + t] = kInf;
+    }
+    __syncthreads();
+    return nfl >> 2;
+}
+
+template <int K1, int R>
+__global__ void __launch_bounds__(kTileThreads)
+    ksg_tile_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items) {
+    extern __shared__ __align__(16) float dyn[];
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ long long red_sp[kTileThreads / 32], red_sl[kTileThreads / 32];
+    __shared__ int red_z[kTileThreads / 32];
+
+    const KsgItem it = items[blockIdx.x];
+    const int q = it.win;
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    const float* gx = L.pairs[W.pair].x;
+    const float* gy = L.pairs[W.pair].y;
+    const int64_t t0 = W.t0;
+    float* sx = dyn;
+    float* sy = dyn + (kTileJ + 8);
+    const uint32_t bar = smem_u32(&mbar);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+
+    float xi[R], yi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = it.i0 + threadIdx.x + kTileThreads * r;
+        xi[r] = i < w ? gx[t0 + i] : 0.0f;
+        yi[r] = i < w ? gy[t0 + i] : 0.0f;
+    }
+    float rk[R][K1];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < K1; ++m) rk[r][m] = kInf;
+
+    const int nj = (w + kTileJ - 1) / kTileJ;
+    int ng = 0;
+    for (int jt = 0; jt < nj; ++jt) {
+        const int j0 = jt * kTileJ;
+        ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
+        const float4* sx4 = reinterpret_cast<const float4*>(sx);
+        const float4* sy4 = reinterpret_cast<const float4*>(sy);
+        for (int g = 0; g < ng; ++g) knn_step<K1, R>(xi, yi, rk, sx4[g], sy4[g]);
+        if (nj > 1) __syncthreads();
+    }
+    float eps[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) eps[r] = rk[r][K1 - 1];
+    unsigned cx[R], cy[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
+    for (int jt = 0; jt < nj; ++jt) {
+        if (nj > 1) {
+            const int j0 = jt * kTileJ;
+            ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
+        }
+        const float4* sx4 = reinterpret_cast<const float4*>(sx);
+        const float4* sy4 = reinterpret_cast<const float4*>(sy);
+        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g]);
+        if (nj > 1) __syncthreads();
+    }
+
+    long long sp = 0, sl = 0;
+    int z = 0;
+    point_terms<R>(L, w, W.dbg_off, it.i0 + threadIdx.x, kTileThreads, eps, cx, cy, sp, sl, z);
+    warp_sum(sp, sl, z);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red_sp[warp] = sp;
+        red_sl[warp] = sl;
+        red_z[warp] = z;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int v = 1; v < kTileThreads / 32; ++v) {
+            sp += red_sp[v];
+            sl += red_sl[v];
+            z += red_z[v];
+        }
+        const int ntiles = (w + kTileThreads * R - 1) / (kTileThreads * R);
+        if (ntiles == 1) {
+            finalize(L, w, sp, sl, z, &L.out[q]);
+        } else {
+            KsgAcc* A = &L.acc[q];
+            atomicAdd(&A->s_psi, (unsigned long long)sp);
+            atomicAdd(&A->s_log, (unsigned long long)sl);
+            atomicAdd(&A->zero, (unsigned)z);
+            __threadfence();
+            const unsigned ticket = atomicAdd(&A->done, 1u);
+            if (ticket == (unsigned)(ntiles - 1)) {  // last tile of the window: finalize + reset
+                __threadfence();
+                const long long tp = (long long)atomicExch(&A->s_psi, 0ull);
+                const long long tl = (long long)atomicExch(&A->s_log, 0ull);
+                const int tz = (int)atomicExch(&A->zero, 0u);
+                atomicExch(&A->done, 0u);
+                finalize(L, w, tp, tl, tz, &L.out[q]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ digamma tables, input validation
+__global__ void inv_kernel(double* inv, int64_t m_max) {
+    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (m >= 1 && m <= m_max) inv[m] = __ddiv_rn(1.0, (double)m);
+}
+
+// psi(1) = -gamma; psi(m+1) = psi(m) + 1/m, strictly sequential (the canonical definition).
+__global__ void psi_scan_kernel(double* psi, const double* __restrict__ inv, int64_t m_max) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    psi[0] = __longlong_as_double(0x7FF8000000000000LL);
+    double v = -0.57721566490153286061;
+    psi[1] = v;
+    for (int64_t m = 1; m < m_max; ++m) {
+        v = __dadd_rn(v, inv[m]);
+        psi[m + 1] = v;
+    }
+}
+
+__global__ void psiq_kernel(const double* psi, long long* psiq, int64_t m_max) {
+    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (m == 0) psiq[0] = 0;
+    if (m >= 1 && m <= m_max) psiq[m] = q32(psi[m]);
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ p, int64_t n, int* flag) {
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(p[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ------------------------------------------------------------------ dispatch over (k, R)
+template <int K1>
+cudaError_t small_k(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
+    const dim3 grid((n + kSmallWarps - 1) / kSmallWarps), block(kSmallWarps * 32);
+    switch (R) {
+        case 1: ksg_small_kernel<K1, 1><<<grid, block, 0, st>>>(L, list, n); break;
+        case 2: ksg_small_kernel<K1, 2><<<grid, block, 0, st>>>(L, list, n); break;
+        case 4: ksg_small_kernel<K1, 4><<<grid, block, 0, st>>>(L, list, n); break;
+        case 8: ksg_small_kernel<K1, 8><<<grid, block, 0, st>>>(L, list, n); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+template <int K1>
+cudaError_t tile_k(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, cudaStream_t st) {
+    const size_t smem = 2 * (kTileJ + 8) * sizeof(float);
+    switch (R) {
+        case 2: ksg_tile_kernel<K1, 2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
+        case 4: ksg_tile_kernel<K1, 4><<<n, kTileThreads, smem, st>>>(L, items, n); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+#define ISY_K_CASES(FN, ...)                   \
+    switch (L.k) {                             \
+        case 1: return FN<2>(__VA_ARGS__);     \
+        case 2: return FN<3>(__VA_ARGS__);     \
+        case 3: return FN<4>(__VA_ARGS__);     \
+        case 4: return FN<5>(__VA_ARGS__);     \
+        case 5: return FN<6>(__VA_ARGS__);     \
+        case 6: return FN<7>(__VA_ARGS__);     \
+        case 7: return FN<8>(__VA_ARGS__);     \
+        case 8: return FN<9>(__VA_ARGS__);     \
+        case 9: return FN<10>(__VA_ARGS__);    \
+        case 10: return FN<11>(__VA_ARGS__);   \
+        case 11: return FN<12>(__VA_ARGS__);   \
+        case 12: return FN<13>(__VA_ARGS__);   \
+        case 13: return FN<14>(__VA_ARGS__);   \
+        case 14: return FN<15>(__VA_ARGS__);   \
+        case 15: return FN<16>(__VA_ARGS__);   \
+        case 16: return FN<17>(__VA_ARGS__);   \
+        default: return cudaErrorInvalidValue; \
+    }
+
+cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    ISY_K_CASES(small_k, L, list, n, R, st)
+}
+
+cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st) {
+    if (n_items <= 0) return cudaSuccess;
+    ISY_K_CASES(tile_k, L, items, n_items, R, st)
+}
+
+cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, cudaStream_t st) {
+    const int64_t blocks = (m_max + 1 + 255) / 256;
+    inv_kernel<<<(unsigned)blocks, 256, 0, st>>>(inv, m_max);
+    psi_scan_kernel<<<1, 32, 0, st>>>(psi, inv, m_max);
+    psiq_kernel<<<(unsigned)blocks, 256, 0, st>>>(psi, psiq, m_max);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    nonfinite_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, n, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace isy

@@ -1,0 +1,634 @@
+// Batched search driver: SYCOS_TD (Alg. 1), SYCOS_BU (Alg. 2), MI-based noise
+// pruning (Def 6.2, §6.2, §6.3), overlapping chunks (Alg. 4 line 14).
+//
+// SURVEY §8(a) a1 + a7.  The sequential algorithms are re-expressed as resumable state machines that
+// never compute MI themselves: they ask a per-pair window cache, and every miss becomes a request.
+// Each round the driver advances every job as far as the cache allows, then evaluates all pending
+// windows of all jobs in ONE GPU batch (Engine::evaluate).  Two kinds of speculation keep batches
+// large:
+//   TD  at the start of each layer, every window of the layer's delta-grid (plus the noise
+//       sub-windows) is requested at once; the layer is then replayed exactly (rounds = layers).
+//   BU  a climb is a pure function of its start lo (its LAHC stream is keyed by (seed, pair, lo)), so
+//       the climbs at lo, lo + s_min, lo + 2 s_min, ... (the chain if nothing is accepted) run in
+//       lockstep; when the head finishes the chain advances, and an accept re-anchors the chain.
+// Decisions use only canonical, bit-reproducible records, so the result set and the algorithm-level
+// counters equal the sequential oracle's exactly (tests/test_gpu_search.py).
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <unordered_map>
+#include <vector>
+
+#include "engine.h"
+
+namespace isy {
+namespace {
+
+struct Eval {
+    double mi, h, nmi;
+};
+
+struct Entry {
+    Eval e{0, 0, 0};
+    bool ready = false;
+    bool consumed = false;
+};
+
+inline uint64_t wkey(int64_t t0, int64_t t1) { return ((uint64_t)t0 << 20) | (uint64_t)(t1 - t0); }
+inline int64_t key_t0(uint64_t k) { return (int64_t)(k >> 20); }
+inline int64_t key_w(uint64_t k) { return (int64_t)(k & ((1u << 20) - 1)); }
+
+struct PairCache {
+    std::unordered_map<uint64_t, Entry> map;
+    std::vector<uint64_t> pending;
+};
+
+struct AlgStats {
+    int64_t td_windows = 0, td_noise_checks = 0, td_skips = 0, td_accepted = 0;
+    int64_t bu_climbs = 0, bu_iterations = 0, bu_neighbors = 0, bu_noise_checks = 0, bu_prunes = 0,
+            bu_accepted = 0;
+    void add(const AlgStats& o) {
+        td_windows += o.td_windows;
+        td_noise_checks += o.td_noise_checks;
+        td_skips += o.td_skips;
+        td_accepted += o.td_accepted;
+        bu_climbs += o.bu_climbs;
+        bu_iterations += o.bu_iterations;
+        bu_neighbors += o.bu_neighbors;
+        bu_noise_checks += o.bu_noise_checks;
+        bu_prunes += o.bu_prunes;
+        bu_accepted += o.bu_accepted;
+    }
+};
+
+// Window cache access for one pair.  get(): the record if evaluated, else nullptr (and the window is
+// queued for the next batch).  Accesses are recorded in `touched` and marked consumed only when the
+// owning step commits, so speculative work never enters the algorithm-level counters.
+struct View {
+    PairCache* c;
+    std::vector<uint64_t>* touched;
+    const Eval* get(int64_t t0, int64_t t1) {
+        const uint64_t k = wkey(t0, t1);
+        auto r = c->map.try_emplace(k);
+        if (r.second) {
+            c->pending.push_back(k);
+            return nullptr;
+        }
+        if (!r.first->second.ready) return nullptr;
+        touched->push_back(k);
+        return &r.first->second.e;
+    }
+    void want(int64_t t0, int64_t t1) {
+        const uint64_t k = wkey(t0, t1);
+        auto r = c->map.try_emplace(k);
+        if (r.second) c->pending.push_back(k);
+    }
+};
+
+void commit_touched(PairCache* c, const std::vector<uint64_t>& t) {
+    for (uint64_t k : t) c->map[k].consumed = true;
+}
+
+// ------------------------------------------------------------------ SYCOS_TD job
+struct TdJob {
+    const SearchParams* P;
+    PairCache* cache;
+    int32_t pair_id;
+    int64_t lo, hi;
+    std::vector<int64_t> sched;
+    size_t layer = 0;
+    bool layer_requested = false;
+    bool done = false;
+    std::vector<std::pair<int64_t, int64_t>> parts;
+    std::vector<isycos_result_window> results;
+    AlgStats stats;
+
+    void init() {
+        parts.assign(1, {lo, hi});
+        if (!P->sizes.empty()) {
+            sched = P->sizes;
+        } else {
+            sched.assign(1, P->s_max);  // S:348 halving s_max -> s_min
+            while (sched.back() > P->s_min) sched.push_back(std::max(P->s_min, sched.back() / 2));
+        }
+    }
+    int64_t delta(int64_t s) const { return P->delta_td > 0 ? P->delta_td : std::max<int64_t>(1, s / 4); }
+
+    void request_layer(int64_t s) {
+        std::vector<uint64_t> dummy;
+        View v{cache, &dummy};
+        const int64_t d = delta(s);
+        const bool nz = P->noise && d > P->k && s - d > P->k;
+        for (auto [a, b] : parts) {
+            if (b - a < s) continue;
+            for (int64_t t = a; t + s <= b; t += d) {
+                v.want(t, t + s);
+                if (nz && t > a) {
+                    v.want(t, t + s - d);
+                    v.want(t + s - d, t + s);
+                }
+            }
+        }
+    }
+
+    // One exact replay of the layer (Alg. 1 lines 3-15 over every partition).  Returns false if a
+    // window is missing (it is then queued); nothing is committed in that case.
+    bool replay_layer(int64_t s) {
+        const int64_t d = delta(s);
+        const double tau = P->tau_ratio * P->sigma;
+        AlgStats ls;
+        std::vector<isycos_result_window> lr;
+        std::vector<std::pair<int64_t, int64_t>> next;
+        std::vector<uint64_t> touched;
+        View v{cache, &touched};
+        for (auto [a, b] : parts) {
+            if (b - a < s) {
+                next.push_back({a, b});
+                continue;
+            }
+            int64_t t = a, pend = a;
+            int streak = 0;
+            bool shifted = false;
+            while (t + s <= b) {
+                ls.td_windows += 1;
+                const Eval* e = v.get(t, t + s);
+                if (!e) return false;
+                if (e->nmi >= P->sigma) {
+                    lr.push_back({pair_id, 1, t, t + s, e->mi, e->h, e->nmi});
+                    ls.td_accepted += 1;
+                    if (t > pend) next.push_back({pend, t});
+                    t = t + s;
+                    pend = t;
+                    streak = 0;
+                    shifted = false;
+                    continue;
+                }
+                if (P->noise && shifted && d > P->k && s - d > P->k) {
+                    ls.td_noise_checks += 1;
+                    const Eval* wo = v.get(t, t + s - d);
+                    const Eval* wd = v.get(t + s - d, t + s);
+                    if (!wo || !wd) return false;
+                    const bool noisy = wd->nmi < tau && e->mi < wo->mi && wo->mi > 0.0;
+                    streak = noisy ? streak + 1 : 0;
+                    if (streak >= P->p) {
+                        ls.td_skips += 1;
+                        t = t + s;
+                        streak = 0;
+                        shifted = false;
+                        continue;
+                    }
+                }
+                t = t + d;
+                shifted = true;
+            }
+            if (pend < b) next.push_back({pend, b});
+        }
+        // commit
+        stats.add(ls);
+        results.insert(results.end(), lr.begin(), lr.end());
+        commit_touched(cache, touched);
+        parts.clear();
+        for (auto& q : next)
+            if (q.second - q.first >= P->s_min) parts.push_back(q);
+        return true;
+    }
+
+    void advance() {
+        while (!done) {
+            if (layer >= sched.size()) {
+                done = true;
+                break;
+            }
+            const int64_t s = sched[layer];
+            if (!layer_requested) {
+                layer_requested = true;
+                request_layer(s);
+                if (!cache->pending.empty()) return;  // wait for the grid batch
+            }
+            if (!replay_layer(s)) return;
+            ++layer;
+            layer_requested = false;
+        }
+    }
+};
+
+// ------------------------------------------------------------------ SYCOS_BU: one climb (Alg. 2 lines 2-24)
+struct Rng {
+    uint64_t s;
+    uint64_t next() {
+        s += 0x9E3779B97F4A7C15ull;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+};
+
+struct Climb {
+    int64_t lo = 0;
+    int state = 0;  // 0 start, 1 iterate, 2 done
+    int64_t t0 = 0, t1 = 0;
+    double Iw = 0.0;
+    std::vector<double> L;
+    int idle = 0;
+    int streak[2] = {0, 0};
+    bool pruned[2] = {false, false};
+    Rng rng{0};
+    AlgStats st;
+    std::vector<uint64_t> touched;
+    bool accepted = false;
+    bool finished = false;
+    Eval fin{0, 0, 0};
+
+    // Advance as far as the cache allows.  Returns true when the climb is finished.
+    bool advance(const SearchParams& P, PairCache* cache, int32_t pair_id, int64_t hi) {
+        if (finished) return true;
+        View v{cache, &touched};
+        const int64_t smin = P.s_min, smax = P.s_max;
+        const int64_t d = P.delta_bu > 0 ? P.delta_bu : std::max<int64_t>(1, smin / 3);
+        const double tau = P.tau_ratio * P.sigma;
+        for (;;) {
+            if (state == 0) {
+                const Eval* e = v.get(lo, lo + smin);
+                if (!e) return false;
+                st.bu_climbs = 1;
+                t0 = lo;
+                t1 = lo + smin;
+                Iw = e->mi;
+                L.assign(P.h, Iw);
+                idle = 0;
+                rng.s = P.seed ^ ((uint64_t)(uint32_t)pair_id * 0x9E3779B97F4A7C15ull) ^
+                        ((uint64_t)lo * 0xD1B54A32D192ED03ull);
+                state = 1;
+            }
+            if (state == 1) {
+                if (idle > P.t_max_idle) {
+                    state = 2;
+                    continue;
+                }
+                // gather the iteration's windows: N1 (Def 5.2-5.3) in (t0,t1) order + noise windows
+                int64_t c0s[8], c1s[8];
+                int nc = 0;
+                for (int da = -1; da <= 1; ++da)
+                    for (int db = -1; db <= 1; ++db) {
+                        if (da == 0 && db == 0) continue;
+                        if (da == -1 && pruned[0]) continue;
+                        if (db == 1 && pruned[1]) continue;
+                        const int64_t c0 = t0 + da * d, c1 = t1 + db * d;
+                        if (c0 < lo || c1 > hi) continue;
+                        const int64_t sz = c1 - c0;
+                        if (sz < smin || sz > smax) continue;
+                        c0s[nc] = c0;
+                        c1s[nc] = c1;
+                        ++nc;
+                    }
+                if (nc == 0) {
+                    state = 2;
+                    continue;
+                }
+                bool applicable[2] = {false, false};
+                int64_t e0[2], e1[2], m0[2], m1[2];
+                const bool nz = P.noise && d > P.k;
+                for (int dir = 0; dir < 2 && nz; ++dir) {
+                    if (pruned[dir]) continue;
+                    if (dir == 0) {
+                        e0[0] = t0 - d; e1[0] = t0; m0[0] = t0 - d; m1[0] = t1;
+                    } else {
+                        e0[1] = t1; e1[1] = t1 + d; m0[1] = t0; m1[1] = t1 + d;
+                    }
+                    applicable[dir] = !(e0[dir] < lo || e1[dir] > hi || m1[dir] - m0[dir] > smax);
+                }
+                const size_t mark = touched.size();
+                bool missing = false;
+                const Eval* ce[8];
+                for (int i = 0; i < nc; ++i) {
+                    ce[i] = v.get(c0s[i], c1s[i]);
+                    missing |= (ce[i] == nullptr);
+                }
+                const Eval* ee[2] = {nullptr, nullptr};
+                const Eval* me[2] = {nullptr, nullptr};
+                for (int dir = 0; dir < 2; ++dir) {
+                    if (!applicable[dir]) continue;
+                    ee[dir] = v.get(e0[dir], e1[dir]);
+                    me[dir] = v.get(m0[dir], m1[dir]);
+                    missing |= (ee[dir] == nullptr) | (me[dir] == nullptr);
+                }
+                if (missing) {
+                    touched.resize(mark);
+                    return false;
+                }
+                // the iteration, exactly as Alg. 2 lines 7-21
+                int best = 0;
+                for (int i = 0; i < nc; ++i) {
+                    st.bu_neighbors += 1;
+                    if (i > 0 && ce[i]->mi > ce[best]->mi) best = i;
+                }
+                st.bu_iterations += 1;
+                for (int dir = 0; dir < 2; ++dir) {
+                    if (!applicable[dir]) continue;
+                    st.bu_noise_checks += 1;
+                    const bool noisy = ee[dir]->nmi < tau && me[dir]->mi < Iw && Iw > 0.0;
+                    streak[dir] = noisy ? streak[dir] + 1 : 0;
+                    if (streak[dir] >= P.p) {
+                        pruned[dir] = true;
+                        st.bu_prunes += 1;
+                    }
+                }
+                const int r = (int)((rng.next() >> 32) % (uint64_t)P.h);
+                const double Ih = L[r];
+                const double bI = ce[best]->mi;
+                if (bI > Ih || bI > Iw) {
+                    t0 = c0s[best];
+                    t1 = c1s[best];
+                    Iw = bI;
+                    idle = 0;
+                } else {
+                    idle += 1;
+                }
+                if (Iw > Ih) L[r] = Iw;
+                continue;
+            }
+            // state 2: final acceptance test (Alg. 2 line 23)
+            const Eval* e = v.get(t0, t1);
+            if (!e) return false;
+            fin = *e;
+            accepted = fin.nmi >= P.sigma;
+            finished = true;
+            return true;
+        }
+    }
+};
+
+// ------------------------------------------------------------------ SYCOS_BU job: chain of climbs
+struct BuJob {
+    const SearchParams* P;
+    PairCache* cache;
+    int32_t pair_id;
+    int64_t lo_c, hi;
+    int64_t chain = 0;
+    bool done = false;
+    std::map<int64_t, Climb> climbs;
+    std::vector<isycos_result_window> results;
+    AlgStats stats;
+
+    void init() { chain = lo_c; }
+
+    void ensure_lookahead() {
+        const int la = P->lookahead > 0 ? P->lookahead : 256;
+        for (int j = 0; j < la; ++j) {
+            const int64_t l = chain + (int64_t)j * P->s_min;
+            if (l + P->s_min > hi) break;
+            auto r = climbs.try_emplace(l);
+            if (r.second) {
+                r.first->second.lo = l;
+                r.first->second.advance(*P, cache, pair_id, hi);
+            }
+        }
+    }
+
+    void advance() {
+        if (done) return;
+        for (auto& kv : climbs) kv.second.advance(*P, cache, pair_id, hi);
+        ensure_lookahead();
+        for (;;) {
+            if (chain + P->s_min > hi) {
+                done = true;
+                climbs.clear();
+                return;
+            }
+            auto it = climbs.find(chain);
+            if (it == climbs.end()) {
+                ensure_lookahead();
+                it = climbs.find(chain);
+            }
+            Climb& c = it->second;
+            if (!c.advance(*P, cache, pair_id, hi)) return;
+            // commit the head climb (Alg. 2 lines 23-24; restart on the remainder)
+            stats.add(c.st);
+            commit_touched(cache, c.touched);
+            int64_t next;
+            if (c.accepted) {
+                results.push_back({pair_id, 2, c.t0, c.t1, c.fin.mi, c.fin.h, c.fin.nmi});
+                stats.bu_accepted += 1;
+                next = std::max(c.t1, chain + P->s_min);
+            } else {
+                next = chain + P->s_min;
+            }
+            // drop climbs behind the chain and (after a re-anchor) those off the new grid
+            for (auto jt = climbs.begin(); jt != climbs.end();) {
+                const int64_t l = jt->first;
+                if (l < next || (l - next) % P->s_min != 0)
+                    jt = climbs.erase(jt);
+                else
+                    ++jt;
+            }
+            chain = next;
+            ensure_lookahead();
+        }
+    }
+};
+
+// ------------------------------------------------------------------ chunks + merge
+std::vector<std::pair<int64_t, int64_t>> chunks_of(int64_t n, int32_t n_p, int64_t s_max) {
+    std::vector<std::pair<int64_t, int64_t>> c;
+    const int64_t len = (n + n_p - 1) / n_p;
+    for (int32_t i = 0; i < n_p; ++i) {
+        const int64_t a = (int64_t)i * len;
+        if (a >= n) break;
+        c.push_back({std::max<int64_t>(0, a - s_max), std::min<int64_t>(n, a + len)});
+    }
+    return c;
+}
+
+// greedy by (nmi desc, mi desc, t0 asc, t1 asc), keep if disjoint from every kept window, sort by t0
+std::vector<isycos_result_window> merge_windows(std::vector<isycos_result_window> all) {
+    std::sort(all.begin(), all.end(), [](const isycos_result_window& a, const isycos_result_window& b) {
+        if (a.nmi != b.nmi) return a.nmi > b.nmi;
+        if (a.mi != b.mi) return a.mi > b.mi;
+        if (a.t0 != b.t0) return a.t0 < b.t0;
+        return a.t1 < b.t1;
+    });
+    std::vector<isycos_result_window> kept;
+    for (auto& r : all) {
+        bool clash = false;
+        for (auto& q : kept)
+            if (r.t0 < q.t1 && q.t0 < r.t1) {
+                clash = true;
+                break;
+            }
+        if (!clash) kept.push_back(r);
+    }
+    std::sort(kept.begin(), kept.end(),
+              [](const isycos_result_window& a, const isycos_result_window& b) { return a.t0 < b.t0; });
+    return kept;
+}
+
+struct PairWork {
+    int32_t slot = -1;  // index into the active PairPtrs table
+    int32_t pair_id = 0;
+    PairPtrs ptrs{};
+    PairCache cache;
+    std::vector<TdJob> td;
+    std::vector<BuJob> bu;
+    bool finished() const {
+        for (auto& j : td)
+            if (!j.done) return false;
+        for (auto& j : bu)
+            if (!j.done) return false;
+        return true;
+    }
+};
+
+}  // namespace
+
+Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std::vector<int32_t>& pair_ids,
+                  int64_t n, const SearchParams& P, cudaStream_t st, std::vector<isycos_result_window>* out,
+                  isycos_search_stats* stats) {
+    const int32_t n_pairs = (int32_t)pair_ptrs.size();
+    const auto plan = chunks_of(n, std::max(1, P.n_chunks), P.s_max);
+    const int max_active = 64;
+    AlgStats total;
+    BatchStats bs;
+    int64_t distinct_w = 0, distinct_pp = 0;
+    std::vector<isycos_result_window> all;
+    std::vector<std::unique_ptr<PairWork>> active;
+    int32_t next_pair = 0;
+    std::vector<KsgWin> batch;
+    std::vector<KsgRec> recs;
+    std::vector<std::pair<PairWork*, uint64_t>> owners;
+
+    for (;;) {
+        // admit pairs
+        while ((int)active.size() < max_active && next_pair < n_pairs) {
+            auto pw = std::make_unique<PairWork>();
+            pw->pair_id = pair_ids[next_pair];
+            pw->ptrs = pair_ptrs[next_pair];
+            for (auto [lo, hi] : plan) {
+                if (P.method & 1) {
+                    TdJob j;
+                    j.P = &P;
+                    j.cache = &pw->cache;
+                    j.pair_id = pw->pair_id;
+                    j.lo = lo;
+                    j.hi = hi;
+                    pw->td.push_back(std::move(j));
+                }
+                if (P.method & 2) {
+                    BuJob j;
+                    j.P = &P;
+                    j.cache = &pw->cache;
+                    j.pair_id = pw->pair_id;
+                    j.lo_c = lo;
+                    j.hi = hi;
+                    pw->bu.push_back(std::move(j));
+                }
+            }
+            for (auto& j : pw->td) {
+                j.cache = &pw->cache;
+                j.init();
+            }
+            for (auto& j : pw->bu) {
+                j.cache = &pw->cache;
+                j.init();
+            }
+            active.push_back(std::move(pw));
+            ++next_pair;
+        }
+        if (active.empty()) break;
+        // advance every job
+        for (auto& pw : active) {
+            for (auto& j : pw->td) j.advance();
+            for (auto& j : pw->bu) j.advance();
+        }
+        // retire finished pairs
+        for (size_t i = 0; i < active.size();) {
+            PairWork* pw = active[i].get();
+            if (pw->finished()) {
+                pw->cache.pending.clear();  // leftover speculative requests of discarded climbs
+                AlgStats ps;
+                for (int m = 1; m <= 2; ++m) {
+                    std::vector<isycos_result_window> per;
+                    if (m == 1)
+                        for (auto& j : pw->td) {
+                            per.insert(per.end(), j.results.begin(), j.results.end());
+                            ps.add(j.stats);
+                        }
+                    else
+                        for (auto& j : pw->bu) {
+                            per.insert(per.end(), j.results.begin(), j.results.end());
+                            ps.add(j.stats);
+                        }
+                    if (!(P.method & m)) continue;
+                    auto merged = merge_windows(per);
+                    all.insert(all.end(), merged.begin(), merged.end());
+                }
+                total.add(ps);
+                for (auto& kv : pw->cache.map)
+                    if (kv.second.consumed) {
+                        const int64_t w = key_w(kv.first);
+                        distinct_w += 1;
+                        distinct_pp += w * (w - 1);
+                    }
+                active.erase(active.begin() + i);
+            } else {
+                ++i;
+            }
+        }
+        // one batch of every pending window of every active pair
+        std::vector<PairPtrs> table;
+        batch.clear();
+        owners.clear();
+        for (auto& pw : active) {
+            if (pw->cache.pending.empty()) continue;
+            pw->slot = (int32_t)table.size();
+            table.push_back(pw->ptrs);
+            for (uint64_t k : pw->cache.pending) {
+                batch.push_back(KsgWin{key_t0(k), (int32_t)key_w(k), pw->slot, -1});
+                owners.push_back({pw.get(), k});
+            }
+            pw->cache.pending.clear();
+        }
+        if (batch.empty()) {
+            bool any_active = false;
+            for (auto& pw : active)
+                if (!pw->finished()) any_active = true;
+            if (any_active) return make_err(ISYCOS_E_CUDA, "search driver stalled (internal error)");
+            continue;
+        }
+        recs.resize(batch.size());
+        Status s = eng->evaluate(table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
+                                 P.variant, recs.data(), DebugOut{}, st, P.profile, &bs);
+        if (!s.ok()) return s;
+        for (size_t i = 0; i < batch.size(); ++i) {
+            Entry& e = owners[i].first->cache.map[owners[i].second];
+            e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
+            e.ready = true;
+        }
+    }
+    std::stable_sort(all.begin(), all.end(), [](const isycos_result_window& a, const isycos_result_window& b) {
+        if (a.pair != b.pair) return a.pair < b.pair;
+        if (a.method != b.method) return a.method < b.method;
+        return a.t0 < b.t0;
+    });
+    *out = std::move(all);
+    if (stats) {
+        stats->td_windows = total.td_windows;
+        stats->td_noise_checks = total.td_noise_checks;
+        stats->td_skips = total.td_skips;
+        stats->td_accepted = total.td_accepted;
+        stats->bu_climbs = total.bu_climbs;
+        stats->bu_iterations = total.bu_iterations;
+        stats->bu_neighbors = total.bu_neighbors;
+        stats->bu_noise_checks = total.bu_noise_checks;
+        stats->bu_prunes = total.bu_prunes;
+        stats->bu_accepted = total.bu_accepted;
+        stats->distinct_windows = distinct_w;
+        stats->distinct_pairs = distinct_pp;
+        bs.add_to(&stats->kernel);
+    }
+    return Status{};
+}
+
+}  // namespace isy
