@@ -83,6 +83,8 @@ typedef struct {
     int64_t rounds;        /* host<->device rounds (batches) */
     double kernel_ms;      /* sum of KSG kernel durations (CUDA events; ISYCOS_F_PROFILE only) */
     int64_t h2d_bytes, d2h_bytes;
+    double host_ms;        /* host time spent forming batches and replaying decisions (search) */
+    double wall_ms;        /* wall time of the call */
 } isycos_kernel_stats;
 
 /*

@@ -56,6 +56,8 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
     s->kernel_ms += kernel_ms;
     s->h2d_bytes += h2d_bytes;
     s->d2h_bytes += d2h_bytes;
+    s->host_ms += host_ms;
+    s->wall_ms += wall_ms;
 }
 
 // ---------------------------------------------------------------- engine registry (one per device)

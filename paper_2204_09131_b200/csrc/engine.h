@@ -96,6 +96,7 @@ struct BatchStats {
     int64_t windows = 0, point_pairs = 0, launches = 0, ksg_launches = 0, rounds = 0;
     double kernel_ms = 0.0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
+    double host_ms = 0.0, wall_ms = 0.0;
     void add_to(isycos_kernel_stats* s) const;
 };
 
@@ -160,6 +161,7 @@ struct SearchParams {
     double sigma = 0.2;
     int64_t delta_td = 0, delta_bu = 0;
     int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 256;
+    int64_t spec_cap_mult = 4;   // BU: speculative climbs pause beyond this many s_min
     uint64_t seed = 0;
     bool profile = false;
 };

@@ -15,6 +15,7 @@
 // counters equal the sequential oracle's exactly (tests/test_gpu_search.py).
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -242,8 +243,10 @@ struct Climb {
     bool finished = false;
     Eval fin{0, 0, 0};
 
-    // Advance as far as the cache allows.  Returns true when the climb is finished.
-    bool advance(const SearchParams& P, PairCache* cache, int32_t pair_id, int64_t hi) {
+    // Advance as far as the cache allows.  Returns true when the climb is finished.  A speculative
+    // climb whose window has grown beyond `cap` pauses (requests nothing) until it nears the chain head.
+    bool advance(const SearchParams& P, PairCache* cache, int32_t pair_id, int64_t hi,
+                 int64_t cap = INT64_MAX) {
         if (finished) return true;
         View v{cache, &touched};
         const int64_t smin = P.s_min, smax = P.s_max;
@@ -268,6 +271,7 @@ struct Climb {
                     state = 2;
                     continue;
                 }
+                if (t1 - t0 > cap) return false;
                 // gather the iteration's windows: N1 (Def 5.2-5.3) in (t0,t1) order + noise windows
                 int64_t c0s[8], c1s[8];
                 int nc = 0;
@@ -383,14 +387,22 @@ struct BuJob {
             auto r = climbs.try_emplace(l);
             if (r.second) {
                 r.first->second.lo = l;
-                r.first->second.advance(*P, cache, pair_id, hi);
+                r.first->second.advance(*P, cache, pair_id, hi, cap_for(l));
             }
         }
     }
 
+    // Speculation policy: the head and the next climb run unrestricted; climbs further ahead pause
+    // once their window exceeds spec_cap_mult * s_min (they are likely skipped by an accept).
+    int64_t cap_for(int64_t l) const {
+        const int64_t rank = (l - chain) / P->s_min;
+        if (rank <= 1 || P->spec_cap_mult <= 0) return INT64_MAX;
+        return P->spec_cap_mult * P->s_min;
+    }
+
     void advance() {
         if (done) return;
-        for (auto& kv : climbs) kv.second.advance(*P, cache, pair_id, hi);
+        for (auto& kv : climbs) kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first));
         ensure_lookahead();
         for (;;) {
             if (chain + P->s_min > hi) {
@@ -498,6 +510,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     std::vector<KsgWin> batch;
     std::vector<KsgRec> recs;
     std::vector<std::pair<PairWork*, uint64_t>> owners;
+    using clk = std::chrono::steady_clock;
+    const auto t_start = clk::now();
+    double eval_ms = 0.0;
 
     for (;;) {
         // admit pairs
@@ -598,8 +613,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             continue;
         }
         recs.resize(batch.size());
+        const auto t_ev = clk::now();
         Status s = eng->evaluate(table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
                                  P.variant, recs.data(), DebugOut{}, st, P.profile, &bs);
+        eval_ms += std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
         if (!s.ok()) return s;
         for (size_t i = 0; i < batch.size(); ++i) {
             Entry& e = owners[i].first->cache.map[owners[i].second];
@@ -626,6 +643,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         stats->bu_accepted = total.bu_accepted;
         stats->distinct_windows = distinct_w;
         stats->distinct_pairs = distinct_pp;
+        const double wall = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+        bs.wall_ms = wall;
+        bs.host_ms = wall - eval_ms;
         bs.add_to(&stats->kernel);
     }
     return Status{};

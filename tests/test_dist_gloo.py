@@ -1,0 +1,119 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the sharding + gather logic.
+
+The compute step is injected: the oracle stands in for the GPU library (tests only), so what is
+checked is that sharding + all_gather + merge reproduce the single-process results exactly and do
+not depend on the number of ranks.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import datagen
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_mi_batch(x, y, W, k):
+    import oracle
+
+    r = oracle.mi_batch(x, y, W, k)
+    return {f: r[f] for f in ("mi", "h", "nmi")}
+
+
+def _oracle_search(series, pairs, **kw):
+    import oracle
+
+    P = oracle.make_params(None, **{k: v for k, v in kw.items() if k in (
+        "k", "method", "noise", "p", "h", "t_max_idle", "n_chunks", "s_min", "s_max", "sigma", "tau_ratio",
+        "seed")})
+    return oracle.search(series, pairs, P)
+
+
+def _worker(rank, world, port, task, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2204_09131_b200 import dist as idist
+
+        if task == "sweep":
+            wl = datagen.cfg1()
+            x, y = wl.series
+            W = datagen.sweep_windows(len(x), [64, 128, 256], 24)
+            out = idist.sweep_sharded(x, y, W, 4, mi_batch=_oracle_mi_batch, device="cpu")
+            q.put((rank, {f: out[f].tolist() for f in out}))
+        else:
+            wl = datagen.cfg4(n=6000, n_series=4, n_planted=1)
+            pairs = [(a, b, 10 + i) for i, (a, b) in enumerate(wl.pairs)]
+            res, st = idist.search_sharded(wl.series, pairs, search=_oracle_search, device="cpu",
+                                           k=4, s_min=64, s_max=512, method=3, noise=1)
+            q.put((rank, (res, st)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(task, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, task, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_lpt_and_interleave():
+    from paper_2204_09131_b200 import dist as idist
+
+    a = idist.lpt_assign([5, 1, 4, 2, 3], 2)
+    assert sorted(a[0] + a[1]) == [0, 1, 2, 3, 4]
+    loads = [sum([5, 1, 4, 2, 3][i] for i in v) for v in a]
+    assert max(loads) - min(loads) <= 1
+    W = datagen.sweep_windows(1000, [64, 128], 8)
+    parts = idist.interleave_by_class(W, 3)
+    assert sorted(np.concatenate(parts).tolist()) == list(range(len(W)))
+    for s in (64, 128):
+        counts = [int(((W[p, 1] - W[p, 0]) == s).sum()) for p in parts]
+        assert max(counts) - min(counts) <= 1
+
+
+def test_sweep_sharded_world2_equals_single(orc):
+    out = _run("sweep", 2)
+    wl = datagen.cfg1()
+    x, y = wl.series
+    W = datagen.sweep_windows(len(x), [64, 128, 256], 24)
+    ref = orc.mi_batch(x, y, W, 4)
+    for rank in (0, 1):
+        for f in ("mi", "h", "nmi"):
+            assert np.array_equal(np.asarray(out[rank][f]), ref[f])
+
+
+def test_search_sharded_world2_equals_single(orc):
+    out = _run("search", 2)
+    wl = datagen.cfg4(n=6000, n_series=4, n_planted=1)
+    pairs = [(a, b, 10 + i) for i, (a, b) in enumerate(wl.pairs)]
+    ref, rst = _oracle_search(wl.series, pairs, k=4, s_min=64, s_max=512, method=3, noise=1)
+    for rank in (0, 1):
+        res, st = out[rank]
+        assert res == ref
+        assert st == rst
