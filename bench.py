@@ -247,6 +247,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ms_total, comps, wins, kms, kpairs, launches, ksg_launches, rounds = 0.0, 0.0, 0, 0.0, 0, 0, 0, 0
+    host_ms = wall_ms = 0.0
     h2d = d2h = 0
     results = None
     for _ in range(args.steps):
@@ -265,6 +266,8 @@ def main():
         launches += k["launches"]
         ksg_launches += k["ksg_launches"]
         rounds += k["rounds"]
+        host_ms += k["host_ms"]
+        wall_ms += k["wall_ms"]
         results = res
     clocks = sampler.stop()
 
@@ -324,6 +327,8 @@ def main():
             "gpu_launches": launches,
             "ksg_launches": ksg_launches,
             "rounds_per_step": rounds / args.steps,
+            "host_ms_per_step": host_ms / args.steps,
+            "driver_wall_ms_per_step": wall_ms / args.steps,
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -85,6 +85,8 @@ typedef struct {
     int64_t h2d_bytes, d2h_bytes;
     double host_ms;        /* host time spent forming batches and replaying decisions (search) */
     double wall_ms;        /* wall time of the call */
+    int64_t scan_steps;    /* sorted-marginal path: outward k-NN scan steps executed (algorithmic work) */
+    int64_t sorted_windows, sorted_points; /* windows / points evaluated on the sorted-marginal path */
 } isycos_kernel_stats;
 
 /*

@@ -39,7 +39,8 @@ class KernelStats(C.Structure):
     _fields_ = [("windows", C.c_int64), ("point_pairs", C.c_int64), ("launches", C.c_int64),
                 ("ksg_launches", C.c_int64), ("rounds", C.c_int64), ("kernel_ms", C.c_double),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("host_ms", C.c_double),
-                ("wall_ms", C.c_double)]
+                ("wall_ms", C.c_double), ("scan_steps", C.c_int64), ("sorted_windows", C.c_int64),
+                ("sorted_points", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

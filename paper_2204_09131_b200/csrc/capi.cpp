@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -256,6 +257,11 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     P.lookahead = opts->lookahead > 0 ? opts->lookahead : 256;
     P.seed = opts->seed;
     P.profile = (opts->flags & ISYCOS_F_PROFILE) != 0;
+    // speculation tuning knobs (do not change results)
+    if (const char* e = std::getenv("ISYCOS_BU_DEPTH")) P.bu_depth = std::atoi(e);
+    if (const char* e = std::getenv("ISYCOS_ANCHOR")) P.anchor_lookahead = std::atoi(e);
+    if (const char* e = std::getenv("ISYCOS_SPEC_CAP")) P.spec_cap_mult = std::atoi(e);
+    if (const char* e = std::getenv("ISYCOS_LOOKAHEAD")) P.lookahead = std::atoi(e);
     auto bad = [&](const char* m) { return fail(make_err(ISYCOS_E_INVAL, m)); };
     if (k < 1 || k > ISYCOS_MAX_K) return bad("k must be in [1, 16]");
     if (P.variant != 0) return bad("variant 1 (KSG-2) has no GPU kernel in this build (oracle only)");

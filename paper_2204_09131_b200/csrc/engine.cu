@@ -5,6 +5,7 @@
 // pinned buffer, one H2D copy, one launch per non-empty class, one D2H copy of the records.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -58,6 +59,9 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
     s->d2h_bytes += d2h_bytes;
     s->host_ms += host_ms;
     s->wall_ms += wall_ms;
+    s->scan_steps += scan_steps;
+    s->sorted_windows += sorted_windows;
+    s->sorted_points += sorted_points;
 }
 
 // ---------------------------------------------------------------- engine registry (one per device)
@@ -107,18 +111,26 @@ void release_engine_for_current_device() {
 
 Status Engine::init(int dev) {
     dev_ = dev;
+    // tuning knobs (defaults are the measured best; see profiles/)
+    if (const char* m = std::getenv("ISYCOS_KNN_MODE")) knn_mode_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_SORTED")) sorted_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
+    ISY_CK(cudaMalloc(&dsteps_, sizeof(unsigned long long)));
     return Status{};
 }
 
 Engine::~Engine() {
     cudaFree(psi_);
     cudaFree(psiq_);
+    cudaFree(lnc_);
     cudaFree(acc_);
     cudaFree(dstage_);
     cudaFree(drec_);
     cudaFree(dflag_);
+    cudaFree(dsteps_);
+    cudaFree(sscratch_);
     cudaFreeHost(hstage_);
     cudaFreeHost(hrec_);
     for (auto e : events_) cudaEventDestroy(e);
@@ -134,7 +146,8 @@ Status Engine::ensure_psi(int64_t w_max, cudaStream_t st) {
     ISY_CK(cudaMalloc(&psi, (m + 1) * sizeof(double)));
     ISY_CK(cudaMalloc(&inv, (m + 1) * sizeof(double)));
     ISY_CK(cudaMalloc(&psiq, (m + 1) * sizeof(long long)));
-    ISY_CK(launch_psi_tables(psi, psiq, inv, m, st));
+    if (!lnc_) ISY_CK(cudaMalloc(&lnc_, 16 * sizeof(double)));
+    ISY_CK(launch_psi_tables(psi, psiq, inv, m, lnc_, st));
     ISY_CK(cudaStreamSynchronize(st));
     cudaFree(inv);
     cudaFree(psi_);
@@ -169,7 +182,7 @@ Status Engine::ensure_capacity(int64_t n_wins, int64_t n_items, int32_t n_pairs,
         hrec_cap_ = c;
     }
     const int64_t bytes = 64 + n_pairs * (int64_t)sizeof(PairPtrs) + n_wins * (int64_t)sizeof(KsgWin) +
-                          n_lists * 4 + n_items * (int64_t)sizeof(KsgItem) + 4 * 64;
+                          n_lists * 4 + n_items * (int64_t)sizeof(KsgItem) + 16 * 64;
     if (dstage_cap_ < bytes) {
         int64_t c = std::max<int64_t>(bytes, dstage_cap_ * 2);
         cudaFree(dstage_);
@@ -200,35 +213,56 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         Status s = ensure_psi(w_max + 1, st);
         if (!s.ok()) return s;
     }
-    // bin windows: small classes R = 1,2,4,8; tile classes R = 2,4
+    // bin windows: small (warp per window) R = 1,2,4,8; sorted-marginal path; brute-force tile R = 2,4
     std::vector<int32_t> small[4];
     std::vector<int32_t> tile[2];
-    int64_t n_items = 0;
+    std::vector<int32_t> sorted;
+    std::vector<int64_t> soff;
+    int64_t n_items = 0, n_sitems = 0, spts = 0;
+    int W2 = 0;
     int64_t pp = 0;
     for (int64_t i = 0; i < n; ++i) {
         const int w = wins[i].w;
         pp += (int64_t)w * (w - 1);
         const int R = small_class_R(w);
-        if (R) {
+        if (R && !(sorted_on_ && w >= sorted_min_w_)) {
             small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
+        } else if (sorted_on_ && w >= sorted_min_w_ && w <= kSortedMaxW) {
+            sorted.push_back((int32_t)i);
+            soff.push_back(spts);
+            spts += w;
+            n_sitems += (w + kSortedPts - 1) / kSortedPts;
+            int n2 = 1;
+            while (n2 < w) n2 <<= 1;
+            W2 = std::max(W2, n2);
         } else {
             const int tr = tile_R(w);
             tile[tr == 2 ? 0 : 1].push_back((int32_t)i);
             n_items += (w + kTileThreads * tr - 1) / (kTileThreads * tr);
         }
     }
-    int64_t n_lists = 0;
+    int64_t n_lists = (int64_t)sorted.size();
     for (auto& v : small) n_lists += (int64_t)v.size();
     {
-        Status s = ensure_capacity(n, n_items, n_pairs, n_lists);
+        Status s = ensure_capacity(n, n_items + n_sitems, n_pairs, n_lists + 2 * (int64_t)sorted.size() + 16);
         if (!s.ok()) return s;
     }
-    // pack [pairs | wins | lists | items] into the pinned stage
-    int64_t off_pairs = 0;
-    int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
-    int64_t off_lists = align64(off_wins + n * (int64_t)sizeof(KsgWin));
-    int64_t off_items = align64(off_lists + n_lists * 4);
-    int64_t total = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
+    if (spts > 0 && sscratch_cap_ < spts * 16) {
+        const int64_t c = std::max<int64_t>(spts * 16, sscratch_cap_ * 2);
+        cudaFree(sscratch_);
+        sscratch_ = nullptr;
+        ISY_CK(cudaMalloc(&sscratch_, c));
+        sscratch_cap_ = c;
+    }
+    // pack [pairs | wins | small lists | sorted list | sorted offsets | tile items | sorted items]
+    const int64_t off_pairs = 0;
+    const int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
+    const int64_t off_lists = align64(off_wins + n * (int64_t)sizeof(KsgWin));
+    const int64_t off_slist = align64(off_lists + (n_lists - (int64_t)sorted.size()) * 4);
+    const int64_t off_soff = align64(off_slist + (int64_t)sorted.size() * 4);
+    const int64_t off_items = align64(off_soff + (int64_t)sorted.size() * 8);
+    const int64_t off_sitems = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
+    const int64_t total = align64(off_sitems + n_sitems * (int64_t)sizeof(KsgItem));
     std::memcpy(hstage_ + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
     std::memcpy(hstage_ + off_wins, wins, n * sizeof(KsgWin));
     int64_t list_off[4];
@@ -240,6 +274,8 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
             std::memcpy(lp + c, small[s].data(), small[s].size() * 4);
             c += (int64_t)small[s].size();
         }
+        std::memcpy(hstage_ + off_slist, sorted.data(), sorted.size() * 4);
+        std::memcpy(hstage_ + off_soff, soff.data(), soff.size() * 8);
     }
     int64_t item_off[2];
     {
@@ -253,15 +289,24 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
                 for (int i0 = 0; i0 < w; i0 += kTileThreads * tr) ip[c++] = KsgItem{q, i0};
             }
         }
+        KsgItem* sp = reinterpret_cast<KsgItem*>(hstage_ + off_sitems);
+        c = 0;
+        for (size_t b = 0; b < sorted.size(); ++b) {
+            const int w = wins[sorted[b]].w;
+            for (int i0 = 0; i0 < w; i0 += kSortedPts) sp[c++] = KsgItem{(int32_t)b, i0};
+        }
     }
     ISY_CK(cudaMemcpyAsync(dstage_, hstage_, total, cudaMemcpyHostToDevice, st));
     if (bs) bs->h2d_bytes += total;
+    if (!sorted.empty()) ISY_CK(cudaMemsetAsync(dsteps_, 0, sizeof(unsigned long long), st));
 
     KsgLaunch L;
     L.pairs = reinterpret_cast<const PairPtrs*>(dstage_ + off_pairs);
     L.wins = reinterpret_cast<const KsgWin*>(dstage_ + off_wins);
     L.psi = psi_;
     L.psiq = psiq_;
+    L.lnc = lnc_;
+    L.scan_steps = sorted.empty() ? nullptr : dsteps_;
     L.acc = acc_;
     L.out = drec_;
     L.dbg_eps = dbg.eps;
@@ -269,11 +314,13 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
     L.dbg_ny = dbg.ny;
     L.k = k;
     L.variant = variant;
+    L.knn_mode = knn_mode_;
+    L.two = 2;
     const int32_t* dlists = reinterpret_cast<const int32_t*>(dstage_ + off_lists);
     const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dstage_ + off_items);
 
     // launches: biggest work first so the small classes fill the tail
-    int n_launch = 0;
+    int n_launch = 0, n_ksg = 0;
     auto ev_pair = [&](int i) -> std::pair<cudaEvent_t, cudaEvent_t> {
         while ((int)events_.size() < 2 * (i + 1)) {
             cudaEvent_t e;
@@ -282,17 +329,30 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         }
         return {events_[2 * i], events_[2 * i + 1]};
     };
-    auto launch = [&](auto&& fn) -> Status {
+    auto launch = [&](int nk, auto&& fn) -> Status {
         std::pair<cudaEvent_t, cudaEvent_t> ev{};
         if (profile) {
-            ev = ev_pair(n_launch);
+            ev = ev_pair(n_ksg);
             ISY_CK(cudaEventRecord(ev.first, st));
         }
         ISY_CK(fn());
         if (profile) ISY_CK(cudaEventRecord(ev.second, st));
-        ++n_launch;
+        ++n_ksg;
+        n_launch += nk;
         return Status{};
     };
+    if (!sorted.empty()) {
+        const int32_t* dsl = reinterpret_cast<const int32_t*>(dstage_ + off_slist);
+        const int64_t* dso = reinterpret_cast<const int64_t*>(dstage_ + off_soff);
+        const KsgItem* dsi = reinterpret_cast<const KsgItem*>(dstage_ + off_sitems);
+        float2* P2 = reinterpret_cast<float2*>(sscratch_);
+        int32_t* OX = reinterpret_cast<int32_t*>(sscratch_ + spts * 8);
+        float* YS = reinterpret_cast<float*>(sscratch_ + spts * 12);
+        Status r = launch(2, [&] {
+            return launch_sorted(L, dsl, (int32_t)sorted.size(), dso, P2, OX, YS, W2, dsi, (int32_t)n_sitems, st);
+        });
+        if (!r.ok()) return r;
+    }
     for (int s = 1; s >= 0; --s) {
         if (tile[s].empty()) continue;
         int64_t cnt = 0;
@@ -302,7 +362,7 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         }
         const int R = s == 0 ? 2 : 4;
         const KsgItem* ip = ditems + item_off[s];
-        Status r = launch([&] { return launch_ksg_tile(L, ip, (int32_t)cnt, R, st); });
+        Status r = launch(1, [&] { return launch_ksg_tile(L, ip, (int32_t)cnt, R, st); });
         if (!r.ok()) return r;
     }
     for (int s = 3; s >= 0; --s) {
@@ -310,9 +370,11 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         const int R = 1 << s;
         const int32_t* lp = dlists + list_off[s];
         const int32_t cnt = (int32_t)small[s].size();
-        Status r = launch([&] { return launch_ksg_small(L, lp, cnt, R, st); });
+        Status r = launch(1, [&] { return launch_ksg_small(L, lp, cnt, R, st); });
         if (!r.ok()) return r;
     }
+    unsigned long long steps = 0;
+    if (!sorted.empty()) ISY_CK(cudaMemcpyAsync(&steps, dsteps_, sizeof(steps), cudaMemcpyDeviceToHost, st));
     if (recs_host) {
         ISY_CK(cudaMemcpyAsync(hrec_, drec_, n * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
         if (bs) bs->d2h_bytes += n * (int64_t)sizeof(KsgRec);
@@ -325,8 +387,11 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         bs->launches += n_launch;
         bs->ksg_launches += n_launch;
         bs->rounds += 1;
+        bs->scan_steps += (int64_t)steps;
+        bs->sorted_windows += (int64_t)sorted.size();
+        bs->sorted_points += spts;
         if (profile) {
-            for (int i = 0; i < n_launch; ++i) {
+            for (int i = 0; i < n_ksg; ++i) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, events_[2 * i], events_[2 * i + 1]);
                 bs->kernel_ms += ms;

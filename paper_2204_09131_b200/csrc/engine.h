@@ -53,6 +53,8 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     const KsgWin* wins;
     const double* psi;       // psi[m], m = 0..w_max
     const long long* psiq;   // q(psi[m]) = rint(psi[m] * 2^32)
+    const double* lnc;       // LN series coefficients 1/(2j+1), j = 1..9
+    unsigned long long* scan_steps;  // sorted path: total outward-scan steps (algorithmic work), or null
     KsgAcc* acc;
     KsgRec* out;
     float* dbg_eps;
@@ -60,6 +62,8 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t* dbg_ny;
     int32_t k;
     int32_t variant;
+    int32_t knn_mode;        // small-window kNN insertion: 1 branch-free network, 0 guarded
+    int32_t two;             // the constant 2, passed at run time (see acc_lt)
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -68,11 +72,18 @@ constexpr int kTileThreads = 256;        // threads per CTA of the tile kernel
 constexpr int kTileJ = 4096;             // j-tile (points) staged per cp.async.bulk round
 int small_class_R(int w);                // 1,2,4,8 for w <= 256; 0 => tile kernel
 int tile_R(int w);                       // points per thread of the tile kernel
+constexpr int kSortedPts = 128;          // points per CTA of the sorted-path scan kernel
+constexpr int kSortedMaxW = 16384;       // sorted path: window sorted in one CTA's SMEM
 
 // Launchers (ksg_kernels.cu).  Return cudaGetLastError().
 cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
 cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st);
-cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, cudaStream_t st);
+// sorted path: sort kernel (one CTA per window of `list`) then scan kernel over `items` (win = list pos)
+cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, int32_t n_list, const int64_t* soff,
+                          float2* P2, int32_t* OX, float* YS, int W2, const KsgItem* items, int32_t n_items,
+                          cudaStream_t st);
+cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, double* lnc,
+                              cudaStream_t st);
 cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st);
 
 // ---------------------------------------------------------------- errors
@@ -94,6 +105,7 @@ struct DebugOut {
 
 struct BatchStats {
     int64_t windows = 0, point_pairs = 0, launches = 0, ksg_launches = 0, rounds = 0;
+    int64_t scan_steps = 0, sorted_windows = 0, sorted_points = 0;
     double kernel_ms = 0.0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     double host_ms = 0.0, wall_ms = 0.0;
@@ -134,7 +146,9 @@ private:
     // digamma tables
     double* psi_ = nullptr;
     long long* psiq_ = nullptr;
+    double* lnc_ = nullptr;
     int64_t psi_max_ = 0;
+    int32_t knn_mode_ = 1;
     // batch buffers (device) and pinned staging (host)
     KsgAcc* acc_ = nullptr;
     int64_t acc_cap_ = 0;
@@ -148,6 +162,12 @@ private:
     int64_t hrec_cap_ = 0;
     int* dflag_ = nullptr;
     std::vector<cudaEvent_t> events_;
+    // sorted path scratch: [P2 float2 | OX int32 | YS float] per point, + step counter
+    char* sscratch_ = nullptr;
+    int64_t sscratch_cap_ = 0;
+    unsigned long long* dsteps_ = nullptr;
+    bool sorted_on_ = true;
+    int32_t sorted_min_w_ = 257;
 };
 
 // ---------------------------------------------------------------- search driver
@@ -162,6 +182,8 @@ struct SearchParams {
     int64_t delta_td = 0, delta_bu = 0;
     int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 256;
     int64_t spec_cap_mult = 4;   // BU: speculative climbs pause beyond this many s_min
+    int32_t anchor_lookahead = 64;  // BU: climbs started at the predicted re-anchor point
+    int32_t bu_depth = 3;           // BU: iterations of delta-neighbourhood requested per round
     uint64_t seed = 0;
     bool profile = false;
 };

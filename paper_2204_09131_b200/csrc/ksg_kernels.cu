@@ -69,7 +69,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ long long q32(double v) { return __double2ll_rn(__dmul_rn(v, 4294967296.0)); }
 
 // LN(v), v > 0 normal: frexp -> [sqrt(1/2), sqrt(2)) -> 2 atanh(s) series to s^19, fixed op order.
-__device__ double canon_ln(double v) {
+// c[j] = 1/(2j+1) (j = 1..9) are computed once by psi_scan_kernel with __ddiv_rn.
+__device__ double canon_ln(double v, const double* __restrict__ c) {
     const long long bits = __double_as_longlong(v);
     int e = (int)((bits >> 52) & 0x7FF) - 1022;
     double m = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FE0000000000000LL);  // [0.5, 1)
@@ -79,9 +80,9 @@ __device__ double canon_ln(double v) {
     }
     const double s = __ddiv_rn(__dsub_rn(m, 1.0), __dadd_rn(m, 1.0));
     const double z = __dmul_rn(s, s);
-    double p = __ddiv_rn(1.0, 19.0);
+    double p = c[9];
 #pragma unroll
-    for (int j = 8; j >= 1; --j) p = __dadd_rn(__dmul_rn(p, z), __ddiv_rn(1.0, (double)(2 * j + 1)));
+    for (int j = 8; j >= 1; --j) p = __dadd_rn(__dmul_rn(p, z), c[j]);
     const double two_s = __dmul_rn(2.0, s);
     const double tail = __dmul_rn(__dmul_rn(two_s, z), p);
     const double r = __dadd_rn(two_s, tail);
@@ -134,7 +135,10 @@ __device__ __forceinline__ void topk_insert(float (&r)[K1], float d) {
 }
 
 // a3: four candidates j (one float4 of x and of y, broadcast to the warp) against R points.
-template <int K1, int R>
+// BRANCHLESS: insert every candidate through the min/max network (small windows, where nearly every
+// step has some lane inserting and divergence would serialize the warp anyway); otherwise a per-4
+// min-tree guards the (then rare) insertions.
+template <int K1, int R, bool BRANCHLESS>
 __device__ __forceinline__ void knn_step(const float (&xi)[R], const float (&yi)[R], float (&rk)[R][K1],
                                          const float4 X, const float4 Y) {
 #pragma unroll
@@ -143,30 +147,44 @@ __device__ __forceinline__ void knn_step(const float (&xi)[R], const float (&yi)
         const float d1 = fmaxf(fabsf(xi[r] - X.y), fabsf(yi[r] - Y.y));
         const float d2 = fmaxf(fabsf(xi[r] - X.z), fabsf(yi[r] - Y.z));
         const float d3 = fmaxf(fabsf(xi[r] - X.w), fabsf(yi[r] - Y.w));
-        const float m = fminf(fminf(d0, d1), fminf(d2, d3));
-        if (m < rk[r][K1 - 1]) {
-            if (d0 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d0);
-            if (d1 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d1);
-            if (d2 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d2);
-            if (d3 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d3);
+        if (BRANCHLESS) {
+            topk_insert<K1>(rk[r], d0);
+            topk_insert<K1>(rk[r], d1);
+            topk_insert<K1>(rk[r], d2);
+            topk_insert<K1>(rk[r], d3);
+        } else {
+            const float m = fminf(fminf(d0, d1), fminf(d2, d3));
+            if (m < rk[r][K1 - 1]) {
+                if (d0 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d0);
+                if (d1 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d1);
+                if (d2 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d2);
+                if (d3 < rk[r][K1 - 1]) topk_insert<K1>(rk[r], d3);
+            }
         }
     }
 }
 
 // a4: sign bit of fl(|fl(x_i - x_j)| - eps_i) is 1 iff |fl(x_i - x_j)| < eps_i (finite, no FTZ).
-__device__ __forceinline__ unsigned lt_bit(float xi, float xj, float eps) {
-    return __float_as_uint(fabsf(xi - xj) - eps) >> 31;
+// The sign bit is accumulated as acc += t >> 31 (one LEA.HI).  (Moving it to the FMA pipe with
+// mad.hi.u32 by a runtime 2 measured slower: 0.45 vs 0.59 of the roofline at w = 4096.)
+__device__ __forceinline__ void acc_lt(unsigned& acc, float xi, float xj, float eps, unsigned) {
+    acc += __float_as_uint(fabsf(xi - xj) - eps) >> 31;
 }
 
 template <int R>
 __device__ __forceinline__ void count_step(const float (&xi)[R], const float (&yi)[R], const float (&eps)[R],
-                                           unsigned (&cx)[R], unsigned (&cy)[R], const float4 X, const float4 Y) {
+                                           unsigned (&cx)[R], unsigned (&cy)[R], const float4 X, const float4 Y,
+                                           unsigned two) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        cx[r] += lt_bit(xi[r], X.x, eps[r]) + lt_bit(xi[r], X.y, eps[r]) + lt_bit(xi[r], X.z, eps[r]) +
-                 lt_bit(xi[r], X.w, eps[r]);
-        cy[r] += lt_bit(yi[r], Y.x, eps[r]) + lt_bit(yi[r], Y.y, eps[r]) + lt_bit(yi[r], Y.z, eps[r]) +
-                 lt_bit(yi[r], Y.w, eps[r]);
+        acc_lt(cx[r], xi[r], X.x, eps[r], two);
+        acc_lt(cx[r], xi[r], X.y, eps[r], two);
+        acc_lt(cx[r], xi[r], X.z, eps[r], two);
+        acc_lt(cx[r], xi[r], X.w, eps[r], two);
+        acc_lt(cy[r], yi[r], Y.x, eps[r], two);
+        acc_lt(cy[r], yi[r], Y.y, eps[r], two);
+        acc_lt(cy[r], yi[r], Y.z, eps[r], two);
+        acc_lt(cy[r], yi[r], Y.w, eps[r], two);
     }
 }
 
@@ -184,7 +202,7 @@ __device__ __forceinline__ void point_terms(const KsgLaunch& L, int w, int64_t d
             const int ny = (int)cy[r] - pos;
             sp += L.psiq[nx + 1] + L.psiq[ny + 1];
             if (pos)
-                sl += q32(canon_ln(__dmul_rn(2.0, (double)eps[r])));
+                sl += q32(canon_ln(__dmul_rn(2.0, (double)eps[r]), L.lnc));
             else
                 z += 1;
             if (dbg_off >= 0) {
@@ -206,7 +224,7 @@ __device__ __forceinline__ void warp_sum(long long& a, long long& b, int& c) {
 }
 
 // ------------------------------------------------------------------ small windows: one warp per window
-template <int K1, int R>
+template <int K1, int R, bool BL>
 __global__ void __launch_bounds__(kSmallWarps * 32)
     ksg_small_kernel(const KsgLaunch L, const int32_t* __restrict__ list, int32_t n) {
     constexpr int CAP = 32 * R + 4;
@@ -242,14 +260,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     const float4* sx4 = reinterpret_cast<const float4*>(sx);
     const float4* sy4 = reinterpret_cast<const float4*>(sy);
     const int ng = wpad >> 2;
-    for (int g = 0; g < ng; ++g) knn_step<K1, R>(xi, yi, rk, sx4[g], sy4[g]);
+    for (int g = 0; g < ng; ++g) knn_step<K1, R, BL>(xi, yi, rk, sx4[g], sy4[g]);
     float eps[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) eps[r] = rk[r][K1 - 1];
     unsigned cx[R], cy[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
-    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g]);
+    const unsigned two = (unsigned)L.two;
+    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g], two);
     long long sp = 0, sl = 0;
     int z = 0;
     point_terms<R>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
@@ -334,7 +353,7 @@ __global__ void __launch_bounds__(kTileThreads)
         ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
         const float4* sx4 = reinterpret_cast<const float4*>(sx);
         const float4* sy4 = reinterpret_cast<const float4*>(sy);
-        for (int g = 0; g < ng; ++g) knn_step<K1, R>(xi, yi, rk, sx4[g], sy4[g]);
+        for (int g = 0; g < ng; ++g) knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
         if (nj > 1) __syncthreads();
     }
     float eps[R];
@@ -350,7 +369,7 @@ __global__ void __launch_bounds__(kTileThreads)
         }
         const float4* sx4 = reinterpret_cast<const float4*>(sx);
         const float4* sy4 = reinterpret_cast<const float4*>(sy);
-        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g]);
+        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g], (unsigned)L.two);
         if (nj > 1) __syncthreads();
     }
 
@@ -394,6 +413,246 @@ __global__ void __launch_bounds__(kTileThreads)
     }
 }
 
+// ------------------------------------------------------------------ CTA reduce + window accumulate/finalize
+template <int NT>
+__device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int ntiles, long long sp, long long sl,
+                                           int z, unsigned long long steps) {
+    __shared__ long long r_sp[NT / 32], r_sl[NT / 32];
+    __shared__ int r_z[NT / 32];
+    __shared__ unsigned long long r_st[NT / 32];
+    warp_sum(sp, sl, z);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) steps += __shfl_down_sync(0xffffffffu, steps, off);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        r_sp[warp] = sp;
+        r_sl[warp] = sl;
+        r_z[warp] = z;
+        r_st[warp] = steps;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int v = 1; v < NT / 32; ++v) {
+        sp += r_sp[v];
+        sl += r_sl[v];
+        z += r_z[v];
+        steps += r_st[v];
+    }
+    if (L.scan_steps) atomicAdd(L.scan_steps, steps);
+    if (ntiles == 1) {
+        finalize(L, w, sp, sl, z, &L.out[q]);
+        return;
+    }
+    KsgAcc* A = &L.acc[q];
+    atomicAdd(&A->s_psi, (unsigned long long)sp);
+    atomicAdd(&A->s_log, (unsigned long long)sl);
+    atomicAdd(&A->zero, (unsigned)z);
+    __threadfence();
+    const unsigned ticket = atomicAdd(&A->done, 1u);
+    if (ticket == (unsigned)(ntiles - 1)) {  // last tile of the window: finalize + reset the slot
+        __threadfence();
+        const long long tp = (long long)atomicExch(&A->s_psi, 0ull);
+        const long long tl = (long long)atomicExch(&A->s_log, 0ull);
+        const int tz = (int)atomicExch(&A->zero, 0u);
+        atomicExch(&A->done, 0u);
+        finalize(L, w, tp, tl, tz, &L.out[q]);
+    }
+}
+
+// ------------------------------------------------------------------ sorted-marginal path
+// The paper's box-assisted k-NN reaches O(n log n) per window by searching only near each
+// point.  The GPU analogue here is exact: sort the window by x (payload: original index) and sort y;
+// then for each point
+//   eps_i: outward scan in x order from the point's own position, visiting candidates in non-decreasing
+//          |fl(x_i - x_j)| (merge of the left and right runs; fl is monotone, so the runs are sorted) and
+//          stopping as soon as that |dx| >= r_{k+1}: every unvisited j has d_ij >= |dx| >= r_{k+1} and
+//          cannot change the (k+1)-th order statistic.  Same multiset statistic as the brute force.
+//   n_x:   {j : |fl(x_i - x_j)| < eps} is an index interval of the x-sorted array (the predicate is
+//          monotone on each side of x_i), found by two binary searches with the identical predicate;
+//          n_y likewise on the sorted y.  Bit-identical to the brute-force counts.
+constexpr int kSortedThreads = 128;  // points per CTA of the scan kernel (one point per thread)
+
+// One CTA per window (w <= kSortedMaxW): bitonic sorts in SMEM of (x, idx) and of y, written to the
+// batch scratch: P2[m] = (x, y) of the m-th point in x order, OX[m] = its original index, YS = sorted y.
+__global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
+                                   const int64_t* __restrict__ soff, float2* __restrict__ P2,
+                                   int32_t* __restrict__ OX, float* __restrict__ YS, int W2) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    float* key = reinterpret_cast<float*>(sm);
+    int32_t* pay = reinterpret_cast<int32_t*>(key + W2);
+    const int b = blockIdx.x;
+    const int q = list[b];
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    int n2 = 1;
+    while (n2 < w) n2 <<= 1;
+    const float* gx = L.pairs[W.pair].x + W.t0;
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    const int64_t o = soff[b];
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+            key[i] = i < w ? (pass == 0 ? gx[i] : gy[i]) : kInf;
+            pay[i] = i;
+        }
+        __syncthreads();
+        for (int k = 2; k <= n2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
+                    const int i = 2 * t - (t & (j - 1));
+                    const int ixj = i + j;
+                    const float a = key[i], c = key[ixj];
+                    const bool up = (i & k) == 0;
+                    if (up ? (a > c) : (a < c)) {
+                        key[i] = c;
+                        key[ixj] = a;
+                        const int32_t pa = pay[i];
+                        pay[i] = pay[ixj];
+                        pay[ixj] = pa;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int m = threadIdx.x; m < w; m += blockDim.x) {
+            if (pass == 0) {
+                const int32_t idx = pay[m];
+                P2[o + m] = make_float2(key[m], gy[idx]);
+                OX[o + m] = idx;
+            } else {
+                YS[o + m] = key[m];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// first index in [lo, hi) where pred is false, for pred true...true false...false
+// left side: smallest j in [0, m] with fl(v - s[j]) < eps (pred false...true)
+__device__ __forceinline__ int left_bound(const float* s, int m, float v, float eps) {
+    int lo = 0, hi = m;  // answer in [lo, hi]; s[hi]... pred(m) true iff eps > 0 (checked by caller)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v - s[mid] < eps) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+// right side: largest j in [m, w) with fl(s[j] - v) < eps, returned as one past it
+__device__ __forceinline__ int right_bound(const float* s, int m, int w, float v, float eps) {
+    int lo = m, hi = w;  // first j >= m with pred false, in [m, w]
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid] - v < eps) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int lower_bound_f(const float* s, int w, float v) {
+    int lo = 0, hi = w;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int left_bound_f(const float* s, int m, float v, float eps) { return left_bound(s, m, v, eps); }
+
+template <int K1>
+__global__ void __launch_bounds__(kSortedThreads)
+    sorted_knn_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
+                      const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
+                      const KsgItem* __restrict__ items) {
+    const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list
+    const int b = it.win;
+    const int q = list[b];
+    const int w = L.wins[q].w;
+    const int64_t o = soff[b];
+    const float2* P2 = P2g + o;
+    const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
+    const float* YS = YSg + o;
+    const int m = it.i0 + threadIdx.x;
+    long long sp = 0, sl = 0;
+    int z = 0;
+    unsigned long long steps = 0;
+    if (m < w) {
+        const float2 me = P2[m];
+        const float xi = me.x, yi = me.y;
+        float rk[K1];
+        rk[0] = 0.0f;  // self: d_ii = 0
+#pragma unroll
+        for (int t = 1; t < K1; ++t) rk[t] = kInf;
+        // a3: outward scan in x order
+        int l = m - 1, r = m + 1;
+        float2 pl = l >= 0 ? P2[l] : make_float2(0.f, 0.f);
+        float2 pr = r < w ? P2[r] : make_float2(0.f, 0.f);
+        float dl = l >= 0 ? xi - pl.x : kInf;  // >= 0: sorted ascending
+        float dr = r < w ? pr.x - xi : kInf;
+        for (;;) {
+            const float dmin = fminf(dl, dr);
+            if (!(dmin < rk[K1 - 1])) break;
+            float d;
+            if (dl <= dr) {
+                d = fmaxf(dl, fabsf(yi - pl.y));
+                --l;
+                if (l >= 0) {
+                    pl = P2[l];
+                    dl = xi - pl.x;
+                } else {
+                    dl = kInf;
+                }
+            } else {
+                d = fmaxf(dr, fabsf(yi - pr.y));
+                ++r;
+                if (r < w) {
+                    pr = P2[r];
+                    dr = pr.x - xi;
+                } else {
+                    dr = kInf;
+                }
+            }
+            ++steps;
+            if (d < rk[K1 - 1]) topk_insert<K1>(rk, d);
+        }
+        const float eps = rk[K1 - 1];
+        // a4: interval counts by binary search with the identical predicates
+        int nx = 0, ny = 0;
+        if (eps > 0.0f) {
+            // x: left part [0, m] uses fl(x_i - x_j) < eps, right part [m, w) uses fl(x_j - x_i) < eps
+            int lo = 0, hi = m;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (xi - XS[2 * mid] < eps) hi = mid; else lo = mid + 1;
+            }
+            const int Lx = lo;
+            lo = m;
+            hi = w;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (XS[2 * mid] - xi < eps) lo = mid + 1; else hi = mid;
+            }
+            nx = lo - Lx - 1;
+            const int p = lower_bound_f(YS, w, yi);
+            const int Ly = left_bound_f(YS, p, yi, eps);
+            const int Ry = right_bound(YS, p, w, yi, eps);
+            ny = Ry - Ly - 1;
+        }
+        // a5: per-point terms
+        sp = L.psiq[nx + 1] + L.psiq[ny + 1];
+        if (eps > 0.0f)
+            sl = q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
+        else
+            z = 1;
+        const int64_t dbg = L.wins[q].dbg_off;
+        if (dbg >= 0) {
+            const int i = OXg[o + m];
+            if (L.dbg_eps) L.dbg_eps[dbg + i] = eps;
+            if (L.dbg_nx) L.dbg_nx[dbg + i] = nx;
+            if (L.dbg_ny) L.dbg_ny[dbg + i] = ny;
+        }
+    }
+    const int ntiles = (w + kSortedThreads - 1) / kSortedThreads;
+    cta_finish<kSortedThreads>(L, q, w, ntiles, sp, sl, z, steps);
+}
+
 // ------------------------------------------------------------------ digamma tables, input validation
 __global__ void inv_kernel(double* inv, int64_t m_max) {
     const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -401,8 +660,10 @@ __global__ void inv_kernel(double* inv, int64_t m_max) {
 }
 
 // psi(1) = -gamma; psi(m+1) = psi(m) + 1/m, strictly sequential (the canonical definition).
-__global__ void psi_scan_kernel(double* psi, const double* __restrict__ inv, int64_t m_max) {
+__global__ void psi_scan_kernel(double* psi, const double* __restrict__ inv, int64_t m_max, double* lnc) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    lnc[0] = 0.0;
+    for (int j = 1; j <= 9; ++j) lnc[j] = __ddiv_rn(1.0, (double)(2 * j + 1));  // LN series coefficients
     psi[0] = __longlong_as_double(0x7FF8000000000000LL);
     double v = -0.57721566490153286061;
     psi[1] = v;
@@ -426,17 +687,22 @@ __global__ void nonfinite_kernel(const float* __restrict__ p, int64_t n, int* fl
 }
 
 // ------------------------------------------------------------------ dispatch over (k, R)
-template <int K1>
-cudaError_t small_k(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
+template <int K1, bool BL>
+cudaError_t small_kb(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
     const dim3 grid((n + kSmallWarps - 1) / kSmallWarps), block(kSmallWarps * 32);
     switch (R) {
-        case 1: ksg_small_kernel<K1, 1><<<grid, block, 0, st>>>(L, list, n); break;
-        case 2: ksg_small_kernel<K1, 2><<<grid, block, 0, st>>>(L, list, n); break;
-        case 4: ksg_small_kernel<K1, 4><<<grid, block, 0, st>>>(L, list, n); break;
-        case 8: ksg_small_kernel<K1, 8><<<grid, block, 0, st>>>(L, list, n); break;
+        case 1: ksg_small_kernel<K1, 1, BL><<<grid, block, 0, st>>>(L, list, n); break;
+        case 2: ksg_small_kernel<K1, 2, BL><<<grid, block, 0, st>>>(L, list, n); break;
+        case 4: ksg_small_kernel<K1, 4, BL><<<grid, block, 0, st>>>(L, list, n); break;
+        case 8: ksg_small_kernel<K1, 8, BL><<<grid, block, 0, st>>>(L, list, n); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+
+template <int K1>
+cudaError_t small_k(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
+    return L.knn_mode == 1 ? small_kb<K1, true>(L, list, n, R, st) : small_kb<K1, false>(L, list, n, R, st);
 }
 
 template <int K1>
@@ -483,10 +749,38 @@ cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_
     ISY_K_CASES(tile_k, L, items, n_items, R, st)
 }
 
-cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, cudaStream_t st) {
+namespace {
+template <int K1>
+cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const float2* P2,
+                     const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st) {
+    sorted_knn_kernel<K1><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, int32_t n_list, const int64_t* soff, float2* P2,
+                          int32_t* OX, float* YS, int W2, const KsgItem* items, int32_t n_items, cudaStream_t st) {
+    static_assert(kSortedThreads == kSortedPts, "scan CTA size");
+    if (n_list <= 0) return cudaSuccess;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kSortedMaxW * 8);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int threads = std::min(1024, std::max(64, W2 / 2));
+    sort_window_kernel<<<n_list, threads, (size_t)W2 * 8, st>>>(L, list, soff, P2, OX, YS, W2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st)
+}
+
+cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, double* lnc,
+                              cudaStream_t st) {
     const int64_t blocks = (m_max + 1 + 255) / 256;
     inv_kernel<<<(unsigned)blocks, 256, 0, st>>>(inv, m_max);
-    psi_scan_kernel<<<1, 32, 0, st>>>(psi, inv, m_max);
+    psi_scan_kernel<<<1, 32, 0, st>>>(psi, inv, m_max, lnc);
     psiq_kernel<<<(unsigned)blocks, 256, 0, st>>>(psi, psiq, m_max);
     return cudaGetLastError();
 }

@@ -16,10 +16,12 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
-#include <unordered_map>
 #include <vector>
 
 #include "engine.h"
@@ -41,8 +43,61 @@ inline uint64_t wkey(int64_t t0, int64_t t1) { return ((uint64_t)t0 << 20) | (ui
 inline int64_t key_t0(uint64_t k) { return (int64_t)(k >> 20); }
 inline int64_t key_w(uint64_t k) { return (int64_t)(k & ((1u << 20) - 1)); }
 
+// Open-addressing window cache: keys -> index into a stable arena (entry pointers never move).
+struct FlatMap {
+    std::vector<uint64_t> keys;  // 0 = empty (a window key is never 0: w >= 2)
+    std::vector<uint32_t> slot;
+    std::deque<Entry> arena;
+    std::vector<uint64_t> arena_keys;
+    size_t mask = 0;
+
+    static size_t hash(uint64_t k) {
+        k ^= k >> 33;
+        k *= 0xff51afd7ed558ccdull;
+        k ^= k >> 33;
+        return (size_t)k;
+    }
+    void grow() {
+        const size_t cap = keys.empty() ? 4096 : keys.size() * 2;
+        std::vector<uint64_t> nk(cap, 0);
+        std::vector<uint32_t> ns(cap, 0);
+        const size_t m = cap - 1;
+        for (size_t a = 0; a < arena_keys.size(); ++a) {
+            size_t i = hash(arena_keys[a]) & m;
+            while (nk[i]) i = (i + 1) & m;
+            nk[i] = arena_keys[a];
+            ns[i] = (uint32_t)a;
+        }
+        keys.swap(nk);
+        slot.swap(ns);
+        mask = m;
+    }
+    std::pair<Entry*, bool> try_emplace(uint64_t k) {
+        if ((arena.size() + 1) * 2 > keys.size()) grow();
+        size_t i = hash(k) & mask;
+        while (keys[i]) {
+            if (keys[i] == k) return {&arena[slot[i]], false};
+            i = (i + 1) & mask;
+        }
+        keys[i] = k;
+        slot[i] = (uint32_t)arena.size();
+        arena.emplace_back();
+        arena_keys.push_back(k);
+        return {&arena.back(), true};
+    }
+    Entry* find(uint64_t k) {
+        if (keys.empty()) return nullptr;
+        size_t i = hash(k) & mask;
+        while (keys[i]) {
+            if (keys[i] == k) return &arena[slot[i]];
+            i = (i + 1) & mask;
+        }
+        return nullptr;
+    }
+};
+
 struct PairCache {
-    std::unordered_map<uint64_t, Entry> map;
+    FlatMap map;
     std::vector<uint64_t> pending;
 };
 
@@ -77,19 +132,23 @@ struct View {
             c->pending.push_back(k);
             return nullptr;
         }
-        if (!r.first->second.ready) return nullptr;
+        if (!r.first->ready) return nullptr;
         touched->push_back(k);
-        return &r.first->second.e;
+        return &r.first->e;
     }
     void want(int64_t t0, int64_t t1) {
         const uint64_t k = wkey(t0, t1);
         auto r = c->map.try_emplace(k);
         if (r.second) c->pending.push_back(k);
     }
+    const Eval* peek(int64_t t0, int64_t t1) {  // no request, no consumption
+        Entry* e = c->map.find(wkey(t0, t1));
+        return (e && e->ready) ? &e->e : nullptr;
+    }
 };
 
 void commit_touched(PairCache* c, const std::vector<uint64_t>& t) {
-    for (uint64_t k : t) c->map[k].consumed = true;
+    for (uint64_t k : t) c->map.find(k)->consumed = true;
 }
 
 // ------------------------------------------------------------------ SYCOS_TD job
@@ -243,6 +302,29 @@ struct Climb {
     bool finished = false;
     Eval fin{0, 0, 0};
 
+    // Depth speculation: request every window the next bu_depth iterations could need — the rings
+    // N_1..N_D of the delta-neighbourhood (Defs 5.2-5.3, Fig. 4's N_1/N_2) plus their noise extensions —
+    // so a climb advances up to bu_depth iterations per round.  Requests only; nothing is consumed.
+    void want_ring(View& v, const SearchParams& P, int64_t hi, int64_t d) const {
+        const int D = P.bu_depth;
+        if (D <= 1) return;
+        for (int a = -D; a <= D; ++a) {
+            if (a < 0 && pruned[0]) continue;
+            for (int b = -D; b <= D; ++b) {
+                if ((a == 0 && b == 0) || (b > 0 && pruned[1])) continue;
+                const int64_t c0 = t0 + a * d, c1 = t1 + b * d;
+                if (c0 < lo || c1 > hi || c1 - c0 < P.s_min || c1 - c0 > P.s_max) continue;
+                v.want(c0, c1);
+            }
+        }
+        if (!(P.noise && d > P.k)) return;
+        for (int a = -(D - 1); a <= D - 1; ++a) {
+            const int64_t l0 = t0 + a * d - d, r0 = t1 + a * d;
+            if (!pruned[0] && l0 >= lo) v.want(l0, l0 + d);
+            if (!pruned[1] && r0 >= lo && r0 + d <= hi) v.want(r0, r0 + d);
+        }
+    }
+
     // Advance as far as the cache allows.  Returns true when the climb is finished.  A speculative
     // climb whose window has grown beyond `cap` pauses (requests nothing) until it nears the chain head.
     bool advance(const SearchParams& P, PairCache* cache, int32_t pair_id, int64_t hi,
@@ -321,6 +403,7 @@ struct Climb {
                 }
                 if (missing) {
                     touched.resize(mark);
+                    want_ring(v, P, hi, d);
                     return false;
                 }
                 // the iteration, exactly as Alg. 2 lines 7-21
@@ -400,6 +483,26 @@ struct BuJob {
         return P->spec_cap_mult * P->s_min;
     }
 
+    // Anchor speculation: while the head idles on a window that would be accepted (nmi >= sigma), the
+    // chain will most likely re-anchor at max(t1, lo + s_min); start the climbs of that chain now.
+    void speculate_anchor(const Climb& c) {
+        if (P->anchor_lookahead <= 0 || c.state != 1 || c.idle < 1) return;
+        std::vector<uint64_t> none;
+        View v{cache, &none};
+        const Eval* e = v.peek(c.t0, c.t1);
+        if (!e || !(e->nmi >= P->sigma)) return;
+        const int64_t a = std::max(c.t1, chain + P->s_min);
+        for (int j = 0; j < P->anchor_lookahead; ++j) {
+            const int64_t l = a + (int64_t)j * P->s_min;
+            if (l + P->s_min > hi) break;
+            auto r = climbs.try_emplace(l);
+            if (r.second) {
+                r.first->second.lo = l;
+                r.first->second.advance(*P, cache, pair_id, hi, j <= 1 ? INT64_MAX : P->spec_cap_mult * P->s_min);
+            }
+        }
+    }
+
     void advance() {
         if (done) return;
         for (auto& kv : climbs) kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first));
@@ -416,7 +519,10 @@ struct BuJob {
                 it = climbs.find(chain);
             }
             Climb& c = it->second;
-            if (!c.advance(*P, cache, pair_id, hi)) return;
+            if (!c.advance(*P, cache, pair_id, hi)) {
+                speculate_anchor(c);
+                return;
+            }
             // commit the head climb (Alg. 2 lines 23-24; restart on the remainder)
             stats.add(c.st);
             commit_touched(cache, c.touched);
@@ -509,10 +615,20 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     int32_t next_pair = 0;
     std::vector<KsgWin> batch;
     std::vector<KsgRec> recs;
-    std::vector<std::pair<PairWork*, uint64_t>> owners;
+    std::vector<Entry*> owners;
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
+    auto t_last = t_start;
     double eval_ms = 0.0;
+    int64_t round_no = 0;
+    std::FILE* trace = nullptr;
+    if (const char* tp = std::getenv("ISYCOS_TRACE")) trace = std::fopen(tp, "a");
+    struct Closer {
+        std::FILE*& f;
+        ~Closer() {
+            if (f) std::fclose(f);
+        }
+    } closer{trace};
 
     for (;;) {
         // admit pairs
@@ -580,9 +696,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                     all.insert(all.end(), merged.begin(), merged.end());
                 }
                 total.add(ps);
-                for (auto& kv : pw->cache.map)
-                    if (kv.second.consumed) {
-                        const int64_t w = key_w(kv.first);
+                const FlatMap& fm = pw->cache.map;
+                for (size_t a = 0; a < fm.arena.size(); ++a)
+                    if (fm.arena[a].consumed) {
+                        const int64_t w = key_w(fm.arena_keys[a]);
                         distinct_w += 1;
                         distinct_pp += w * (w - 1);
                     }
@@ -601,7 +718,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             table.push_back(pw->ptrs);
             for (uint64_t k : pw->cache.pending) {
                 batch.push_back(KsgWin{key_t0(k), (int32_t)key_w(k), pw->slot, -1});
-                owners.push_back({pw.get(), k});
+                owners.push_back(pw->cache.map.find(k));
             }
             pw->cache.pending.clear();
         }
@@ -616,10 +733,23 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         const auto t_ev = clk::now();
         Status s = eng->evaluate(table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
                                  P.variant, recs.data(), DebugOut{}, st, P.profile, &bs);
-        eval_ms += std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
+        const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
+        eval_ms += ev_ms;
         if (!s.ok()) return s;
+        if (trace) {  // per-round trace (ISYCOS_TRACE=<path>): round, host ms since last eval, eval ms, batch
+            int64_t sw2 = 0, wmax = 0;
+            for (const KsgWin& kw : batch) {
+                sw2 += (int64_t)kw.w * kw.w;
+                wmax = std::max<int64_t>(wmax, kw.w);
+            }
+            const double host = std::chrono::duration<double, std::milli>(t_ev - t_last).count();
+            std::fprintf(trace, "%lld %.4f %.4f %zu %lld %lld\n", (long long)round_no, host, ev_ms, batch.size(),
+                         (long long)sw2, (long long)wmax);
+        }
+        ++round_no;
+        t_last = clk::now();
         for (size_t i = 0; i < batch.size(); ++i) {
-            Entry& e = owners[i].first->cache.map[owners[i].second];
+            Entry& e = *owners[i];
             e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
             e.ready = true;
         }

@@ -1,0 +1,110 @@
+#!/usr/bin/env python
+"""Summarise ncu captures into small committed text files under profiles/.
+
+  python scripts/ncu_summary.py rep  gpurun_out/prof.ncu-rep  profiles/r01_tile4096.md
+  python scripts/ncu_summary.py launches gpurun_out/launches.csv profiles/r01_launches.md
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["Duration", "Elapsed Cycles", "SM Frequency", "Compute (SM) Throughput", "Executed Ipc Active",
+        "Issue Slots Busy", "Issued Warp Per Scheduler", "No Eligible", "Active Warps Per Scheduler",
+        "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction", "Avg. Active Threads Per Warp",
+        "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy", "Grid Size", "Block Size",
+        "Dynamic Shared Memory Per Block", "Branch Efficiency", "Avg. Divergent Branches",
+        "Executed Instructions", "L1/TEX Hit Rate", "L2 Hit Rate", "DRAM Throughput", "Memory Throughput"]
+
+
+def ncu_csv(args):
+    out = subprocess.run(["ncu", *args, "--csv"], capture_output=True, text=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def rep(path, dst):
+    rows = ncu_csv(["-i", path, "--page", "details"])
+    hdr = rows[0]
+    idx = {h: i for i, h in enumerate(hdr)}
+    lines = [f"# ncu --set full summary: `{path.split('/')[-1]}`", ""]
+    by_id = collections.OrderedDict()
+    for r in rows[1:]:
+        by_id.setdefault(r[idx["ID"]], []).append(r)
+    raw = ncu_csv(["-i", path, "--page", "raw"])
+    rhdr = raw[0] if raw else []
+    for kid, rs in by_id.items():
+        lines.append(f"## launch {kid}: `{rs[0][idx['Kernel Name']][:120]}`")
+        lines.append("")
+        lines.append("| metric | unit | value |")
+        lines.append("|---|---|---|")
+        seen = set()
+        for r in rs:
+            m = r[idx["Metric Name"]]
+            if m in KEYS and m not in seen:
+                seen.add(m)
+                lines.append(f"| {m} | {r[idx['Metric Unit']]} | {r[idx['Metric Value']]} |")
+        # dram bytes from the raw page
+        for want in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+                     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum"):
+            if want in rhdr:
+                j = rhdr.index(want)
+                row = raw[2 + int(kid)] if len(raw) > 2 + int(kid) else None
+                if row:
+                    lines.append(f"| {want} | {raw[1][j]} | {row[j]} |")
+        lines.append("")
+    # instruction mix from the source page
+    src = ncu_csv(["-i", path, "--page", "source", "--print-source", "sass"])
+    if len(src) > 2:
+        h = src[1]
+        ix = {k: i for i, k in enumerate(h)}
+        mix = collections.Counter()
+        stall = collections.Counter()
+        tot = stot = 0
+        for r in src[2:]:
+            if len(r) != len(h) or "Source" not in ix:
+                continue
+            s = r[ix["Source"]].strip()
+            if not s:
+                continue
+            toks = s.split()
+            op = (toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]).split(".")[0]
+            n = int(r[ix["Instructions Executed"]] or 0)
+            sm = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+            mix[op] += n
+            stall[op] += sm
+            tot += n
+            stot += sm
+        lines += ["## instruction mix (first launch, warp-level executed) and stall-sample share", "",
+                  "| opcode | % instr | % stall samples |", "|---|---|---|"]
+        for op, n in mix.most_common(16):
+            lines.append(f"| {op} | {100 * n / max(tot, 1):.1f} | {100 * stall[op] / max(stot, 1):.1f} |")
+    open(dst, "w").write("\n".join(lines) + "\n")
+
+
+def launches(path, dst):
+    rows = [r for r in csv.reader(open(path)) if r]
+    hdr = next(r for r in rows if r[0] == "ID")
+    idx = {h: i for i, h in enumerate(hdr)}
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    for r in rows:
+        if r[0] == "ID" or len(r) != len(hdr) or r[idx["Metric Name"]] != "gpu__time_duration.sum":
+            continue
+        name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[idx["Metric Value"]].replace(",", "")) * scale.get(r[idx["Metric Unit"]], 1.0)
+    tot = sum(v[1] for v in agg.values())
+    lines = [f"# launch list summary: `{path.split('/')[-1]}` (ncu --metrics gpu__time_duration.sum, "
+             "cold-cache, serialised: compare shares, not absolutes)", "",
+             "| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
+    for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"| `{k}` | {n} | {us:.1f} | {100 * us / tot:.1f}% | {us / n:.2f} |")
+    open(dst, "w").write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    {"rep": rep, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
