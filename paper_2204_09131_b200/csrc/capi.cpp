@@ -254,7 +254,7 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     P.t_max_idle = opts->t_max_idle;
     P.h = opts->h;
     P.n_chunks = opts->n_chunks;
-    P.lookahead = opts->lookahead > 0 ? opts->lookahead : 256;
+    P.lookahead = opts->lookahead > 0 ? opts->lookahead : 64;
     P.seed = opts->seed;
     P.profile = (opts->flags & ISYCOS_F_PROFILE) != 0;
     // speculation tuning knobs (do not change results)

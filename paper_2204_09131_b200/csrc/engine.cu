@@ -115,9 +115,15 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_KNN_MODE")) knn_mode_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_SORTED")) sorted_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaMalloc(&dsteps_, sizeof(unsigned long long)));
+    ISY_CK(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+    for (int a = 0; a < kAux; ++a) {
+        ISY_CK(cudaStreamCreateWithFlags(&aux_[a], cudaStreamNonBlocking));
+        ISY_CK(cudaEventCreateWithFlags(&join_ev_[a], cudaEventDisableTiming));
+    }
     return Status{};
 }
 
@@ -134,6 +140,11 @@ Engine::~Engine() {
     cudaFreeHost(hstage_);
     cudaFreeHost(hrec_);
     for (auto e : events_) cudaEventDestroy(e);
+    for (int a = 0; a < kAux; ++a) {
+        if (aux_[a]) cudaStreamDestroy(aux_[a]);
+        if (join_ev_[a]) cudaEventDestroy(join_ev_[a]);
+    }
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -213,12 +224,15 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         Status s = ensure_psi(w_max + 1, st);
         if (!s.ok()) return s;
     }
-    // bin windows: small (warp per window) R = 1,2,4,8; sorted-marginal path; brute-force tile R = 2,4
+    // bin windows: small (warp per window) R = 1,2,4,8; sorted-marginal path; brute-force tile R = 2,4,
+    // and tile R = 1 ("latency mode": a CTA per small window, one point per thread) for small classes too
+    // sparse to fill the GPU, where a warp walking 32R points serially would set the round's latency.
     std::vector<int32_t> small[4];
-    std::vector<int32_t> tile[2];
+    std::vector<int32_t> tile[3];
+    static const int kTileRs[3] = {2, 4, 1};
     std::vector<int32_t> sorted;
     std::vector<int64_t> soff;
-    int64_t n_items = 0, n_sitems = 0, spts = 0;
+    int64_t n_items = 0, n_sitems = 0, spts = 0, n_segs = 0, n_mblocks = 0;
     int W2 = 0;
     int64_t pp = 0;
     for (int64_t i = 0; i < n; ++i) {
@@ -227,13 +241,15 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         const int R = small_class_R(w);
         if (R && !(sorted_on_ && w >= sorted_min_w_)) {
             small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
-        } else if (sorted_on_ && w >= sorted_min_w_ && w <= kSortedMaxW) {
+        } else if (sorted_on_ && w >= sorted_min_w_) {
             sorted.push_back((int32_t)i);
             soff.push_back(spts);
             spts += w;
             n_sitems += (w + kSortedPts - 1) / kSortedPts;
+            n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
+            if (w > kSortedMaxW) n_mblocks += (w + kMergePts - 1) / kMergePts;
             int n2 = 1;
-            while (n2 < w) n2 <<= 1;
+            while (n2 < std::min(w, kSortedMaxW)) n2 <<= 1;
             W2 = std::max(W2, n2);
         } else {
             const int tr = tile_R(w);
@@ -241,14 +257,24 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
             n_items += (w + kTileThreads * tr - 1) / (kTileThreads * tr);
         }
     }
+    for (int s = 0; s < 4; ++s) {
+        if (small[s].empty() || (int64_t)small[s].size() >= lat_windows_) continue;
+        for (int32_t q : small[s]) {
+            tile[2].push_back(q);
+            n_items += (wins[q].w + kTileThreads - 1) / kTileThreads;
+        }
+        small[s].clear();
+    }
     int64_t n_lists = (int64_t)sorted.size();
     for (auto& v : small) n_lists += (int64_t)v.size();
     {
-        Status s = ensure_capacity(n, n_items + n_sitems, n_pairs, n_lists + 2 * (int64_t)sorted.size() + 16);
+        Status s = ensure_capacity(n + 1, n_items + n_sitems + n_segs + n_mblocks, n_pairs,
+                                   n_lists + 2 * (int64_t)sorted.size() + 16);
         if (!s.ok()) return s;
     }
-    if (spts > 0 && sscratch_cap_ < spts * 16) {
-        const int64_t c = std::max<int64_t>(spts * 16, sscratch_cap_ * 2);
+    // scratch per sorted point: P2 (8) | OX (4) | YS (4) | TX (4) | TI (4) | TY (4)
+    if (spts > 0 && sscratch_cap_ < spts * 28) {
+        const int64_t c = std::max<int64_t>(spts * 28, sscratch_cap_ * 2);
         cudaFree(sscratch_);
         sscratch_ = nullptr;
         ISY_CK(cudaMalloc(&sscratch_, c));
@@ -262,7 +288,9 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
     const int64_t off_soff = align64(off_slist + (int64_t)sorted.size() * 4);
     const int64_t off_items = align64(off_soff + (int64_t)sorted.size() * 8);
     const int64_t off_sitems = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
-    const int64_t total = align64(off_sitems + n_sitems * (int64_t)sizeof(KsgItem));
+    const int64_t off_segs = align64(off_sitems + n_sitems * (int64_t)sizeof(KsgItem));
+    const int64_t off_mblk = align64(off_segs + n_segs * (int64_t)sizeof(KsgItem));
+    const int64_t total = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
     std::memcpy(hstage_ + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
     std::memcpy(hstage_ + off_wins, wins, n * sizeof(KsgWin));
     int64_t list_off[4];
@@ -277,23 +305,29 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         std::memcpy(hstage_ + off_slist, sorted.data(), sorted.size() * 4);
         std::memcpy(hstage_ + off_soff, soff.data(), soff.size() * 8);
     }
-    int64_t item_off[2];
+    int64_t item_off[3];
     {
         KsgItem* ip = reinterpret_cast<KsgItem*>(hstage_ + off_items);
         int64_t c = 0;
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < 3; ++s) {
             item_off[s] = c;
-            const int tr = s == 0 ? 2 : 4;
+            const int tr = kTileRs[s];
             for (int32_t q : tile[s]) {
                 const int w = wins[q].w;
                 for (int i0 = 0; i0 < w; i0 += kTileThreads * tr) ip[c++] = KsgItem{q, i0};
             }
         }
         KsgItem* sp = reinterpret_cast<KsgItem*>(hstage_ + off_sitems);
+        KsgItem* sg = reinterpret_cast<KsgItem*>(hstage_ + off_segs);
+        KsgItem* mb = reinterpret_cast<KsgItem*>(hstage_ + off_mblk);
+        int64_t cs = 0, cm = 0;
         c = 0;
         for (size_t b = 0; b < sorted.size(); ++b) {
             const int w = wins[sorted[b]].w;
             for (int i0 = 0; i0 < w; i0 += kSortedPts) sp[c++] = KsgItem{(int32_t)b, i0};
+            for (int s0 = 0; s0 < w; s0 += kSortedMaxW) sg[cs++] = KsgItem{(int32_t)b, s0};
+            if (w > kSortedMaxW)
+                for (int i0 = 0; i0 < w; i0 += kMergePts) mb[cm++] = KsgItem{(int32_t)b, i0};
         }
     }
     ISY_CK(cudaMemcpyAsync(dstage_, hstage_, total, cudaMemcpyHostToDevice, st));
@@ -329,14 +363,30 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         }
         return {events_[2 * i], events_[2 * i + 1]};
     };
+    // Launch groups fork onto auxiliary streams after the descriptor copy and join before the record
+    // copy, so independent size classes overlap (a round's latency is the slowest class, not the sum).
+    int n_aux_used = 0;
+    bool forked = false;
     auto launch = [&](int nk, auto&& fn) -> Status {
+        cudaStream_t sg = st;
+        if (n_ksg > 0) {
+            if (!forked) {
+                ISY_CK(cudaEventRecord(fork_ev_, st));
+                forked = true;
+            }
+            sg = aux_[(n_ksg - 1) % kAux];
+            if (n_ksg - 1 < kAux) {
+                ISY_CK(cudaStreamWaitEvent(sg, fork_ev_, 0));
+                n_aux_used = n_ksg;
+            }
+        }
         std::pair<cudaEvent_t, cudaEvent_t> ev{};
         if (profile) {
             ev = ev_pair(n_ksg);
-            ISY_CK(cudaEventRecord(ev.first, st));
+            ISY_CK(cudaEventRecord(ev.first, sg));
         }
-        ISY_CK(fn());
-        if (profile) ISY_CK(cudaEventRecord(ev.second, st));
+        ISY_CK(fn(sg));
+        if (profile) ISY_CK(cudaEventRecord(ev.second, sg));
         ++n_ksg;
         n_launch += nk;
         return Status{};
@@ -348,21 +398,24 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         float2* P2 = reinterpret_cast<float2*>(sscratch_);
         int32_t* OX = reinterpret_cast<int32_t*>(sscratch_ + spts * 8);
         float* YS = reinterpret_cast<float*>(sscratch_ + spts * 12);
-        Status r = launch(2, [&] {
-            return launch_sorted(L, dsl, (int32_t)sorted.size(), dso, P2, OX, YS, W2, dsi, (int32_t)n_sitems, st);
+        float* TX = reinterpret_cast<float*>(sscratch_ + spts * 16);
+        int32_t* TI = reinterpret_cast<int32_t*>(sscratch_ + spts * 20);
+        float* TY = reinterpret_cast<float*>(sscratch_ + spts * 24);
+        const KsgItem* dsg = reinterpret_cast<const KsgItem*>(dstage_ + off_segs);
+        const KsgItem* dmb = reinterpret_cast<const KsgItem*>(dstage_ + off_mblk);
+        Status r = launch(n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
+            return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
+                                 W2, dsi, (int32_t)n_sitems, sg);
         });
         if (!r.ok()) return r;
     }
-    for (int s = 1; s >= 0; --s) {
+    for (int s : {1, 0, 2}) {
         if (tile[s].empty()) continue;
+        const int R = kTileRs[s];
         int64_t cnt = 0;
-        for (int32_t q : tile[s]) {
-            const int tr = s == 0 ? 2 : 4;
-            cnt += (wins[q].w + kTileThreads * tr - 1) / (kTileThreads * tr);
-        }
-        const int R = s == 0 ? 2 : 4;
+        for (int32_t q : tile[s]) cnt += (wins[q].w + kTileThreads * R - 1) / (kTileThreads * R);
         const KsgItem* ip = ditems + item_off[s];
-        Status r = launch(1, [&] { return launch_ksg_tile(L, ip, (int32_t)cnt, R, st); });
+        Status r = launch(1, [&](cudaStream_t sg) { return launch_ksg_tile(L, ip, (int32_t)cnt, R, sg); });
         if (!r.ok()) return r;
     }
     for (int s = 3; s >= 0; --s) {
@@ -370,16 +423,29 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         const int R = 1 << s;
         const int32_t* lp = dlists + list_off[s];
         const int32_t cnt = (int32_t)small[s].size();
-        Status r = launch(1, [&] { return launch_ksg_small(L, lp, cnt, R, st); });
+        Status r = launch(1, [&](cudaStream_t sg) { return launch_ksg_small(L, lp, cnt, R, sg); });
         if (!r.ok()) return r;
     }
+    for (int a = 0; a < std::min(n_aux_used, kAux); ++a) {  // join
+        ISY_CK(cudaEventRecord(join_ev_[a], aux_[a]));
+        ISY_CK(cudaStreamWaitEvent(st, join_ev_[a], 0));
+    }
+    // the step counter rides in the pinned record buffer (slot n), one D2H copy for both
     unsigned long long steps = 0;
-    if (!sorted.empty()) ISY_CK(cudaMemcpyAsync(&steps, dsteps_, sizeof(steps), cudaMemcpyDeviceToHost, st));
-    if (recs_host) {
-        ISY_CK(cudaMemcpyAsync(hrec_, drec_, n * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
-        if (bs) bs->d2h_bytes += n * (int64_t)sizeof(KsgRec);
+    if (!sorted.empty())
+        ISY_CK(cudaMemcpyAsync(reinterpret_cast<char*>(drec_ + n), dsteps_, sizeof(steps), cudaMemcpyDeviceToDevice,
+                               st));
+    if (recs_host || !sorted.empty()) {
+        const int64_t cnt = recs_host ? n + (sorted.empty() ? 0 : 1) : 0;
+        if (recs_host) {
+            ISY_CK(cudaMemcpyAsync(hrec_, drec_, cnt * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
+        } else {
+            ISY_CK(cudaMemcpyAsync(hrec_ + n, drec_ + n, sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
+        }
+        if (bs) bs->d2h_bytes += cnt * (int64_t)sizeof(KsgRec);
     }
     ISY_CK(cudaStreamSynchronize(st));
+    if (!sorted.empty()) std::memcpy(&steps, hrec_ + n, sizeof(steps));
     if (recs_host) std::memcpy(recs_host, hrec_, n * sizeof(KsgRec));
     if (bs) {
         bs->windows += n;

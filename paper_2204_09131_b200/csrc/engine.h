@@ -73,15 +73,18 @@ constexpr int kTileJ = 4096;             // j-tile (points) staged per cp.async.
 int small_class_R(int w);                // 1,2,4,8 for w <= 256; 0 => tile kernel
 int tile_R(int w);                       // points per thread of the tile kernel
 constexpr int kSortedPts = 128;          // points per CTA of the sorted-path scan kernel
-constexpr int kSortedMaxW = 16384;       // sorted path: window sorted in one CTA's SMEM
+constexpr int kSortedMaxW = 16384;       // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
+constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
 
 // Launchers (ksg_kernels.cu).  Return cudaGetLastError().
 cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
 cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st);
-// sorted path: sort kernel (one CTA per window of `list`) then scan kernel over `items` (win = list pos)
-cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, int32_t n_list, const int64_t* soff,
-                          float2* P2, int32_t* OX, float* YS, int W2, const KsgItem* items, int32_t n_items,
-                          cudaStream_t st);
+// sorted path: sort kernel over segments {list pos, start}, XL rank merge over blocks {list pos, start},
+// then the scan kernel over `items` {list pos, first point}
+cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const KsgItem* segs,
+                          int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
+                          float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
+                          int32_t n_items, cudaStream_t st);
 cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, double* lnc,
                               cudaStream_t st);
 cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st);
@@ -168,6 +171,11 @@ private:
     unsigned long long* dsteps_ = nullptr;
     bool sorted_on_ = true;
     int32_t sorted_min_w_ = 257;
+    int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
+    static constexpr int kAux = 4;   // auxiliary streams for overlapping size classes
+    cudaStream_t aux_[kAux] = {};
+    cudaEvent_t fork_ev_ = nullptr;
+    cudaEvent_t join_ev_[kAux] = {};
 };
 
 // ---------------------------------------------------------------- search driver
@@ -180,10 +188,10 @@ struct SearchParams {
     int32_t p = 3;
     double sigma = 0.2;
     int64_t delta_td = 0, delta_bu = 0;
-    int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 256;
+    int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 64;
     int64_t spec_cap_mult = 4;   // BU: speculative climbs pause beyond this many s_min
     int32_t anchor_lookahead = 64;  // BU: climbs started at the predicted re-anchor point
-    int32_t bu_depth = 3;           // BU: iterations of delta-neighbourhood requested per round
+    int32_t bu_depth = 4;           // BU: iterations of delta-neighbourhood requested per round
     uint64_t seed = 0;
     bool profile = false;
 };

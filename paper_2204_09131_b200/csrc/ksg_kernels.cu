@@ -472,28 +472,37 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
 //          monotone on each side of x_i), found by two binary searches with the identical predicate;
 //          n_y likewise on the sorted y.  Bit-identical to the brute-force counts.
 constexpr int kSortedThreads = 128;  // points per CTA of the scan kernel (one point per thread)
+constexpr int kMergeThreads = kMergePts;  // elements per CTA of the XL rank merge
 
-// One CTA per window (w <= kSortedMaxW): bitonic sorts in SMEM of (x, idx) and of y, written to the
-// batch scratch: P2[m] = (x, y) of the m-th point in x order, OX[m] = its original index, YS = sorted y.
+// One CTA per (window, segment of <= kSortedMaxW points): bitonic sorts in SMEM of (x, idx) and of y.
+// A window that is one segment writes the scan layout directly: P2[m] = (x, y) of the m-th point in x
+// order, OX[m] = its original index, YS = sorted y.  Segments of an XL window write sorted runs to
+// TX/TI/TY instead; rank_merge_kernel then places every element by its rank across the runs.
 __global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
-                                   const int64_t* __restrict__ soff, float2* __restrict__ P2,
-                                   int32_t* __restrict__ OX, float* __restrict__ YS, int W2) {
+                                   const int64_t* __restrict__ soff, const KsgItem* __restrict__ segs,
+                                   float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
+                                   float* __restrict__ TX, int32_t* __restrict__ TI, float* __restrict__ TY,
+                                   int W2) {
     extern __shared__ __align__(16) unsigned char sm[];
     float* key = reinterpret_cast<float*>(sm);
     int32_t* pay = reinterpret_cast<int32_t*>(key + W2);
-    const int b = blockIdx.x;
+    const KsgItem sg = segs[blockIdx.x];  // win = position in the sorted list, i0 = segment start
+    const int b = sg.win;
     const int q = list[b];
     const KsgWin W = L.wins[q];
     const int w = W.w;
+    const int s0 = sg.i0;
+    const int len = min(kSortedMaxW, w - s0);
+    const bool whole = (s0 == 0 && len == w);
     int n2 = 1;
-    while (n2 < w) n2 <<= 1;
+    while (n2 < len) n2 <<= 1;
     const float* gx = L.pairs[W.pair].x + W.t0;
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int64_t o = soff[b];
     for (int pass = 0; pass < 2; ++pass) {
         for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-            key[i] = i < w ? (pass == 0 ? gx[i] : gy[i]) : kInf;
-            pay[i] = i;
+            key[i] = i < len ? (pass == 0 ? gx[s0 + i] : gy[s0 + i]) : kInf;
+            pay[i] = s0 + i;
         }
         __syncthreads();
         for (int k = 2; k <= n2; k <<= 1) {
@@ -514,17 +523,68 @@ __global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict_
                 __syncthreads();
             }
         }
-        for (int m = threadIdx.x; m < w; m += blockDim.x) {
-            if (pass == 0) {
-                const int32_t idx = pay[m];
-                P2[o + m] = make_float2(key[m], gy[idx]);
-                OX[o + m] = idx;
+        for (int m = threadIdx.x; m < len; m += blockDim.x) {
+            if (whole) {
+                if (pass == 0) {
+                    const int32_t idx = pay[m];
+                    P2[o + m] = make_float2(key[m], gy[idx]);
+                    OX[o + m] = idx;
+                } else {
+                    YS[o + m] = key[m];
+                }
             } else {
-                YS[o + m] = key[m];
+                if (pass == 0) {
+                    TX[o + s0 + m] = key[m];
+                    TI[o + s0 + m] = pay[m];
+                } else {
+                    TY[o + s0 + m] = key[m];
+                }
             }
         }
         __syncthreads();
     }
+}
+
+// count of elements < v (strict) or <= v in a sorted run s[0..n)
+__device__ __forceinline__ int count_below(const float* s, int n, float v, bool inclusive) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (inclusive ? (s[mid] <= v) : (s[mid] < v)) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// XL windows: element p of run c goes to rank = (p - start(c)) + sum_{c' < c} #{run c' <= v}
+// + sum_{c' > c} #{run c' < v}: a total order (ties by run), so ranks are a permutation.
+__global__ void rank_merge_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
+                                  const int64_t* __restrict__ soff, const KsgItem* __restrict__ blocks,
+                                  float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
+                                  const float* __restrict__ TX, const int32_t* __restrict__ TI,
+                                  const float* __restrict__ TY) {
+    const KsgItem bk = blocks[blockIdx.x];  // win = list position, i0 = first element of this block
+    const int b = bk.win;
+    const KsgWin W = L.wins[list[b]];
+    const int w = W.w;
+    const int p = bk.i0 + threadIdx.x;
+    if (p >= w) return;
+    const int64_t o = soff[b];
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    const int c = p / kSortedMaxW;
+    const int nruns = (w + kSortedMaxW - 1) / kSortedMaxW;
+    const float vx = TX[o + p], vy = TY[o + p];
+    int rx = p - c * kSortedMaxW, ry = rx;
+    for (int c2 = 0; c2 < nruns; ++c2) {
+        if (c2 == c) continue;
+        const int st = c2 * kSortedMaxW;
+        const int n = min(kSortedMaxW, w - st);
+        rx += count_below(TX + o + st, n, vx, c2 < c);
+        ry += count_below(TY + o + st, n, vy, c2 < c);
+    }
+    const int32_t idx = TI[o + p];
+    P2[o + rx] = make_float2(vx, gy[idx]);
+    OX[o + rx] = idx;
+    YS[o + ry] = vy;
 }
 
 // first index in [lo, hi) where pred is false, for pred true...true false...false
@@ -709,6 +769,7 @@ template <int K1>
 cudaError_t tile_k(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, cudaStream_t st) {
     const size_t smem = 2 * (kTileJ + 8) * sizeof(float);
     switch (R) {
+        case 1: ksg_tile_kernel<K1, 1><<<n, kTileThreads, smem, st>>>(L, items, n); break;  // latency mode
         case 2: ksg_tile_kernel<K1, 2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
         case 4: ksg_tile_kernel<K1, 4><<<n, kTileThreads, smem, st>>>(L, items, n); break;
         default: return cudaErrorInvalidValue;
@@ -758,10 +819,12 @@ cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* sof
 }
 }  // namespace
 
-cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, int32_t n_list, const int64_t* soff, float2* P2,
-                          int32_t* OX, float* YS, int W2, const KsgItem* items, int32_t n_items, cudaStream_t st) {
+cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const KsgItem* segs,
+                          int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
+                          float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
+                          int32_t n_items, cudaStream_t st) {
     static_assert(kSortedThreads == kSortedPts, "scan CTA size");
-    if (n_list <= 0) return cudaSuccess;
+    if (n_segs <= 0) return cudaSuccess;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -770,9 +833,14 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, int32_t n_lis
         attr = true;
     }
     const int threads = std::min(1024, std::max(64, W2 / 2));
-    sort_window_kernel<<<n_list, threads, (size_t)W2 * 8, st>>>(L, list, soff, P2, OX, YS, W2);
+    sort_window_kernel<<<n_segs, threads, (size_t)W2 * 8, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (n_mblocks > 0) {
+        rank_merge_kernel<<<n_mblocks, kMergeThreads, 0, st>>>(L, list, soff, mblocks, P2, OX, YS, TX, TI, TY);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st)
 }
 

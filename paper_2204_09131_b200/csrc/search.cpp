@@ -301,13 +301,21 @@ struct Climb {
     bool accepted = false;
     bool finished = false;
     Eval fin{0, 0, 0};
+    int64_t ring_t0 = -1, ring_t1 = -1;  // last depth-speculation request (want_ring)
+    int ring_pf = -1;
 
     // Depth speculation: request every window the next bu_depth iterations could need — the rings
     // N_1..N_D of the delta-neighbourhood (Defs 5.2-5.3, Fig. 4's N_1/N_2) plus their noise extensions —
     // so a climb advances up to bu_depth iterations per round.  Requests only; nothing is consumed.
-    void want_ring(View& v, const SearchParams& P, int64_t hi, int64_t d) const {
+    void want_ring(View& v, const SearchParams& P, int64_t hi, int64_t d) {
         const int D = P.bu_depth;
         if (D <= 1) return;
+        // already requested around this window with the same pruned directions
+        const int pf = (pruned[0] ? 1 : 0) | (pruned[1] ? 2 : 0);
+        if (ring_t0 == t0 && ring_t1 == t1 && ring_pf == pf) return;
+        ring_t0 = t0;
+        ring_t1 = t1;
+        ring_pf = pf;
         for (int a = -D; a <= D; ++a) {
             if (a < 0 && pruned[0]) continue;
             for (int b = -D; b <= D; ++b) {
@@ -463,7 +471,7 @@ struct BuJob {
     void init() { chain = lo_c; }
 
     void ensure_lookahead() {
-        const int la = P->lookahead > 0 ? P->lookahead : 256;
+        const int la = P->lookahead > 0 ? P->lookahead : 64;
         for (int j = 0; j < la; ++j) {
             const int64_t l = chain + (int64_t)j * P->s_min;
             if (l + P->s_min > hi) break;

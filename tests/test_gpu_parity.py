@@ -172,6 +172,17 @@ def test_errors(isy):
         isy.isycos_mi_batch(x, bad, [(0, 64)], 4)
 
 
+def test_sorted_path_segment_boundaries(isy, orc):
+    """Windows at the sorted path's segment boundary (16384 = one SMEM sort; 16385+ = runs + rank merge),
+    with heavy x ties (integer-rounded x) so the run merge must order equal keys consistently."""
+    wl = datagen.cfg2(n=60_000)
+    x, y = wl.series
+    xr = np.round(x * 2).astype(np.float32)
+    W = [(100, 100 + 16384), (7, 7 + 16385), (30_001, 30_001 + 20_001)]
+    check_windows(isy, orc, x, y, W, 4, debug=True, label="segments")
+    check_windows(isy, orc, xr, y, W[1:], 3, debug=True, label="segments ties")
+
+
 def test_large_window_sampled(isy, orc):
     """Full-size XL window (cfg5 s_max = 65,536): sampled per-point outputs against the oracle's
     one-point definition, and the window record against the oracle finish of the GPU's own sums
