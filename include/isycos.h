@@ -87,6 +87,9 @@ typedef struct {
     double wall_ms;        /* wall time of the call */
     int64_t scan_steps;    /* sorted-marginal path: outward k-NN scan steps executed (algorithmic work) */
     int64_t sorted_windows, sorted_points; /* windows / points evaluated on the sorted-marginal path */
+    int64_t brute_point_pairs; /* ordered point pairs of windows evaluated by the brute-force kernels */
+    int64_t search_probes; /* sorted path: binary-search probes (5 searches x ceil(log2 w) per point) */
+    double sorted_kernel_ms, brute_kernel_ms; /* ISYCOS_F_PROFILE: per-path share of kernel_ms */
 } isycos_kernel_stats;
 
 /*

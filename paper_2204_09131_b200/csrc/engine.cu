@@ -62,6 +62,10 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
     s->scan_steps += scan_steps;
     s->sorted_windows += sorted_windows;
     s->sorted_points += sorted_points;
+    s->brute_point_pairs += brute_pairs;
+    s->search_probes += search_probes;
+    s->sorted_kernel_ms += sorted_ms;
+    s->brute_kernel_ms += brute_ms;
 }
 
 // ---------------------------------------------------------------- engine registry (one per device)
@@ -245,7 +249,6 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
             sorted.push_back((int32_t)i);
             soff.push_back(spts);
             spts += w;
-            n_sitems += (w + kSortedPts - 1) / kSortedPts;
             n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
             if (w > kSortedMaxW) n_mblocks += (w + kMergePts - 1) / kMergePts;
             int n2 = 1;
@@ -265,6 +268,10 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         }
         small[s].clear();
     }
+    // sorted scan: 1024 points per CTA when the batch fills the GPU (better lane balance in the per-warp
+    // work queues), else 256 (more CTAs per window: latency-bound rounds)
+    const int ppc = spts >= (int64_t)148 * 8 * 1024 ? 1024 : 256;
+    for (int32_t q : sorted) n_sitems += (wins[q].w + ppc - 1) / ppc;
     int64_t n_lists = (int64_t)sorted.size();
     for (auto& v : small) n_lists += (int64_t)v.size();
     {
@@ -324,7 +331,7 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         c = 0;
         for (size_t b = 0; b < sorted.size(); ++b) {
             const int w = wins[sorted[b]].w;
-            for (int i0 = 0; i0 < w; i0 += kSortedPts) sp[c++] = KsgItem{(int32_t)b, i0};
+            for (int i0 = 0; i0 < w; i0 += ppc) sp[c++] = KsgItem{(int32_t)b, i0};
             for (int s0 = 0; s0 < w; s0 += kSortedMaxW) sg[cs++] = KsgItem{(int32_t)b, s0};
             if (w > kSortedMaxW)
                 for (int i0 = 0; i0 < w; i0 += kMergePts) mb[cm++] = KsgItem{(int32_t)b, i0};
@@ -350,11 +357,24 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
     L.variant = variant;
     L.knn_mode = knn_mode_;
     L.two = 2;
+    L.sorted_ppc = ppc;
     const int32_t* dlists = reinterpret_cast<const int32_t*>(dstage_ + off_lists);
     const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dstage_ + off_items);
 
     // launches: biggest work first so the small classes fill the tail
     int n_launch = 0, n_ksg = 0;
+    std::vector<int> launch_cls;  // 0 sorted-marginal group, 1 brute-force launch
+    // algorithmic work: brute-force ordered pairs; sorted path binary-search probes (5 searches per point)
+    int64_t brute_pairs = 0, probes = 0;
+    for (int s = 0; s < 4; ++s)
+        for (int32_t q : small[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
+    for (int s = 0; s < 3; ++s)
+        for (int32_t q : tile[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
+    for (int32_t q : sorted) {
+        int lg = 0;
+        while ((1 << lg) < wins[q].w) ++lg;
+        probes += (int64_t)wins[q].w * 5 * lg;
+    }
     auto ev_pair = [&](int i) -> std::pair<cudaEvent_t, cudaEvent_t> {
         while ((int)events_.size() < 2 * (i + 1)) {
             cudaEvent_t e;
@@ -403,6 +423,7 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         float* TY = reinterpret_cast<float*>(sscratch_ + spts * 24);
         const KsgItem* dsg = reinterpret_cast<const KsgItem*>(dstage_ + off_segs);
         const KsgItem* dmb = reinterpret_cast<const KsgItem*>(dstage_ + off_mblk);
+        launch_cls.push_back(0);
         Status r = launch(n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
                                  W2, dsi, (int32_t)n_sitems, sg);
@@ -415,6 +436,7 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         int64_t cnt = 0;
         for (int32_t q : tile[s]) cnt += (wins[q].w + kTileThreads * R - 1) / (kTileThreads * R);
         const KsgItem* ip = ditems + item_off[s];
+        launch_cls.push_back(1);
         Status r = launch(1, [&](cudaStream_t sg) { return launch_ksg_tile(L, ip, (int32_t)cnt, R, sg); });
         if (!r.ok()) return r;
     }
@@ -423,6 +445,7 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         const int R = 1 << s;
         const int32_t* lp = dlists + list_off[s];
         const int32_t cnt = (int32_t)small[s].size();
+        launch_cls.push_back(1);
         Status r = launch(1, [&](cudaStream_t sg) { return launch_ksg_small(L, lp, cnt, R, sg); });
         if (!r.ok()) return r;
     }
@@ -456,11 +479,17 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         bs->scan_steps += (int64_t)steps;
         bs->sorted_windows += (int64_t)sorted.size();
         bs->sorted_points += spts;
+        bs->brute_pairs += brute_pairs;
+        bs->search_probes += probes;
         if (profile) {
             for (int i = 0; i < n_ksg; ++i) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, events_[2 * i], events_[2 * i + 1]);
                 bs->kernel_ms += ms;
+                if (launch_cls[i] == 0)
+                    bs->sorted_ms += ms;
+                else
+                    bs->brute_ms += ms;
             }
         }
     }

@@ -64,6 +64,8 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t variant;
     int32_t knn_mode;        // small-window kNN insertion: 1 branch-free network, 0 guarded
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
+    int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
+    int32_t pad2_;
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -72,7 +74,7 @@ constexpr int kTileThreads = 256;        // threads per CTA of the tile kernel
 constexpr int kTileJ = 4096;             // j-tile (points) staged per cp.async.bulk round
 int small_class_R(int w);                // 1,2,4,8 for w <= 256; 0 => tile kernel
 int tile_R(int w);                       // points per thread of the tile kernel
-constexpr int kSortedPts = 128;          // points per CTA of the sorted-path scan kernel
+constexpr int kSortedPts = 1024;         // max points per CTA of the sorted-path scan kernel (4 warps)
 constexpr int kSortedMaxW = 16384;       // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
 constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
 
@@ -109,6 +111,8 @@ struct DebugOut {
 struct BatchStats {
     int64_t windows = 0, point_pairs = 0, launches = 0, ksg_launches = 0, rounds = 0;
     int64_t scan_steps = 0, sorted_windows = 0, sorted_points = 0;
+    int64_t brute_pairs = 0, search_probes = 0;
+    double sorted_ms = 0.0, brute_ms = 0.0;
     double kernel_ms = 0.0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     double host_ms = 0.0, wall_ms = 0.0;

@@ -474,6 +474,41 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
 constexpr int kSortedThreads = 128;  // points per CTA of the scan kernel (one point per thread)
 constexpr int kMergeThreads = kMergePts;  // elements per CTA of the XL rank merge
 
+// Order-preserving map of float bits to unsigned (finite values; -0 sorts just before +0, equal as floats).
+__device__ __forceinline__ unsigned sortable(float f) {
+    const unsigned u = __float_as_uint(f);
+    return u ^ ((u >> 31) ? 0xffffffffu : 0x80000000u);
+}
+__device__ __forceinline__ float unsortable(unsigned s) {
+    return __uint_as_float(s ^ ((s >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
+// In-SMEM bitonic sort of n2 (power of two) keys, ascending.  Exchange steps with stride j <= 32 stay inside
+// one warp's 64-key block (for every t a warp handles), so they only need __syncwarp; wider steps, and the
+// step before one, need the CTA barrier.
+template <typename K>
+__device__ __forceinline__ void bitonic_smem(K* key, int n2) {
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
+                const int i = 2 * t - (t & (j - 1));
+                const int ixj = i + j;
+                const K a = key[i], c = key[ixj];
+                const bool up = (i & k) == 0;
+                const bool sw = up ? (a > c) : (a < c);
+                key[i] = sw ? c : a;
+                key[ixj] = sw ? a : c;
+            }
+            const int next_j = j > 1 ? (j >> 1) : k;  // first stride of the next phase is k (= 2k / 2)
+            if (j > 32 || next_j > 32)
+                __syncthreads();
+            else
+                __syncwarp();
+        }
+    }
+    __syncthreads();
+}
+
 // One CTA per (window, segment of <= kSortedMaxW points): bitonic sorts in SMEM of (x, idx) and of y.
 // A window that is one segment writes the scan layout directly: P2[m] = (x, y) of the m-th point in x
 // order, OX[m] = its original index, YS = sorted y.  Segments of an XL window write sorted runs to
@@ -484,8 +519,6 @@ __global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict_
                                    float* __restrict__ TX, int32_t* __restrict__ TI, float* __restrict__ TY,
                                    int W2) {
     extern __shared__ __align__(16) unsigned char sm[];
-    float* key = reinterpret_cast<float*>(sm);
-    int32_t* pay = reinterpret_cast<int32_t*>(key + W2);
     const KsgItem sg = segs[blockIdx.x];  // win = position in the sorted list, i0 = segment start
     const int b = sg.win;
     const int q = list[b];
@@ -499,49 +532,36 @@ __global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict_
     const float* gx = L.pairs[W.pair].x + W.t0;
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int64_t o = soff[b];
-    for (int pass = 0; pass < 2; ++pass) {
-        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-            key[i] = i < len ? (pass == 0 ? gx[s0 + i] : gy[s0 + i]) : kInf;
-            pay[i] = s0 + i;
+    // pass 0: x with the index packed into one 64-bit word (sortable float bits << 32 | index): one
+    // compare/swap per exchange, ties broken by index.  pass 1: y keys alone (32-bit).
+    unsigned long long* k64 = reinterpret_cast<unsigned long long*>(sm);
+    unsigned* k32 = reinterpret_cast<unsigned*>(sm);
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        k64[i] = i < len ? ((unsigned long long)sortable(gx[s0 + i]) << 32) | (unsigned)(s0 + i) : ~0ull;
+    __syncthreads();
+    bitonic_smem(k64, n2);
+    for (int m = threadIdx.x; m < len; m += blockDim.x) {
+        const unsigned long long v = k64[m];
+        const float xv = unsortable((unsigned)(v >> 32));
+        const int32_t idx = (int32_t)(v & 0xffffffffu);
+        if (whole) {
+            P2[o + m] = make_float2(xv, gy[idx]);
+            OX[o + m] = idx;
+        } else {
+            TX[o + s0 + m] = xv;
+            TI[o + s0 + m] = idx;
         }
-        __syncthreads();
-        for (int k = 2; k <= n2; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
-                    const int i = 2 * t - (t & (j - 1));
-                    const int ixj = i + j;
-                    const float a = key[i], c = key[ixj];
-                    const bool up = (i & k) == 0;
-                    if (up ? (a > c) : (a < c)) {
-                        key[i] = c;
-                        key[ixj] = a;
-                        const int32_t pa = pay[i];
-                        pay[i] = pay[ixj];
-                        pay[ixj] = pa;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        for (int m = threadIdx.x; m < len; m += blockDim.x) {
-            if (whole) {
-                if (pass == 0) {
-                    const int32_t idx = pay[m];
-                    P2[o + m] = make_float2(key[m], gy[idx]);
-                    OX[o + m] = idx;
-                } else {
-                    YS[o + m] = key[m];
-                }
-            } else {
-                if (pass == 0) {
-                    TX[o + s0 + m] = key[m];
-                    TI[o + s0 + m] = pay[m];
-                } else {
-                    TY[o + s0 + m] = key[m];
-                }
-            }
-        }
-        __syncthreads();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) k32[i] = i < len ? sortable(gy[s0 + i]) : ~0u;
+    __syncthreads();
+    bitonic_smem(k32, n2);
+    for (int m = threadIdx.x; m < len; m += blockDim.x) {
+        const float yv = unsortable(k32[m]);
+        if (whole)
+            YS[o + m] = yv;
+        else
+            TY[o + s0 + m] = yv;
     }
 }
 
@@ -616,12 +636,20 @@ __device__ __forceinline__ int lower_bound_f(const float* s, int w, float v) {
 }
 __device__ __forceinline__ int left_bound_f(const float* s, int m, float v, float eps) { return left_bound(s, m, v, eps); }
 
+// Scan kernel: a CTA owns kSortedPts consecutive x-sorted points, each warp a contiguous quarter.
+// Phase A (k-NN scan) runs a warp-local work queue: a lane that finishes its point takes the next one
+// (ballot + popc), so warps do not idle on their slowest lane (per-point scan lengths vary several-fold
+// with the local density ratio f_x/f_y).  The step itself is branch-free (select the nearer side, one
+// predicated load).  Phase B (binary-search counts, digamma/log terms) is uniform per point.
 template <int K1>
 __global__ void __launch_bounds__(kSortedThreads)
     sorted_knn_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
                       const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
                       const KsgItem* __restrict__ items) {
-    const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list
+    const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
+    const int kPerWarp = ppc / (kSortedThreads / 32);
+    __shared__ float eps_s[kSortedPts];
+    const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list, it.i0 = first point
     const int b = it.win;
     const int q = list[b];
     const int w = L.wins[q].w;
@@ -629,79 +657,145 @@ __global__ void __launch_bounds__(kSortedThreads)
     const float2* P2 = P2g + o;
     const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
     const float* YS = YSg + o;
-    const int m = it.i0 + threadIdx.x;
-    long long sp = 0, sl = 0;
-    int z = 0;
+    const int cta0 = it.i0;
+    const int cta_n = min(ppc, w - cta0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wb = warp * kPerWarp;
+    const int we = min(wb + kPerWarp, cta_n);
+    const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long steps = 0;
-    if (m < w) {
+
+    // ---- phase A: exact k-NN radius by outward scan in x order (a3)
+    // Blocked scan: each iteration visits the next 4 candidates on each side (independent loads).  A side
+    // stops once the farthest candidate it visited has |dx| >= r_{k+1}: every unvisited candidate beyond
+    // it has a larger |dx| (x-sorted, fl monotone), hence d_ij >= r_{k+1}, and cannot change eps.
+    constexpr int B = 4;
+    int mloc = wb + lane;
+    bool act = mloc < we;
+    int next = wb + 32;
+    float xi = 0.f, yi = 0.f;
+    int lj = 0, rj = 0;  // next unvisited index on each side
+    bool lact = false, ract = false;
+    float rk[K1];
+    auto start = [&](int ml) {
+        const int m = cta0 + ml;
         const float2 me = P2[m];
-        const float xi = me.x, yi = me.y;
-        float rk[K1];
+        xi = me.x;
+        yi = me.y;
         rk[0] = 0.0f;  // self: d_ii = 0
 #pragma unroll
         for (int t = 1; t < K1; ++t) rk[t] = kInf;
-        // a3: outward scan in x order
-        int l = m - 1, r = m + 1;
-        float2 pl = l >= 0 ? P2[l] : make_float2(0.f, 0.f);
-        float2 pr = r < w ? P2[r] : make_float2(0.f, 0.f);
-        float dl = l >= 0 ? xi - pl.x : kInf;  // >= 0: sorted ascending
-        float dr = r < w ? pr.x - xi : kInf;
-        for (;;) {
-            const float dmin = fminf(dl, dr);
-            if (!(dmin < rk[K1 - 1])) break;
-            float d;
-            if (dl <= dr) {
-                d = fmaxf(dl, fabsf(yi - pl.y));
-                --l;
-                if (l >= 0) {
-                    pl = P2[l];
-                    dl = xi - pl.x;
-                } else {
-                    dl = kInf;
+        lj = m - 1;
+        rj = m + 1;
+        lact = lj >= 0;
+        ract = rj < w;
+    };
+    auto visit = [&](const float (&d)[B]) {
+        const float mn = fminf(fminf(d[0], d[1]), fminf(d[2], d[3]));
+        if (mn < rk[K1 - 1]) {
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                if (d[u] < rk[K1 - 1]) topk_insert<K1>(rk, d[u]);
+        }
+    };
+    if (act) start(mloc);
+    while (__any_sync(0xffffffffu, act)) {
+        bool fin = false;
+        if (act) {
+            if (lact) {
+                float d[B], far = 0.f;
+#pragma unroll
+                for (int u = 0; u < B; ++u) {
+                    const int j = lj - u;
+                    if (j >= 0) {
+                        const float2 c = P2[j];
+                        const float dx = xi - c.x;  // >= 0: ascending order
+                        d[u] = fmaxf(dx, fabsf(yi - c.y));
+                        far = dx;
+                    } else {
+                        d[u] = kInf;
+                    }
                 }
-            } else {
-                d = fmaxf(dr, fabsf(yi - pr.y));
-                ++r;
-                if (r < w) {
-                    pr = P2[r];
-                    dr = pr.x - xi;
+                visit(d);
+                steps += min(B, lj + 1);
+                lj -= B;
+                lact = lj >= 0 && far < rk[K1 - 1];
+            }
+            if (ract) {
+                float d[B], far = 0.f;
+#pragma unroll
+                for (int u = 0; u < B; ++u) {
+                    const int j = rj + u;
+                    if (j < w) {
+                        const float2 c = P2[j];
+                        const float dx = c.x - xi;
+                        d[u] = fmaxf(dx, fabsf(yi - c.y));
+                        far = dx;
+                    } else {
+                        d[u] = kInf;
+                    }
+                }
+                visit(d);
+                steps += min(B, w - rj);
+                rj += B;
+                ract = rj < w && far < rk[K1 - 1];
+            }
+            if (!lact && !ract) {
+                fin = true;
+                eps_s[mloc] = rk[K1 - 1];
+            }
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, fin);
+        if (fm) {
+            if (fin) {
+                const int idx = next + __popc(fm & lt_mask);
+                if (idx < we) {
+                    mloc = idx;
+                    start(mloc);
                 } else {
-                    dr = kInf;
+                    act = false;
                 }
             }
-            ++steps;
-            if (d < rk[K1 - 1]) topk_insert<K1>(rk, d);
+            next += __popc(fm);
         }
-        const float eps = rk[K1 - 1];
-        // a4: interval counts by binary search with the identical predicates
+    }
+    __syncthreads();
+
+    // ---- phase B: interval counts by binary search with the identical predicates (a4) and terms (a5)
+    long long sp = 0, sl = 0;
+    int z = 0;
+    const int64_t dbg = L.wins[q].dbg_off;
+    for (int ml = threadIdx.x; ml < cta_n; ml += kSortedThreads) {
+        const int m = cta0 + ml;
+        const float2 me = P2[m];
+        const float xv = me.x, yv = me.y;
+        const float eps = eps_s[ml];
         int nx = 0, ny = 0;
         if (eps > 0.0f) {
             // x: left part [0, m] uses fl(x_i - x_j) < eps, right part [m, w) uses fl(x_j - x_i) < eps
             int lo = 0, hi = m;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (xi - XS[2 * mid] < eps) hi = mid; else lo = mid + 1;
+                if (xv - XS[2 * mid] < eps) hi = mid; else lo = mid + 1;
             }
             const int Lx = lo;
             lo = m;
             hi = w;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (XS[2 * mid] - xi < eps) lo = mid + 1; else hi = mid;
+                if (XS[2 * mid] - xv < eps) lo = mid + 1; else hi = mid;
             }
             nx = lo - Lx - 1;
-            const int p = lower_bound_f(YS, w, yi);
-            const int Ly = left_bound_f(YS, p, yi, eps);
-            const int Ry = right_bound(YS, p, w, yi, eps);
+            const int p = lower_bound_f(YS, w, yv);
+            const int Ly = left_bound_f(YS, p, yv, eps);
+            const int Ry = right_bound(YS, p, w, yv, eps);
             ny = Ry - Ly - 1;
         }
-        // a5: per-point terms
-        sp = L.psiq[nx + 1] + L.psiq[ny + 1];
+        sp += L.psiq[nx + 1] + L.psiq[ny + 1];
         if (eps > 0.0f)
-            sl = q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
+            sl += q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
         else
-            z = 1;
-        const int64_t dbg = L.wins[q].dbg_off;
+            z += 1;
         if (dbg >= 0) {
             const int i = OXg[o + m];
             if (L.dbg_eps) L.dbg_eps[dbg + i] = eps;
@@ -709,7 +803,7 @@ __global__ void __launch_bounds__(kSortedThreads)
             if (L.dbg_ny) L.dbg_ny[dbg + i] = ny;
         }
     }
-    const int ntiles = (w + kSortedThreads - 1) / kSortedThreads;
+    const int ntiles = (w + ppc - 1) / ppc;
     cta_finish<kSortedThreads>(L, q, w, ntiles, sp, sl, z, steps);
 }
 
@@ -823,7 +917,7 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
                           int32_t n_items, cudaStream_t st) {
-    static_assert(kSortedThreads == kSortedPts, "scan CTA size");
+    static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
     if (n_segs <= 0) return cudaSuccess;
     static bool attr = false;
     if (!attr) {

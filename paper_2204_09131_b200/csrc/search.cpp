@@ -328,7 +328,7 @@ struct Climb {
         if (!(P.noise && d > P.k)) return;
         for (int a = -(D - 1); a <= D - 1; ++a) {
             const int64_t l0 = t0 + a * d - d, r0 = t1 + a * d;
-            if (!pruned[0] && l0 >= lo) v.want(l0, l0 + d);
+            if (!pruned[0] && l0 >= lo && l0 + d <= hi) v.want(l0, l0 + d);
             if (!pruned[1] && r0 >= lo && r0 + d <= hi) v.want(r0, r0 + d);
         }
     }
@@ -627,7 +627,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
-    double eval_ms = 0.0;
+    double eval_ms = 0.0, adv_ms = 0.0, bu_ms = 0.0;
     int64_t round_no = 0;
     std::FILE* trace = nullptr;
     if (const char* tp = std::getenv("ISYCOS_TRACE")) trace = std::fopen(tp, "a");
@@ -677,10 +677,14 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         }
         if (active.empty()) break;
         // advance every job
+        const auto t_adv = clk::now();
         for (auto& pw : active) {
             for (auto& j : pw->td) j.advance();
+            const auto t_bu = clk::now();
             for (auto& j : pw->bu) j.advance();
+            bu_ms += std::chrono::duration<double, std::milli>(clk::now() - t_bu).count();
         }
+        adv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_adv).count();
         // retire finished pairs
         for (size_t i = 0; i < active.size();) {
             PairWork* pw = active[i].get();
@@ -725,7 +729,11 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             pw->slot = (int32_t)table.size();
             table.push_back(pw->ptrs);
             for (uint64_t k : pw->cache.pending) {
-                batch.push_back(KsgWin{key_t0(k), (int32_t)key_w(k), pw->slot, -1});
+                const int64_t t0 = key_t0(k), w = key_w(k);
+                if (t0 < 0 || t0 + w > n || w <= P.k)  // never hand the kernels an out-of-range window
+                    return make_err(ISYCOS_E_RANGE, "internal: search requested window [" + std::to_string(t0) +
+                                                        ", " + std::to_string(t0 + w) + ")");
+                batch.push_back(KsgWin{t0, (int32_t)w, pw->slot, -1});
                 owners.push_back(pw->cache.map.find(k));
             }
             pw->cache.pending.clear();
@@ -785,6 +793,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         bs.wall_ms = wall;
         bs.host_ms = wall - eval_ms;
         bs.add_to(&stats->kernel);
+        if (trace)
+            std::fprintf(trace, "# host: advance %.3f ms (BU %.3f), other %.3f ms, eval %.3f ms, rounds %lld\n", adv_ms,
+                         bu_ms, wall - eval_ms - adv_ms, eval_ms, (long long)round_no);
     }
     return Status{};
 }

@@ -58,17 +58,29 @@ def rep(path, dst):
         lines.append("")
     # instruction mix from the source page
     src = ncu_csv(["-i", path, "--page", "source", "--print-source", "sass"])
-    if len(src) > 2:
-        h = src[1]
+    # one section per kernel: ["Kernel Name", name], header row, data rows
+    sections = []
+    for r in src:
+        if r and r[0] == "Kernel Name":
+            sections.append([r[1] if len(r) > 1 else "?", None, []])
+        elif sections and sections[-1][1] is None:
+            sections[-1][1] = r
+        elif sections:
+            sections[-1][2].append(r)
+    for name, h, rows in sections:
+        if not h:
+            continue
         ix = {k: i for i, k in enumerate(h)}
+        if "Source" not in ix or "Instructions Executed" not in ix:
+            continue
         mix = collections.Counter()
         stall = collections.Counter()
         tot = stot = 0
-        for r in src[2:]:
-            if len(r) != len(h) or "Source" not in ix:
+        for r in rows:
+            if len(r) != len(h):
                 continue
             s = r[ix["Source"]].strip()
-            if not s:
+            if not s or not r[ix["Instructions Executed"]].isdigit():
                 continue
             toks = s.split()
             op = (toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]).split(".")[0]
@@ -78,10 +90,11 @@ def rep(path, dst):
             stall[op] += sm
             tot += n
             stot += sm
-        lines += ["## instruction mix (first launch, warp-level executed) and stall-sample share", "",
+        lines += [f"## instruction mix of `{name[:90]}` (warp-level executed) and stall-sample share", "",
                   "| opcode | % instr | % stall samples |", "|---|---|---|"]
         for op, n in mix.most_common(16):
             lines.append(f"| {op} | {100 * n / max(tot, 1):.1f} | {100 * stall[op] / max(stot, 1):.1f} |")
+        lines.append("")
     open(dst, "w").write("\n".join(lines) + "\n")
 
 

@@ -1,0 +1,68 @@
+"""CPU tests of the product's batched, speculative search driver (csrc/search.cpp).
+
+The driver is linked with a stub engine that evaluates every requested window with the oracle
+(tests/native/driver_harness.cpp), so what is checked here — without a GPU — is the driver logic
+itself: the resumable TD/BU state machines, TD grid speculation, BU lookahead/depth/anchor
+speculation, the window cache and the chunk merge must reproduce the sequential oracle search
+exactly (result windows and algorithm-level counters), for every speculation setting.
+"""
+import os
+import sys
+
+import pytest
+
+import datagen
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "native"))
+
+
+@pytest.fixture(scope="module")
+def hz():
+    import harness
+
+    harness.build()
+    return harness
+
+
+def check(hz, orc, wl, series=None, pairs=None, label="", spec=None, **kw):
+    series = wl.series if series is None else series
+    pairs = wl.pairs if pairs is None else pairs
+    ores, ost = orc.search(series, pairs, orc.make_params(wl.search, **kw))
+    sc = datagen.SearchConfig(**{**wl.search.__dict__, **kw})
+    res, st, _, _ = hz.search(series, pairs, sc, **(spec or {}))
+    assert res == ores, f"{label}: results differ"
+    for f, v in ost.items():
+        assert st[f] == v, f"{label}: {f} driver {st[f]} oracle {v}"
+    return res, st
+
+
+@pytest.mark.parametrize("method", [1, 2, 3])
+@pytest.mark.parametrize("noise", [False, True])
+def test_cfg1_driver_equals_oracle(hz, orc, method, noise):
+    check(hz, orc, datagen.cfg1(), method=method, noise=noise, label=f"m{method} n{noise}")
+
+
+@pytest.mark.parametrize("spec", [dict(lookahead=1), dict(lookahead=3, bu_depth=1), dict(bu_depth=2),
+                                  dict(bu_depth=6, anchor=0), dict(spec_cap=0, anchor=128),
+                                  dict(lookahead=500, spec_cap=1)])
+def test_speculation_settings_do_not_change_results(hz, orc, spec):
+    check(hz, orc, datagen.cfg1(), spec=spec, label=str(spec))
+
+
+def test_chunks_and_params(hz, orc):
+    wl = datagen.cfg1()
+    for kw in (dict(n_chunks=4), dict(delta_td=24, delta_bu=7), dict(sizes=[512, 200, 64], method=1),
+               dict(k=8, sigma=0.3), dict(t_max_idle=0, h=1), dict(p=1, seed=123)):
+        check(hz, orc, wl, label=str(kw), **kw)
+
+
+def test_cfg2_prefix(hz, orc):
+    wl = datagen.cfg2()
+    ser = [s[:12_000] for s in wl.series]
+    check(hz, orc, wl, series=ser, label="cfg2 prefix", s_max=2048)
+
+
+def test_multi_pair_instance(hz, orc):
+    wl = datagen.cfg4(n=8000, n_series=4, n_planted=1)
+    pairs = [(a, b, 40 + i) for i, (a, b) in enumerate(wl.pairs)]
+    check(hz, orc, wl, pairs=pairs, label="cfg4 instance", s_max=1024)
