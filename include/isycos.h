@@ -32,8 +32,13 @@
  *   KSG-1 (variant 0, default; north star):
  *     n_x(i) = #{ j != i : |fl(x_i - x_j)| < eps_i },  n_y likewise (strict)
  *     I = psi(k) + psi(w) - < psi(n_x + 1) + psi(n_y + 1) >
- *   KSG-2 (variant 1, Eq. 2 literal): reserved; returns ISYCOS_E_INVAL in this
- *     build (the oracle implements it; GPU kernel is SURVEY §8(f) NEXT-1).
+ *   KSG-2 (variant 1, Eq. 2 literal, text P:669, example P:671):
+ *     kNN(i) = the first k of j != i in ascending (d_ij, j) order (tie: smaller index)
+ *     d_x(i) = max_{j in kNN(i)} |fl(x_i - x_j)|,  d_y likewise
+ *     n_x(i) = #{ j != i : |fl(x_i - x_j)| <= d_x(i) },  n_y likewise (closed, >= k)
+ *     I = psi(k) - 1/k + psi(w) - < psi(n_x) + psi(n_y) >
+ *     (H and nmi use the KSG-1 radius eps_i for both variants; dbg_nx/dbg_ny report
+ *     the variant's own counts.)
  *   Entropy (Eq. 13 read as the Kozachenko-Leonenko joint entropy, G2):
  *     H = psi(w) - psi(k) + (2/w) * sum_i ln(2 eps_i);  H = -inf if any eps_i == 0
  *   Normalized MI (Eq. 12): nmi = clamp(I/H, 0, 1); if any eps_i == 0 or
@@ -68,6 +73,8 @@ enum {
 
 /* flags */
 #define ISYCOS_F_PROFILE 1u /* record CUDA events around every KSG kernel; fills *_kernel_ms */
+#define ISYCOS_F_BRUTE 2u   /* route every window to the brute-force kernels (no sorted-marginal path);
+                               results are bit-identical either way — an A/B and test knob */
 
 /* Half-open window [t0, t1) of a series pair (Defs 3.2, 3.4). */
 typedef struct {
@@ -107,12 +114,12 @@ int isycos_mi_batch(const float* x, const float* y, int64_t n, const isycos_wind
 
 /* Optional outputs / controls of isycos_mi_batch_ex.  Zero-initialise, then set fields. */
 typedef struct {
-    int32_t variant;        /* 0 = KSG-1 (only value accepted in this build) */
+    int32_t variant;        /* 0 = KSG-1 (default), 1 = KSG-2; anything else: E_INVAL */
     uint32_t flags;         /* ISYCOS_F_* */
     void* stream;           /* cudaStream_t to run on; NULL = the library's own stream */
     double* out_h;          /* [n_windows] KL joint entropy H (nats) */
     double* out_nmi;        /* [n_windows] normalized MI */
-    int64_t* out_sum_psi_q; /* [n_windows] sum_i q(psi(n_x+1)) + q(psi(n_y+1)), q(v) = rint(v*2^32) */
+    int64_t* out_sum_psi_q; /* [n_windows] sum_i q(psi(n_x+1)) + q(psi(n_y+1)) (KSG-2: q(psi(n_x)) + q(psi(n_y))), q(v) = rint(v*2^32) */
     int64_t* out_sum_log_q; /* [n_windows] sum_{eps_i>0} q(LN(2 eps_i)) */
     int32_t* out_zero_eps;  /* [n_windows] #{i : eps_i == 0} */
     float* dbg_eps;         /* [sum w] per-point eps_i, windows concatenated in input order */
@@ -149,7 +156,7 @@ typedef struct {
 typedef struct {
     double sigma;         /* correlation threshold on normalized MI (default 0.2) */
     int32_t method;       /* 1 = TD, 2 = BU, 3 = both (results tagged per method) */
-    int32_t variant;      /* 0 = KSG-1 */
+    int32_t variant;      /* 0 = KSG-1 (default), 1 = KSG-2 (Eq. 2 literal) */
     int64_t delta_td;     /* TD sliding step; 0 => max(1, s/4) per layer */
     int64_t delta_bu;     /* BU neighbour step; 0 => max(1, s_min/3) */
     int32_t t_max_idle;   /* Alg. 2 idle budget (loop while idle <= T_maxIdle, G5) */

@@ -89,8 +89,8 @@ extern "C" int isycos_mi_batch_ex(const float* x, const float* y, int64_t n, con
     if (n_windows < 0) return fail(make_err(ISYCOS_E_INVAL, "n_windows < 0"));
     isycos_mi_opts o{};
     if (opts) o = *opts;
-    if (o.variant != 0)
-        return fail(make_err(ISYCOS_E_INVAL, "variant 1 (KSG-2) has no GPU kernel in this build (oracle only)"));
+    if (o.variant != 0 && o.variant != 1)
+        return fail(make_err(ISYCOS_E_INVAL, "variant must be 0 (KSG-1) or 1 (KSG-2)"));
     if (n_windows == 0) return ok();
 
     Status s;
@@ -176,7 +176,7 @@ extern "C" int isycos_mi_batch_ex(const float* x, const float* y, int64_t n, con
     }
     std::vector<KsgRec> recs(n_windows);
     s = eng->evaluate(&pp, 1, wins.data(), n_windows, k, o.variant, recs.data(), dbg, st,
-                      (o.flags & ISYCOS_F_PROFILE) != 0, &bs);
+                      o.flags, &bs);
     if (!s.ok()) {
         cleanup();
         return fail(s);
@@ -256,7 +256,7 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     P.n_chunks = opts->n_chunks;
     P.lookahead = opts->lookahead > 0 ? opts->lookahead : 64;
     P.seed = opts->seed;
-    P.profile = (opts->flags & ISYCOS_F_PROFILE) != 0;
+    P.flags = opts->flags;
     // speculation tuning knobs (do not change results)
     if (const char* e = std::getenv("ISYCOS_BU_DEPTH")) P.bu_depth = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_ANCHOR")) P.anchor_lookahead = std::atoi(e);
@@ -264,7 +264,7 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     if (const char* e = std::getenv("ISYCOS_LOOKAHEAD")) P.lookahead = std::atoi(e);
     auto bad = [&](const char* m) { return fail(make_err(ISYCOS_E_INVAL, m)); };
     if (k < 1 || k > ISYCOS_MAX_K) return bad("k must be in [1, 16]");
-    if (P.variant != 0) return bad("variant 1 (KSG-2) has no GPU kernel in this build (oracle only)");
+    if (P.variant != 0 && P.variant != 1) return bad("variant must be 0 (KSG-1) or 1 (KSG-2)");
     if (P.s_min < 2 || P.s_min > P.s_max || P.s_max > n) return bad("need 2 <= s_min <= s_max <= n");
     if (P.s_max > ISYCOS_MAX_W) return bad("s_max > ISYCOS_MAX_W");
     if (k >= P.s_min) return bad("need k < s_min");

@@ -218,8 +218,10 @@ Status Engine::ensure_capacity(int64_t n_wins, int64_t n_items, int32_t n_pairs,
 static int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
 
 Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
-                        int32_t variant, KsgRec* recs_host, const DebugOut& dbg, cudaStream_t st, bool profile,
+                        int32_t variant, KsgRec* recs_host, const DebugOut& dbg, cudaStream_t st, uint32_t flags,
                         BatchStats* bs) {
+    const bool profile = (flags & ISYCOS_F_PROFILE) != 0;
+    const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
     if (n > INT32_MAX / 2) return make_err(ISYCOS_E_INVAL, "batch too large");
     int64_t w_max = 0;
@@ -243,9 +245,9 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         const int w = wins[i].w;
         pp += (int64_t)w * (w - 1);
         const int R = small_class_R(w);
-        if (R && !(sorted_on_ && w >= sorted_min_w_)) {
+        if (R && !(use_sorted && w >= sorted_min_w_)) {
             small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
-        } else if (sorted_on_ && w >= sorted_min_w_) {
+        } else if (use_sorted && w >= sorted_min_w_) {
             sorted.push_back((int32_t)i);
             soff.push_back(spts);
             spts += w;

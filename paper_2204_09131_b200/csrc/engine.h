@@ -130,7 +130,7 @@ public:
     // device memory at recs_dev (caller-owned device buffer of n KsgRec).
     Status evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
                     int32_t variant, KsgRec* recs_host, const DebugOut& dbg, cudaStream_t st,
-                    bool profile, BatchStats* bs);
+                    uint32_t flags /* ISYCOS_F_* */, BatchStats* bs);
 
     // Device copy of a series (padded to a multiple of 4 floats, 16-B aligned).
     Status upload_series(const float* src, int64_t n, bool src_is_device, float** dev_out, cudaStream_t st,
@@ -197,7 +197,7 @@ struct SearchParams {
     int32_t anchor_lookahead = 64;  // BU: climbs started at the predicted re-anchor point
     int32_t bu_depth = 4;           // BU: iterations of delta-neighbourhood requested per round
     uint64_t seed = 0;
-    bool profile = false;
+    uint32_t flags = 0;          // ISYCOS_F_PROFILE | ISYCOS_F_BRUTE
 };
 
 Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std::vector<int32_t>& pair_ids,

@@ -17,6 +17,7 @@
 // Compile with -fmad=false is NOT required: every fp64 op below is an explicit _rn
 // intrinsic, and the fp32 inner loops contain no multiply-add.
 
+#include <climits>
 #include <cmath>
 
 #include "engine.h"
@@ -171,25 +172,73 @@ __device__ __forceinline__ void acc_lt(unsigned& acc, float xi, float xj, float 
     acc += __float_as_uint(fabsf(xi - xj) - eps) >> 31;
 }
 
+// Per-marginal thresholds: KSG-1 passes eps_i for both (strict <); KSG-2 passes nextup(d_x), nextup(d_y),
+// since |dx| <= d  <=>  |dx| < nextup(d) for floats (no float lies strictly between d and nextup(d)).
 template <int R>
-__device__ __forceinline__ void count_step(const float (&xi)[R], const float (&yi)[R], const float (&eps)[R],
-                                           unsigned (&cx)[R], unsigned (&cy)[R], const float4 X, const float4 Y,
-                                           unsigned two) {
+__device__ __forceinline__ void count_step(const float (&xi)[R], const float (&yi)[R], const float (&ex)[R],
+                                           const float (&ey)[R], unsigned (&cx)[R], unsigned (&cy)[R],
+                                           const float4 X, const float4 Y, unsigned two) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        acc_lt(cx[r], xi[r], X.x, eps[r], two);
-        acc_lt(cx[r], xi[r], X.y, eps[r], two);
-        acc_lt(cx[r], xi[r], X.z, eps[r], two);
-        acc_lt(cx[r], xi[r], X.w, eps[r], two);
-        acc_lt(cy[r], yi[r], Y.x, eps[r], two);
-        acc_lt(cy[r], yi[r], Y.y, eps[r], two);
-        acc_lt(cy[r], yi[r], Y.z, eps[r], two);
-        acc_lt(cy[r], yi[r], Y.w, eps[r], two);
+        acc_lt(cx[r], xi[r], X.x, ex[r], two);
+        acc_lt(cx[r], xi[r], X.y, ex[r], two);
+        acc_lt(cx[r], xi[r], X.z, ex[r], two);
+        acc_lt(cx[r], xi[r], X.w, ex[r], two);
+        acc_lt(cy[r], yi[r], Y.x, ey[r], two);
+        acc_lt(cy[r], yi[r], Y.y, ey[r], two);
+        acc_lt(cy[r], yi[r], Y.z, ey[r], two);
+        acc_lt(cy[r], yi[r], Y.w, ey[r], two);
     }
 }
 
-// a5: per-point terms of the points this thread owns (i = i_first + stride * r).
+// ------------------------------------------------------------------ KSG-2 (Eq. 2 literal; NEXT-1)
+// kNN(i) = the first k of j != i in ascending (d_ij, j) order (tie rule R1).  With eps_i = the KSG-1 radius
+// (the k-th smallest d over j != i), kNN(i) = {j : d_ij < eps_i} plus the first `need` j in ascending index
+// order with d_ij == eps_i, where need = (k+1) - #{top-(k+1) entries < eps_i} (the top list includes self's
+// 0).  d_x(i) = max |fl(x_i - x_j)| over kNN(i), d_y likewise.  Self (d = 0) adds 0 to both maxima, so no
+// j != i test is needed: if eps > 0 self is a "<" member contributing 0; if eps == 0 every member has
+// |dx| = |dy| = 0 and d_x = d_y = 0 whatever is taken.
+template <int K1>
+__device__ __forceinline__ int ksg2_need(const float (&rk)[K1]) {
+    const float e = rk[K1 - 1];
+    int c = 0;
+#pragma unroll
+    for (int m = 0; m < K1; ++m) c += rk[m] < e ? 1 : 0;
+    return K1 - c;
+}
+
+__device__ __forceinline__ void ksg2_visit(float xi, float yi, float xj, float yj, float eps, int need, int& taken,
+                                           float& mx, float& my) {
+    const float dx = fabsf(xi - xj), dy = fabsf(yi - yj);
+    const float d = fmaxf(dx, dy);
+    const bool tie = (d == eps) && (taken < need);
+    taken += tie ? 1 : 0;
+    if (d < eps || tie) {
+        mx = fmaxf(mx, dx);
+        my = fmaxf(my, dy);
+    }
+}
+
+// candidates j in ascending index order (the tie rule depends on it)
 template <int R>
+__device__ __forceinline__ void ksg2_step(const float (&xi)[R], const float (&yi)[R], const float (&eps)[R],
+                                          const int (&need)[R], int (&taken)[R], float (&mx)[R], float (&my)[R],
+                                          const float4 X, const float4 Y) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        ksg2_visit(xi[r], yi[r], X.x, Y.x, eps[r], need[r], taken[r], mx[r], my[r]);
+        ksg2_visit(xi[r], yi[r], X.y, Y.y, eps[r], need[r], taken[r], mx[r], my[r]);
+        ksg2_visit(xi[r], yi[r], X.z, Y.z, eps[r], need[r], taken[r], mx[r], my[r]);
+        ksg2_visit(xi[r], yi[r], X.w, Y.w, eps[r], need[r], taken[r], mx[r], my[r]);
+    }
+}
+
+__device__ __forceinline__ float nextup(float d) { return __uint_as_float(__float_as_uint(d) + 1u); }  // d >= +0
+
+// a5: per-point terms of the points this thread owns (i = i_first + stride * r).
+// KSG-1: n = count - [eps > 0] (self counted iff 0 < eps), terms q(psi(n_x+1)) + q(psi(n_y+1)).
+// KSG-2: n = count - 1 (self always satisfies 0 <= d_x), terms q(psi(n_x)) + q(psi(n_y)).
+template <int R, bool V2>
 __device__ __forceinline__ void point_terms(const KsgLaunch& L, int w, int64_t dbg_off, int i_first, int stride,
                                             const float (&eps)[R], const unsigned (&cx)[R],
                                             const unsigned (&cy)[R], long long& sp, long long& sl, int& z) {
@@ -198,9 +247,9 @@ __device__ __forceinline__ void point_terms(const KsgLaunch& L, int w, int64_t d
         const int i = i_first + stride * r;
         if (i < w) {
             const int pos = eps[r] > 0.0f ? 1 : 0;
-            const int nx = (int)cx[r] - pos;
-            const int ny = (int)cy[r] - pos;
-            sp += L.psiq[nx + 1] + L.psiq[ny + 1];
+            const int nx = (int)cx[r] - (V2 ? 1 : pos);
+            const int ny = (int)cy[r] - (V2 ? 1 : pos);
+            sp += V2 ? L.psiq[nx] + L.psiq[ny] : L.psiq[nx + 1] + L.psiq[ny + 1];
             if (pos)
                 sl += q32(canon_ln(__dmul_rn(2.0, (double)eps[r]), L.lnc));
             else
@@ -224,7 +273,7 @@ __device__ __forceinline__ void warp_sum(long long& a, long long& b, int& c) {
 }
 
 // ------------------------------------------------------------------ small windows: one warp per window
-template <int K1, int R, bool BL>
+template <int K1, int R, bool BL, bool V2>
 __global__ void __launch_bounds__(kSmallWarps * 32)
     ksg_small_kernel(const KsgLaunch L, const int32_t* __restrict__ list, int32_t n) {
     constexpr int CAP = 32 * R + 4;
@@ -261,17 +310,33 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     const float4* sy4 = reinterpret_cast<const float4*>(sy);
     const int ng = wpad >> 2;
     for (int g = 0; g < ng; ++g) knn_step<K1, R, BL>(xi, yi, rk, sx4[g], sy4[g]);
-    float eps[R];
+    float eps[R], ex[R], ey[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) eps[r] = rk[r][K1 - 1];
+    for (int r = 0; r < R; ++r) ex[r] = ey[r] = eps[r] = rk[r][K1 - 1];
+    if (V2) {  // KSG-2: d_x, d_y over kNN(i), one more pass in ascending j
+        int need[R], taken[R];
+        float mx[R], my[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            need[r] = ksg2_need<K1>(rk[r]);
+            taken[r] = 0;
+            mx[r] = my[r] = 0.0f;
+        }
+        for (int g = 0; g < ng; ++g) ksg2_step<R>(xi, yi, eps, need, taken, mx, my, sx4[g], sy4[g]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ex[r] = nextup(mx[r]);
+            ey[r] = nextup(my[r]);
+        }
+    }
     unsigned cx[R], cy[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
     const unsigned two = (unsigned)L.two;
-    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g], two);
+    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], two);
     long long sp = 0, sl = 0;
     int z = 0;
-    point_terms<R>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
+    point_terms<R, V2>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
     warp_sum(sp, sl, z);
     if (lane == 0) finalize(L, w, sp, sl, z, &L.out[q]);
 }
@@ -308,7 +373,7 @@ __device__ __forceinline__ int stage_tile(const float* gx, const float* gy, int6
     return nfl >> 2;
 }
 
-template <int K1, int R>
+template <int K1, int R, bool V2>
 __global__ void __launch_bounds__(kTileThreads)
     ksg_tile_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items) {
     extern __shared__ __align__(16) float dyn[];
@@ -356,9 +421,34 @@ __global__ void __launch_bounds__(kTileThreads)
         for (int g = 0; g < ng; ++g) knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
         if (nj > 1) __syncthreads();
     }
-    float eps[R];
+    float eps[R], ex[R], ey[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) eps[r] = rk[r][K1 - 1];
+    for (int r = 0; r < R; ++r) ex[r] = ey[r] = eps[r] = rk[r][K1 - 1];
+    if (V2) {  // KSG-2: d_x, d_y over kNN(i); j-tiles in ascending order (tie rule)
+        int need[R], taken[R];
+        float mx[R], my[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            need[r] = ksg2_need<K1>(rk[r]);
+            taken[r] = 0;
+            mx[r] = my[r] = 0.0f;
+        }
+        for (int jt = 0; jt < nj; ++jt) {
+            if (nj > 1) {
+                const int j0 = jt * kTileJ;
+                ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
+            }
+            const float4* sx4 = reinterpret_cast<const float4*>(sx);
+            const float4* sy4 = reinterpret_cast<const float4*>(sy);
+            for (int g = 0; g < ng; ++g) ksg2_step<R>(xi, yi, eps, need, taken, mx, my, sx4[g], sy4[g]);
+            if (nj > 1) __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ex[r] = nextup(mx[r]);
+            ey[r] = nextup(my[r]);
+        }
+    }
     unsigned cx[R], cy[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
@@ -369,13 +459,13 @@ __global__ void __launch_bounds__(kTileThreads)
         }
         const float4* sx4 = reinterpret_cast<const float4*>(sx);
         const float4* sy4 = reinterpret_cast<const float4*>(sy);
-        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, eps, cx, cy, sx4[g], sy4[g], (unsigned)L.two);
+        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], (unsigned)L.two);
         if (nj > 1) __syncthreads();
     }
 
     long long sp = 0, sl = 0;
     int z = 0;
-    point_terms<R>(L, w, W.dbg_off, it.i0 + threadIdx.x, kTileThreads, eps, cx, cy, sp, sl, z);
+    point_terms<R, V2>(L, w, W.dbg_off, it.i0 + threadIdx.x, kTileThreads, eps, cx, cy, sp, sl, z);
     warp_sum(sp, sl, z);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
@@ -636,12 +726,80 @@ __device__ __forceinline__ int lower_bound_f(const float* s, int w, float v) {
 }
 __device__ __forceinline__ int left_bound_f(const float* s, int m, float v, float eps) { return left_bound(s, m, v, eps); }
 
+// KSG-2 on the sorted path: every kNN(i) member has d_ij <= eps_i, hence |dx| <= eps_i, so it lies in the
+// x-sorted interval {p : |fl(x_i - x_p)| < nextup(eps_i)} around the point's position m.  One pass over that
+// interval takes the "<" members and counts the eps-ties; if there are more ties than kNN(i) needs, the
+// `need` ties of smallest original index are selected (ascending (d, j) order, rule R1) by repeated minimum
+// search — rare for continuous data.  Returns ex = nextup(d_x), ey = nextup(d_y) for the "<=" counts.
+__device__ void ksg2_sorted_radii(const float2* __restrict__ P2, const float* __restrict__ XS,
+                                  const int32_t* __restrict__ OX, int m, int w, float xv, float yv, float eps, int k,
+                                  float* ex, float* ey) {
+    float mx = 0.0f, my = 0.0f;
+    if (eps > 0.0f) {
+        const float e1 = nextup(eps);
+        int lo = 0, hi = m;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (xv - XS[2 * mid] < e1) hi = mid; else lo = mid + 1;
+        }
+        const int La = lo;
+        lo = m;
+        hi = w;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (XS[2 * mid] - xv < e1) lo = mid + 1; else hi = mid;
+        }
+        const int Ra = lo;
+        int n_lt = 0, n_tie = 0;  // n_lt counts self (d = 0 < eps)
+        float tx = 0.0f, ty = 0.0f;
+        for (int p = La; p < Ra; ++p) {
+            const float2 c = P2[p];
+            const float dx = fabsf(xv - c.x), dy = fabsf(yv - c.y);
+            const float d = fmaxf(dx, dy);
+            if (d < eps) {
+                ++n_lt;
+                mx = fmaxf(mx, dx);
+                my = fmaxf(my, dy);
+            } else if (d == eps) {
+                ++n_tie;
+                tx = fmaxf(tx, dx);
+                ty = fmaxf(ty, dy);
+            }
+        }
+        const int need = (k + 1) - n_lt;  // ties in kNN(i) (self is among the n_lt)
+        if (n_tie <= need) {
+            mx = fmaxf(mx, tx);
+            my = fmaxf(my, ty);
+        } else {
+            int last = -1;
+            for (int t = 0; t < need; ++t) {
+                int best = INT_MAX, bp = -1;
+                for (int p = La; p < Ra; ++p) {
+                    const float2 c = P2[p];
+                    const float d = fmaxf(fabsf(xv - c.x), fabsf(yv - c.y));
+                    const int j = OX[p];
+                    if (d == eps && j > last && j < best) {
+                        best = j;
+                        bp = p;
+                    }
+                }
+                const float2 c = P2[bp];
+                mx = fmaxf(mx, fabsf(xv - c.x));
+                my = fmaxf(my, fabsf(yv - c.y));
+                last = best;
+            }
+        }
+    }
+    *ex = nextup(mx);
+    *ey = nextup(my);
+}
+
 // Scan kernel: a CTA owns kSortedPts consecutive x-sorted points, each warp a contiguous quarter.
 // Phase A (k-NN scan) runs a warp-local work queue: a lane that finishes its point takes the next one
 // (ballot + popc), so warps do not idle on their slowest lane (per-point scan lengths vary several-fold
 // with the local density ratio f_x/f_y).  The step itself is branch-free (select the nearer side, one
 // predicated load).  Phase B (binary-search counts, digamma/log terms) is uniform per point.
-template <int K1>
+template <int K1, bool V2>
 __global__ void __launch_bounds__(kSortedThreads)
     sorted_knn_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
                       const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
@@ -771,27 +929,29 @@ __global__ void __launch_bounds__(kSortedThreads)
         const float xv = me.x, yv = me.y;
         const float eps = eps_s[ml];
         int nx = 0, ny = 0;
-        if (eps > 0.0f) {
-            // x: left part [0, m] uses fl(x_i - x_j) < eps, right part [m, w) uses fl(x_j - x_i) < eps
+        float ex = eps, ey = eps;
+        if (V2) ksg2_sorted_radii(P2, XS, OXg + o, m, w, xv, yv, eps, L.k, &ex, &ey);
+        if (V2 || eps > 0.0f) {
+            // x: left part [0, m] uses fl(x_i - x_j) < ex, right part [m, w) uses fl(x_j - x_i) < ex
             int lo = 0, hi = m;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (xv - XS[2 * mid] < eps) hi = mid; else lo = mid + 1;
+                if (xv - XS[2 * mid] < ex) hi = mid; else lo = mid + 1;
             }
             const int Lx = lo;
             lo = m;
             hi = w;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (XS[2 * mid] - xv < eps) lo = mid + 1; else hi = mid;
+                if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
             }
             nx = lo - Lx - 1;
             const int p = lower_bound_f(YS, w, yv);
-            const int Ly = left_bound_f(YS, p, yv, eps);
-            const int Ry = right_bound(YS, p, w, yv, eps);
+            const int Ly = left_bound_f(YS, p, yv, ey);
+            const int Ry = right_bound(YS, p, w, yv, ey);
             ny = Ry - Ly - 1;
         }
-        sp += L.psiq[nx + 1] + L.psiq[ny + 1];
+        sp += V2 ? L.psiq[nx] + L.psiq[ny] : L.psiq[nx + 1] + L.psiq[ny + 1];
         if (eps > 0.0f)
             sl += q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
         else
@@ -841,34 +1001,42 @@ __global__ void nonfinite_kernel(const float* __restrict__ p, int64_t n, int* fl
 }
 
 // ------------------------------------------------------------------ dispatch over (k, R)
-template <int K1, bool BL>
+template <int K1, bool BL, bool V2>
 cudaError_t small_kb(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
     const dim3 grid((n + kSmallWarps - 1) / kSmallWarps), block(kSmallWarps * 32);
     switch (R) {
-        case 1: ksg_small_kernel<K1, 1, BL><<<grid, block, 0, st>>>(L, list, n); break;
-        case 2: ksg_small_kernel<K1, 2, BL><<<grid, block, 0, st>>>(L, list, n); break;
-        case 4: ksg_small_kernel<K1, 4, BL><<<grid, block, 0, st>>>(L, list, n); break;
-        case 8: ksg_small_kernel<K1, 8, BL><<<grid, block, 0, st>>>(L, list, n); break;
+        case 1: ksg_small_kernel<K1, 1, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
+        case 2: ksg_small_kernel<K1, 2, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
+        case 4: ksg_small_kernel<K1, 4, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
+        case 8: ksg_small_kernel<K1, 8, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
+// KSG-2 instantiates only the branch-free small kernel (its speed is secondary; halves the build)
 template <int K1>
 cudaError_t small_k(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
-    return L.knn_mode == 1 ? small_kb<K1, true>(L, list, n, R, st) : small_kb<K1, false>(L, list, n, R, st);
+    if (L.variant == 1) return small_kb<K1, true, true>(L, list, n, R, st);
+    return L.knn_mode == 1 ? small_kb<K1, true, false>(L, list, n, R, st)
+                           : small_kb<K1, false, false>(L, list, n, R, st);
+}
+
+template <int K1, bool V2>
+cudaError_t tile_kv(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, cudaStream_t st) {
+    const size_t smem = 2 * (kTileJ + 8) * sizeof(float);
+    switch (R) {
+        case 1: ksg_tile_kernel<K1, 1, V2><<<n, kTileThreads, smem, st>>>(L, items, n); break;  // latency mode
+        case 2: ksg_tile_kernel<K1, 2, V2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
+        case 4: ksg_tile_kernel<K1, 4, V2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 template <int K1>
 cudaError_t tile_k(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, cudaStream_t st) {
-    const size_t smem = 2 * (kTileJ + 8) * sizeof(float);
-    switch (R) {
-        case 1: ksg_tile_kernel<K1, 1><<<n, kTileThreads, smem, st>>>(L, items, n); break;  // latency mode
-        case 2: ksg_tile_kernel<K1, 2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
-        case 4: ksg_tile_kernel<K1, 4><<<n, kTileThreads, smem, st>>>(L, items, n); break;
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
+    return L.variant == 1 ? tile_kv<K1, true>(L, items, n, R, st) : tile_kv<K1, false>(L, items, n, R, st);
 }
 
 }  // namespace
@@ -908,7 +1076,10 @@ namespace {
 template <int K1>
 cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const float2* P2,
                      const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st) {
-    sorted_knn_kernel<K1><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+    if (L.variant == 1)
+        sorted_knn_kernel<K1, true><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+    else
+        sorted_knn_kernel<K1, false><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
     return cudaGetLastError();
 }
 }  // namespace

@@ -748,7 +748,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         recs.resize(batch.size());
         const auto t_ev = clk::now();
         Status s = eng->evaluate(table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
-                                 P.variant, recs.data(), DebugOut{}, st, P.profile, &bs);
+                                 P.variant, recs.data(), DebugOut{}, st, P.flags, &bs);
         const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
         eval_ms += ev_ms;
         if (!s.ok()) return s;

@@ -58,7 +58,7 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
 }
 
 Status Engine::evaluate(const PairPtrs* pairs, int32_t, const KsgWin* wins, int64_t n, int32_t k, int32_t variant,
-                        KsgRec* recs_host, const DebugOut&, cudaStream_t, bool, BatchStats* bs) {
+                        KsgRec* recs_host, const DebugOut&, cudaStream_t, uint32_t, BatchStats* bs) {
     const auto t = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < n; ++i) {
         const PairPtrs& p = pairs[wins[i].pair];

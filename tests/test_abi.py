@@ -71,8 +71,9 @@ def test_validation_before_gpu(capi):
     assert "k must be" in capi.isycos_last_error()
     assert L.isycos_mi_batch(p(x), p(x), 16, p(w), 0, 4, p(out)) == capi.ISYCOS_OK
     o = capi.MiOpts()
-    o.variant = 1
+    o.variant = 2  # 0 = KSG-1, 1 = KSG-2; nothing else
     assert L.isycos_mi_batch_ex(p(x), p(x), 16, p(w), 1, 4, C.byref(o), p(out)) == capi.E_INVAL
+    assert "variant" in capi.isycos_last_error()
 
 
 def test_search_param_validation(capi):

@@ -43,15 +43,15 @@ def assert_records_equal(got, ref, label=""):
     assert np.max(np.abs(np.asarray(got["mi"]) - np.asarray(ref["mi"]))) <= 1e-9
 
 
-def check_windows(isy, orc, x, y, W, k, debug=False, label=""):
+def check_windows(isy, orc, x, y, W, k, debug=False, label="", variant=0, brute=False):
     W = np.asarray(W, np.int64).reshape(-1, 2)
-    got = isy.isycos_mi_batch_ex(x, y, W, k, debug=debug)
-    ref = orc.mi_batch(x, y, W, k)
+    got = isy.isycos_mi_batch_ex(x, y, W, k, debug=debug, variant=variant, brute=brute)
+    ref = orc.mi_batch(x, y, W, k, variant=variant)
     assert_records_equal(got, ref, label)
     if debug:
         off = 0
         for (a, b) in W:
-            o = orc.window(x[a:b], y[a:b], k=k)
+            o = orc.window(x[a:b], y[a:b], k=k, variant=variant)
             w = b - a
             assert np.array_equal(got["eps"][off:off + w], o.eps), f"{label} eps [{a},{b})"
             assert np.array_equal(got["nx"][off:off + w], o.nx), f"{label} nx [{a},{b})"
@@ -217,3 +217,63 @@ def test_cfg3_subsample_bitwise(isy, orc):
             check_windows(isy, orc, x, y, W, k, label=f"cfg3 k={k} w={w}")
     check_windows(isy, orc, x, y, [(512 * 37, 512 * 37 + 16384), (999_000 - 16384, 999_000)], 4,
                   label="cfg3 w=16384")
+
+
+# ---------------------------------------------------------------- brute-force path for w >= 257 (ISYCOS_F_BRUTE)
+def test_brute_path_large_windows(isy, orc):
+    """The tile kernel (multi i-tile, multi j-tile) is the default only when the sorted path is off; the
+    flag routes every window there.  Same bitwise bar."""
+    wl = datagen.cfg2(n=20_000)
+    x, y = wl.series
+    W = [(3, 3 + 257), (100, 612), (7, 7 + 1025), (1000, 1000 + 4097), (n0 := 11_111, n0 + 8191)]
+    check_windows(isy, orc, x, y, W, 4, debug=True, label="brute", brute=True)
+    check_windows(isy, orc, x, y, W[:3], 8, label="brute k=8", brute=True)
+
+
+# ---------------------------------------------------------------- KSG-2 (paper's literal Eq. 2; NEXT-1)
+@pytest.mark.parametrize("k", [1, 4, 8])
+@pytest.mark.parametrize("brute", [False, True])
+def test_ksg2_size_classes(isy, orc, k, brute):
+    """KSG-2 through every kernel: warp (w <= 256), tile (brute), sorted (w >= 257) incl. a multi-j-tile
+    window; per-point eps, n_x, n_y bit-exact (n = the closed <= d_x counts)."""
+    wl = datagen.cfg2(n=20_000)
+    x, y = wl.series
+    rng = np.random.default_rng(100 + k)
+    W = []
+    for w in [9, 32, 33, 100, 128, 129, 256, 257, 513, 1025, 4097, 5003]:
+        if w <= k:
+            continue
+        t0 = int(rng.integers(0, len(x) - w))
+        W.append((t0, t0 + w))
+    check_windows(isy, orc, x, y, W, k, debug=True, label=f"ksg2 k={k} brute={brute}", variant=1, brute=brute)
+
+
+def test_ksg2_ties(isy, orc):
+    """Ties decide KSG-2's kNN set ((d, j) order, smaller index first) and its closed counts: integer
+    data, duplicated points, a constant segment (eps = 0: d_x = d_y = 0, counts of exact duplicates)."""
+    st = datagen.Stream(77, 1)
+    n = 5000
+    xi = np.floor(st.uniform(n) * 6).astype(np.float32)
+    yi = np.floor(st.uniform(n) * 6).astype(np.float32)
+    xd = np.repeat(datagen.f32(st.normal(n // 3 + 1)), 3)[:n]
+    yd = np.repeat(datagen.f32(st.normal(n // 3 + 1)), 3)[:n]
+    xc, yc = xi.copy(), yi.copy()
+    xc[2000:2300] = 1.0
+    yc[2000:2300] = 2.0
+    W = [(0, 40), (5, 200), (50, 700), (0, 4500), (2000, 2300), (1990, 2400)]
+    for k in (1, 3, 4):
+        for brute in (False, True):
+            lab = f"k={k} brute={brute}"
+            check_windows(isy, orc, xi, yi, W, k, debug=True, label="ksg2 int " + lab, variant=1, brute=brute)
+            check_windows(isy, orc, xd, yd, W, k, debug=True, label="ksg2 dup " + lab, variant=1, brute=brute)
+            check_windows(isy, orc, xc, yc, W, k, debug=True, label="ksg2 const " + lab, variant=1, brute=brute)
+
+
+def test_ksg2_cfg1_sweep_and_xl(isy, orc):
+    wl = datagen.cfg1()
+    x, y = wl.series
+    W = datagen.sweep_windows(len(x), wl.sweep["sizes"], wl.sweep["stride"])
+    check_windows(isy, orc, x, y, W, 4, label="ksg2 cfg1 sweep", variant=1)
+    wl2 = datagen.cfg2(n=60_000)
+    x2, y2 = wl2.series
+    check_windows(isy, orc, x2, y2, [(7, 7 + 16385)], 4, debug=True, label="ksg2 xl", variant=1)

@@ -104,3 +104,11 @@ def test_device_series_input(isy, orc):
     ds = [torch.from_numpy(s).cuda() for s in wl.series]
     gres, gst = isy.search_workload(wl, series=ds)
     assert_same(ores, ost, gres, gst, "device series")
+
+
+@pytest.mark.parametrize("method", [1, 2])
+def test_cfg1_search_ksg2(isy, orc, method):
+    """The search driven by KSG-2 (paper's literal Eq. 2) instead of KSG-1: same bitwise bar."""
+    wl = datagen.cfg1()
+    ores, ost, gres, gst = run_both(isy, orc, wl, method=method, variant=1)
+    assert_same(ores, ost, gres, gst, f"cfg1 ksg2 m={method}")
