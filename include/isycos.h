@@ -162,7 +162,7 @@ typedef struct {
     int32_t t_max_idle;   /* Alg. 2 idle budget (loop while idle <= T_maxIdle, G5) */
     int32_t h;            /* LAHC history length L_h */
     int32_t n_chunks;     /* Alg. 4 overlapping chunks per pair (>= 1) */
-    int32_t lookahead;    /* BU speculative climbs per chain (0 => default 64) */
+    int32_t lookahead;    /* BU speculative climbs per chain (0 => default 32) */
     uint64_t seed;        /* LAHC random streams: SplitMix64 keyed by (seed, pair id, climb start) */
     uint32_t flags;       /* ISYCOS_F_* */
     void* stream;         /* cudaStream_t; NULL = the library's own stream */

@@ -9,8 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libisycos.so")
-SOURCES = ["ksg_kernels.cu", "engine.cu", "search.cpp", "capi.cpp"]
-HEADERS = ["engine.h"]
+SOURCES = ["ksg_small.cu", "ksg_tile.cu", "ksg_sorted.cu", "ksg_fused.cu", "ksg_misc.cu", "engine.cu", "search.cpp",
+           "capi.cpp"]
+HEADERS = ["engine.h", "ksg_device.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",

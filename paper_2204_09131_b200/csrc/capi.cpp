@@ -254,11 +254,13 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     P.t_max_idle = opts->t_max_idle;
     P.h = opts->h;
     P.n_chunks = opts->n_chunks;
-    P.lookahead = opts->lookahead > 0 ? opts->lookahead : 64;
+    P.lookahead = opts->lookahead > 0 ? opts->lookahead : 32;
     P.seed = opts->seed;
     P.flags = opts->flags;
     // speculation tuning knobs (do not change results)
     if (const char* e = std::getenv("ISYCOS_BU_DEPTH")) P.bu_depth = std::atoi(e);
+    if (const char* e = std::getenv("ISYCOS_TREND_DEPTH")) P.trend_depth = std::atoi(e);
+    if (const char* e = std::getenv("ISYCOS_PIPELINE")) P.pipeline = std::atoi(e) != 0;
     if (const char* e = std::getenv("ISYCOS_ANCHOR")) P.anchor_lookahead = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_SPEC_CAP")) P.spec_cap_mult = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_LOOKAHEAD")) P.lookahead = std::atoi(e);

@@ -120,13 +120,18 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_SORTED")) sorted_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
+    if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
-    ISY_CK(cudaMalloc(&dsteps_, sizeof(unsigned long long)));
-    ISY_CK(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
-    for (int a = 0; a < kAux; ++a) {
-        ISY_CK(cudaStreamCreateWithFlags(&aux_[a], cudaStreamNonBlocking));
-        ISY_CK(cudaEventCreateWithFlags(&join_ev_[a], cudaEventDisableTiming));
+    ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
+    ISY_CK(cudaEventCreateWithFlags(&xev_, cudaEventDisableTiming));
+    for (Slot& S : slots_) {
+        ISY_CK(cudaEventCreateWithFlags(&S.fork_ev, cudaEventDisableTiming));
+        for (int a = 0; a < kAux; ++a) {
+            ISY_CK(cudaStreamCreateWithFlags(&S.aux[a], cudaStreamNonBlocking));
+            ISY_CK(cudaEventCreateWithFlags(&S.join_ev[a], cudaEventDisableTiming));
+        }
     }
     return Status{};
 }
@@ -135,20 +140,23 @@ Engine::~Engine() {
     cudaFree(psi_);
     cudaFree(psiq_);
     cudaFree(lnc_);
-    cudaFree(acc_);
-    cudaFree(dstage_);
-    cudaFree(drec_);
     cudaFree(dflag_);
-    cudaFree(dsteps_);
-    cudaFree(sscratch_);
-    cudaFreeHost(hstage_);
-    cudaFreeHost(hrec_);
-    for (auto e : events_) cudaEventDestroy(e);
-    for (int a = 0; a < kAux; ++a) {
-        if (aux_[a]) cudaStreamDestroy(aux_[a]);
-        if (join_ev_[a]) cudaEventDestroy(join_ev_[a]);
+    for (Slot& S : slots_) {
+        cudaFree(S.acc);
+        cudaFree(S.dstage);
+        cudaFree(S.ddrec);
+        cudaFree(S.sscratch);
+        cudaFreeHost(S.hstage);
+        cudaFreeHost(S.hrec);
+        for (auto e : S.events) cudaEventDestroy(e);
+        for (int a = 0; a < kAux; ++a) {
+            if (S.aux[a]) cudaStreamDestroy(S.aux[a]);
+            if (S.join_ev[a]) cudaEventDestroy(S.join_ev[a]);
+        }
+        if (S.fork_ev) cudaEventDestroy(S.fork_ev);
     }
-    if (fork_ev_) cudaEventDestroy(fork_ev_);
+    if (stream2_) cudaStreamDestroy(stream2_);
+    if (xev_) cudaEventDestroy(xev_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -173,44 +181,46 @@ Status Engine::ensure_psi(int64_t w_max, cudaStream_t st) {
     return Status{};
 }
 
-Status Engine::ensure_capacity(int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists) {
-    if (acc_cap_ < n_wins) {
-        int64_t c = std::max<int64_t>(n_wins, acc_cap_ * 2);
-        cudaFree(acc_);
-        acc_ = nullptr;
-        ISY_CK(cudaMalloc(&acc_, c * sizeof(KsgAcc)));
-        ISY_CK(cudaMemset(acc_, 0, c * sizeof(KsgAcc)));
-        acc_cap_ = c;
+Status Engine::ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists) {
+    if (S.acc_cap < n_wins) {
+        int64_t c = std::max<int64_t>(n_wins, S.acc_cap * 2);
+        cudaFree(S.acc);
+        S.acc = nullptr;
+        ISY_CK(cudaMalloc(&S.acc, c * sizeof(KsgAcc)));
+        ISY_CK(cudaMemset(S.acc, 0, c * sizeof(KsgAcc)));
+        S.acc_cap = c;
     }
-    if (drec_cap_ < n_wins) {
-        int64_t c = std::max<int64_t>(n_wins, drec_cap_ * 2);
-        cudaFree(drec_);
-        drec_ = nullptr;
-        ISY_CK(cudaMalloc(&drec_, c * sizeof(KsgRec)));
-        drec_cap_ = c;
+    if (S.hrec_cap < n_wins) {  // records: mapped pinned host memory, written by the kernels (zero-copy)
+        int64_t c = std::max<int64_t>(n_wins, S.hrec_cap * 2);
+        cudaFreeHost(S.hrec);
+        S.hrec = nullptr;
+        S.drec = nullptr;
+        ISY_CK(cudaHostAlloc(&S.hrec, c * sizeof(KsgRec), cudaHostAllocMapped));
+        ISY_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.drec), S.hrec, 0));
+        S.hrec_cap = c;
     }
-    if (hrec_cap_ < n_wins) {
-        int64_t c = std::max<int64_t>(n_wins, hrec_cap_ * 2);
-        cudaFreeHost(hrec_);
-        hrec_ = nullptr;
-        ISY_CK(cudaMallocHost(&hrec_, c * sizeof(KsgRec)));
-        hrec_cap_ = c;
+    if (n_wins > kZeroCopyMaxRecs && S.ddrec_cap < n_wins) {
+        int64_t c = std::max<int64_t>(n_wins, S.ddrec_cap * 2);
+        cudaFree(S.ddrec);
+        S.ddrec = nullptr;
+        ISY_CK(cudaMalloc(&S.ddrec, c * sizeof(KsgRec)));
+        S.ddrec_cap = c;
     }
     const int64_t bytes = 64 + n_pairs * (int64_t)sizeof(PairPtrs) + n_wins * (int64_t)sizeof(KsgWin) +
                           n_lists * 4 + n_items * (int64_t)sizeof(KsgItem) + 16 * 64;
-    if (dstage_cap_ < bytes) {
-        int64_t c = std::max<int64_t>(bytes, dstage_cap_ * 2);
-        cudaFree(dstage_);
-        dstage_ = nullptr;
-        ISY_CK(cudaMalloc(&dstage_, c));
-        dstage_cap_ = c;
+    if (S.dstage_cap < bytes) {
+        int64_t c = std::max<int64_t>(bytes, S.dstage_cap * 2);
+        cudaFree(S.dstage);
+        S.dstage = nullptr;
+        ISY_CK(cudaMalloc(&S.dstage, c));
+        S.dstage_cap = c;
     }
-    if (hstage_cap_ < bytes) {
-        int64_t c = std::max<int64_t>(bytes, hstage_cap_ * 2);
-        cudaFreeHost(hstage_);
-        hstage_ = nullptr;
-        ISY_CK(cudaMallocHost(&hstage_, c));
-        hstage_cap_ = c;
+    if (S.hstage_cap < bytes) {
+        int64_t c = std::max<int64_t>(bytes, S.hstage_cap * 2);
+        cudaFreeHost(S.hstage);
+        S.hstage = nullptr;
+        ISY_CK(cudaMallocHost(&S.hstage, c));
+        S.hstage_cap = c;
     }
     return Status{};
 }
@@ -220,6 +230,16 @@ static int64_t align64(int64_t v) { return (v + 63) & ~int64_t(63); }
 Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
                         int32_t variant, KsgRec* recs_host, const DebugOut& dbg, cudaStream_t st, uint32_t flags,
                         BatchStats* bs) {
+    Status s = submit(0, pairs, n_pairs, wins, n, k, variant, dbg, st, flags, bs);
+    if (!s.ok()) return s;
+    return collect(0, recs_host, bs);
+}
+
+Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
+                      int32_t variant, const DebugOut& dbg, cudaStream_t st, uint32_t flags, BatchStats* bs) {
+    Slot& S = slots_[si];
+    S.n = 0;
+    S.busy = false;
     const bool profile = (flags & ISYCOS_F_PROFILE) != 0;
     const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
@@ -238,15 +258,29 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
     static const int kTileRs[3] = {2, 4, 1};
     std::vector<int32_t> sorted;
     std::vector<int64_t> soff;
+    std::vector<int32_t> fused;  // sorted path, fused sort+scan kernel (w <= kFusedMaxW)
+    int fused_n2 = 256;
     int64_t n_items = 0, n_sitems = 0, spts = 0, n_segs = 0, n_mblocks = 0;
     int W2 = 0;
     int64_t pp = 0;
+    // latency mode for the sorted path: few sorted points in the batch -> fused sort+scan kernel (a CTA
+    // per window slice, no scratch round trip); otherwise the throughput form (sort once, then scan)
+    bool fuse = use_sorted && fused_on_;
+    if (fuse) {
+        int64_t fpts = 0;
+        for (int64_t i = 0; i < n; ++i)
+            if (wins[i].w >= sorted_min_w_ && wins[i].w <= kFusedMaxW) fpts += wins[i].w;
+        fuse = fpts <= fused_max_pts_;
+    }
     for (int64_t i = 0; i < n; ++i) {
         const int w = wins[i].w;
         pp += (int64_t)w * (w - 1);
         const int R = small_class_R(w);
         if (R && !(use_sorted && w >= sorted_min_w_)) {
             small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
+        } else if (fuse && w >= sorted_min_w_ && w <= kFusedMaxW) {
+            fused.push_back((int32_t)i);
+            while (fused_n2 < w) fused_n2 <<= 1;
         } else if (use_sorted && w >= sorted_min_w_) {
             sorted.push_back((int32_t)i);
             soff.push_back(spts);
@@ -274,49 +308,66 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
     // work queues), else 256 (more CTAs per window: latency-bound rounds)
     const int ppc = spts >= (int64_t)148 * 8 * 1024 ? 1024 : 256;
     for (int32_t q : sorted) n_sitems += (wins[q].w + ppc - 1) / ppc;
-    int64_t n_lists = (int64_t)sorted.size();
+    // fused: split windows into up to ceil(w / 512) slices while the batch has fewer than 2 CTAs per SM
+    const int gmax = std::max<int>(1, (int)(2 * 148 / std::max<size_t>(1, fused.size())));
+    int64_t n_fitems = 0;
+    for (int32_t q : fused) {
+        const int fp = fused_ppc(wins[q].w, gmax);
+        n_fitems += (wins[q].w + fp - 1) / fp;
+    }
+    int64_t n_lists = (int64_t)sorted.size() + (int64_t)fused.size();
     for (auto& v : small) n_lists += (int64_t)v.size();
     {
-        Status s = ensure_capacity(n + 1, n_items + n_sitems + n_segs + n_mblocks, n_pairs,
+        Status s = ensure_capacity(S, n + 1, n_items + n_sitems + n_segs + n_mblocks + n_fitems, n_pairs,
                                    n_lists + 2 * (int64_t)sorted.size() + 16);
         if (!s.ok()) return s;
     }
     // scratch per sorted point: P2 (8) | OX (4) | YS (4) | TX (4) | TI (4) | TY (4)
-    if (spts > 0 && sscratch_cap_ < spts * 28) {
-        const int64_t c = std::max<int64_t>(spts * 28, sscratch_cap_ * 2);
-        cudaFree(sscratch_);
-        sscratch_ = nullptr;
-        ISY_CK(cudaMalloc(&sscratch_, c));
-        sscratch_cap_ = c;
+    if (spts > 0 && S.sscratch_cap < spts * 28) {
+        const int64_t c = std::max<int64_t>(spts * 28, S.sscratch_cap * 2);
+        cudaFree(S.sscratch);
+        S.sscratch = nullptr;
+        ISY_CK(cudaMalloc(&S.sscratch, c));
+        S.sscratch_cap = c;
     }
     // pack [pairs | wins | small lists | sorted list | sorted offsets | tile items | sorted items]
     const int64_t off_pairs = 0;
     const int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
     const int64_t off_lists = align64(off_wins + n * (int64_t)sizeof(KsgWin));
-    const int64_t off_slist = align64(off_lists + (n_lists - (int64_t)sorted.size()) * 4);
+    const int64_t off_flist = align64(off_lists + (n_lists - (int64_t)sorted.size() - (int64_t)fused.size()) * 4);
+    const int64_t off_fitems = align64(off_flist + (int64_t)fused.size() * 4);
+    const int64_t off_slist = align64(off_fitems + n_fitems * (int64_t)sizeof(KsgItem));
     const int64_t off_soff = align64(off_slist + (int64_t)sorted.size() * 4);
     const int64_t off_items = align64(off_soff + (int64_t)sorted.size() * 8);
     const int64_t off_sitems = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
     const int64_t off_segs = align64(off_sitems + n_sitems * (int64_t)sizeof(KsgItem));
     const int64_t off_mblk = align64(off_segs + n_segs * (int64_t)sizeof(KsgItem));
     const int64_t total = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
-    std::memcpy(hstage_ + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
-    std::memcpy(hstage_ + off_wins, wins, n * sizeof(KsgWin));
+    std::memcpy(S.hstage + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
+    std::memcpy(S.hstage + off_wins, wins, n * sizeof(KsgWin));
     int64_t list_off[4];
     {
-        int32_t* lp = reinterpret_cast<int32_t*>(hstage_ + off_lists);
+        int32_t* lp = reinterpret_cast<int32_t*>(S.hstage + off_lists);
         int64_t c = 0;
         for (int s = 0; s < 4; ++s) {
             list_off[s] = c;
             std::memcpy(lp + c, small[s].data(), small[s].size() * 4);
             c += (int64_t)small[s].size();
         }
-        std::memcpy(hstage_ + off_slist, sorted.data(), sorted.size() * 4);
-        std::memcpy(hstage_ + off_soff, soff.data(), soff.size() * 8);
+        std::memcpy(S.hstage + off_flist, fused.data(), fused.size() * 4);
+        KsgItem* fp = reinterpret_cast<KsgItem*>(S.hstage + off_fitems);
+        int64_t cf = 0;
+        for (size_t b = 0; b < fused.size(); ++b) {
+            const int w = wins[fused[b]].w;
+            const int pp_w = fused_ppc(w, gmax);
+            for (int i0 = 0; i0 < w; i0 += pp_w) fp[cf++] = KsgItem{(int32_t)b, i0};
+        }
+        std::memcpy(S.hstage + off_slist, sorted.data(), sorted.size() * 4);
+        std::memcpy(S.hstage + off_soff, soff.data(), soff.size() * 8);
     }
     int64_t item_off[3];
     {
-        KsgItem* ip = reinterpret_cast<KsgItem*>(hstage_ + off_items);
+        KsgItem* ip = reinterpret_cast<KsgItem*>(S.hstage + off_items);
         int64_t c = 0;
         for (int s = 0; s < 3; ++s) {
             item_off[s] = c;
@@ -326,9 +377,9 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
                 for (int i0 = 0; i0 < w; i0 += kTileThreads * tr) ip[c++] = KsgItem{q, i0};
             }
         }
-        KsgItem* sp = reinterpret_cast<KsgItem*>(hstage_ + off_sitems);
-        KsgItem* sg = reinterpret_cast<KsgItem*>(hstage_ + off_segs);
-        KsgItem* mb = reinterpret_cast<KsgItem*>(hstage_ + off_mblk);
+        KsgItem* sp = reinterpret_cast<KsgItem*>(S.hstage + off_sitems);
+        KsgItem* sg = reinterpret_cast<KsgItem*>(S.hstage + off_segs);
+        KsgItem* mb = reinterpret_cast<KsgItem*>(S.hstage + off_mblk);
         int64_t cs = 0, cm = 0;
         c = 0;
         for (size_t b = 0; b < sorted.size(); ++b) {
@@ -339,19 +390,18 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
                 for (int i0 = 0; i0 < w; i0 += kMergePts) mb[cm++] = KsgItem{(int32_t)b, i0};
         }
     }
-    ISY_CK(cudaMemcpyAsync(dstage_, hstage_, total, cudaMemcpyHostToDevice, st));
+    ISY_CK(cudaMemcpyAsync(S.dstage, S.hstage, total, cudaMemcpyHostToDevice, st));
     if (bs) bs->h2d_bytes += total;
-    if (!sorted.empty()) ISY_CK(cudaMemsetAsync(dsteps_, 0, sizeof(unsigned long long), st));
 
     KsgLaunch L;
-    L.pairs = reinterpret_cast<const PairPtrs*>(dstage_ + off_pairs);
-    L.wins = reinterpret_cast<const KsgWin*>(dstage_ + off_wins);
+    L.pairs = reinterpret_cast<const PairPtrs*>(S.dstage + off_pairs);
+    L.wins = reinterpret_cast<const KsgWin*>(S.dstage + off_wins);
     L.psi = psi_;
     L.psiq = psiq_;
     L.lnc = lnc_;
-    L.scan_steps = sorted.empty() ? nullptr : dsteps_;
-    L.acc = acc_;
-    L.out = drec_;
+    L.acc = S.acc;
+    const bool zc = n <= kZeroCopyMaxRecs;  // big sweeps: device records + one D2H copy (PCIe-friendlier)
+    L.out = zc ? S.drec : S.ddrec;
     L.dbg_eps = dbg.eps;
     L.dbg_nx = dbg.nx;
     L.dbg_ny = dbg.ny;
@@ -360,8 +410,9 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
     L.knn_mode = knn_mode_;
     L.two = 2;
     L.sorted_ppc = ppc;
-    const int32_t* dlists = reinterpret_cast<const int32_t*>(dstage_ + off_lists);
-    const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dstage_ + off_items);
+    L.fused_n2 = fused_n2;
+    const int32_t* dlists = reinterpret_cast<const int32_t*>(S.dstage + off_lists);
+    const KsgItem* ditems = reinterpret_cast<const KsgItem*>(S.dstage + off_items);
 
     // launches: biggest work first so the small classes fill the tail
     int n_launch = 0, n_ksg = 0;
@@ -372,18 +423,23 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         for (int32_t q : small[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
     for (int s = 0; s < 3; ++s)
         for (int32_t q : tile[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
+    for (int32_t q : fused) {
+        int lg = 0;
+        while ((1 << lg) < wins[q].w) ++lg;
+        probes += (int64_t)wins[q].w * 5 * lg;
+    }
     for (int32_t q : sorted) {
         int lg = 0;
         while ((1 << lg) < wins[q].w) ++lg;
         probes += (int64_t)wins[q].w * 5 * lg;
     }
     auto ev_pair = [&](int i) -> std::pair<cudaEvent_t, cudaEvent_t> {
-        while ((int)events_.size() < 2 * (i + 1)) {
+        while ((int)S.events.size() < 2 * (i + 1)) {
             cudaEvent_t e;
             cudaEventCreate(&e);
-            events_.push_back(e);
+            S.events.push_back(e);
         }
-        return {events_[2 * i], events_[2 * i + 1]};
+        return {S.events[2 * i], S.events[2 * i + 1]};
     };
     // Launch groups fork onto auxiliary streams after the descriptor copy and join before the record
     // copy, so independent size classes overlap (a round's latency is the slowest class, not the sum).
@@ -393,12 +449,12 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         cudaStream_t sg = st;
         if (n_ksg > 0) {
             if (!forked) {
-                ISY_CK(cudaEventRecord(fork_ev_, st));
+                ISY_CK(cudaEventRecord(S.fork_ev, st));
                 forked = true;
             }
-            sg = aux_[(n_ksg - 1) % kAux];
+            sg = S.aux[(n_ksg - 1) % kAux];
             if (n_ksg - 1 < kAux) {
-                ISY_CK(cudaStreamWaitEvent(sg, fork_ev_, 0));
+                ISY_CK(cudaStreamWaitEvent(sg, S.fork_ev, 0));
                 n_aux_used = n_ksg;
             }
         }
@@ -413,18 +469,25 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         n_launch += nk;
         return Status{};
     };
+    if (!fused.empty()) {
+        const int32_t* dfl = reinterpret_cast<const int32_t*>(S.dstage + off_flist);
+        const KsgItem* dfi = reinterpret_cast<const KsgItem*>(S.dstage + off_fitems);
+        launch_cls.push_back(0);
+        Status r = launch(1, [&](cudaStream_t sg) { return launch_fused(L, dfl, dfi, (int32_t)n_fitems, gmax, sg); });
+        if (!r.ok()) return r;
+    }
     if (!sorted.empty()) {
-        const int32_t* dsl = reinterpret_cast<const int32_t*>(dstage_ + off_slist);
-        const int64_t* dso = reinterpret_cast<const int64_t*>(dstage_ + off_soff);
-        const KsgItem* dsi = reinterpret_cast<const KsgItem*>(dstage_ + off_sitems);
-        float2* P2 = reinterpret_cast<float2*>(sscratch_);
-        int32_t* OX = reinterpret_cast<int32_t*>(sscratch_ + spts * 8);
-        float* YS = reinterpret_cast<float*>(sscratch_ + spts * 12);
-        float* TX = reinterpret_cast<float*>(sscratch_ + spts * 16);
-        int32_t* TI = reinterpret_cast<int32_t*>(sscratch_ + spts * 20);
-        float* TY = reinterpret_cast<float*>(sscratch_ + spts * 24);
-        const KsgItem* dsg = reinterpret_cast<const KsgItem*>(dstage_ + off_segs);
-        const KsgItem* dmb = reinterpret_cast<const KsgItem*>(dstage_ + off_mblk);
+        const int32_t* dsl = reinterpret_cast<const int32_t*>(S.dstage + off_slist);
+        const int64_t* dso = reinterpret_cast<const int64_t*>(S.dstage + off_soff);
+        const KsgItem* dsi = reinterpret_cast<const KsgItem*>(S.dstage + off_sitems);
+        float2* P2 = reinterpret_cast<float2*>(S.sscratch);
+        int32_t* OX = reinterpret_cast<int32_t*>(S.sscratch + spts * 8);
+        float* YS = reinterpret_cast<float*>(S.sscratch + spts * 12);
+        float* TX = reinterpret_cast<float*>(S.sscratch + spts * 16);
+        int32_t* TI = reinterpret_cast<int32_t*>(S.sscratch + spts * 20);
+        float* TY = reinterpret_cast<float*>(S.sscratch + spts * 24);
+        const KsgItem* dsg = reinterpret_cast<const KsgItem*>(S.dstage + off_segs);
+        const KsgItem* dmb = reinterpret_cast<const KsgItem*>(S.dstage + off_mblk);
         launch_cls.push_back(0);
         Status r = launch(n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
@@ -452,49 +515,74 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
         if (!r.ok()) return r;
     }
     for (int a = 0; a < std::min(n_aux_used, kAux); ++a) {  // join
-        ISY_CK(cudaEventRecord(join_ev_[a], aux_[a]));
-        ISY_CK(cudaStreamWaitEvent(st, join_ev_[a], 0));
+        ISY_CK(cudaEventRecord(S.join_ev[a], S.aux[a]));
+        ISY_CK(cudaStreamWaitEvent(st, S.join_ev[a], 0));
     }
-    // the step counter rides in the pinned record buffer (slot n), one D2H copy for both
+    if (!zc) ISY_CK(cudaMemcpyAsync(S.hrec, S.ddrec, n * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
+    for (int32_t q : fused) spts += wins[q].w;
+    S.busy = true;
+    S.st = st;
+    S.n = n;
+    S.profile = profile;
+    S.n_ksg = n_ksg;
+    S.launch_cls = std::move(launch_cls);
+    S.pp = pp;
+    S.n_launch = n_launch;
+    S.brute_pairs = brute_pairs;
+    S.probes = probes;
+    S.sorted_windows = (int64_t)sorted.size() + (int64_t)fused.size();
+    S.spts = spts;
+    return Status{};
+}
+
+// Wait for a submitted batch; copy its records out.  The kernels wrote the records (and per-window
+// scan-step counts) into mapped pinned host memory (or a device buffer copied back by submit): the stream
+// synchronisation makes them visible.
+Status Engine::collect(int si, KsgRec* recs_host, BatchStats* bs) {
+    Slot& S = slots_[si];
+    if (!S.busy) return Status{};
+    S.busy = false;
+    const int64_t n = S.n;
+    ISY_CK(cudaStreamSynchronize(S.st));
     unsigned long long steps = 0;
-    if (!sorted.empty())
-        ISY_CK(cudaMemcpyAsync(reinterpret_cast<char*>(drec_ + n), dsteps_, sizeof(steps), cudaMemcpyDeviceToDevice,
-                               st));
-    if (recs_host || !sorted.empty()) {
-        const int64_t cnt = recs_host ? n + (sorted.empty() ? 0 : 1) : 0;
-        if (recs_host) {
-            ISY_CK(cudaMemcpyAsync(hrec_, drec_, cnt * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
-        } else {
-            ISY_CK(cudaMemcpyAsync(hrec_ + n, drec_ + n, sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
-        }
-        if (bs) bs->d2h_bytes += cnt * (int64_t)sizeof(KsgRec);
-    }
-    ISY_CK(cudaStreamSynchronize(st));
-    if (!sorted.empty()) std::memcpy(&steps, hrec_ + n, sizeof(steps));
-    if (recs_host) std::memcpy(recs_host, hrec_, n * sizeof(KsgRec));
+    for (int64_t i = 0; i < n; ++i) steps += S.hrec[i].steps;
+    if (recs_host) std::memcpy(recs_host, S.hrec, n * sizeof(KsgRec));
     if (bs) {
+        bs->d2h_bytes += n * (int64_t)sizeof(KsgRec);
         bs->windows += n;
-        bs->point_pairs += pp;
-        bs->launches += n_launch;
-        bs->ksg_launches += n_launch;
+        bs->point_pairs += S.pp;
+        bs->launches += S.n_launch;
+        bs->ksg_launches += S.n_launch;
         bs->rounds += 1;
         bs->scan_steps += (int64_t)steps;
-        bs->sorted_windows += (int64_t)sorted.size();
-        bs->sorted_points += spts;
-        bs->brute_pairs += brute_pairs;
-        bs->search_probes += probes;
-        if (profile) {
-            for (int i = 0; i < n_ksg; ++i) {
+        bs->sorted_windows += S.sorted_windows;
+        bs->sorted_points += S.spts;
+        bs->brute_pairs += S.brute_pairs;
+        bs->search_probes += S.probes;
+        if (S.profile) {
+            for (int i = 0; i < S.n_ksg; ++i) {
                 float ms = 0.f;
-                cudaEventElapsedTime(&ms, events_[2 * i], events_[2 * i + 1]);
+                cudaEventElapsedTime(&ms, S.events[2 * i], S.events[2 * i + 1]);
                 bs->kernel_ms += ms;
-                if (launch_cls[i] == 0)
+                if (S.launch_cls[i] == 0)
                     bs->sorted_ms += ms;
                 else
                     bs->brute_ms += ms;
             }
         }
     }
+    return Status{};
+}
+
+Status Engine::fork_second_stream(cudaStream_t st) {
+    ISY_CK(cudaEventRecord(xev_, st));
+    ISY_CK(cudaStreamWaitEvent(stream2_, xev_, 0));
+    return Status{};
+}
+
+Status Engine::join_second_stream(cudaStream_t st) {
+    ISY_CK(cudaEventRecord(xev_, stream2_));
+    ISY_CK(cudaStreamWaitEvent(st, xev_, 0));
     return Status{};
 }
 

@@ -35,17 +35,18 @@ struct KsgItem {             // one (window, i-tile) work item of the tile kerne
     int32_t i0;
 };
 
-struct KsgRec {              // per-window result (48 B)
+struct KsgRec {              // per-window result (56 B), written by the kernels straight into mapped pinned host memory
     double mi, h, nmi;
     long long s_psi, s_log;
     int32_t zero_eps;
     int32_t pad;
+    unsigned long long steps;  // sorted path: outward-scan candidate visits of this window (algorithmic work)
 };
 
 struct KsgAcc {              // self-cleaning accumulator of a multi-tile window
     unsigned long long s_psi, s_log;
     unsigned int zero, done;
-    unsigned long long pad;
+    unsigned long long steps;
 };
 
 struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
@@ -54,7 +55,6 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     const double* psi;       // psi[m], m = 0..w_max
     const long long* psiq;   // q(psi[m]) = rint(psi[m] * 2^32)
     const double* lnc;       // LN series coefficients 1/(2j+1), j = 1..9
-    unsigned long long* scan_steps;  // sorted path: total outward-scan steps (algorithmic work), or null
     KsgAcc* acc;
     KsgRec* out;
     float* dbg_eps;
@@ -65,7 +65,7 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t knn_mode;        // small-window kNN insertion: 1 branch-free network, 0 guarded
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
     int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
-    int32_t pad2_;
+    int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -77,6 +77,8 @@ int tile_R(int w);                       // points per thread of the tile kernel
 constexpr int kSortedPts = 1024;         // max points per CTA of the sorted-path scan kernel (4 warps)
 constexpr int kSortedMaxW = 16384;       // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
 constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
+constexpr int kFusedMaxW = 4096;         // fused sort+scan path (latency mode): windows up to this size
+constexpr int kFusedThreads = 512;       // threads per fused CTA (16 warps: one 256-key sort chunk each)
 
 // Launchers (ksg_kernels.cu).  Return cudaGetLastError().
 cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
@@ -87,6 +89,10 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
                           int32_t n_items, cudaStream_t st);
+// fused latency path: items {list pos, slice start}; slices of fused_ppc(w, gmax) points
+cudaError_t launch_fused(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
+                         cudaStream_t st);
+int fused_ppc(int w, int gmax);
 cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, double* lnc,
                               cudaStream_t st);
 cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st);
@@ -144,42 +150,65 @@ public:
 
     Status init(int dev);
 
+    // Asynchronous form (the search driver pipelines two batches): submit() packs and launches a batch on
+    // slot si (0 or 1) and returns; collect() waits for it and copies the records out.  A slot holds one
+    // batch at a time; its buffers stay untouched until collected.  evaluate() = submit(0) + collect(0).
+    Status submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
+                  int32_t variant, const DebugOut& dbg, cudaStream_t st, uint32_t flags, BatchStats* bs);
+    Status collect(int si, KsgRec* recs_host, BatchStats* bs);
+    cudaStream_t second_stream() const { return stream2_; }
+    Status fork_second_stream(cudaStream_t st);  // second stream waits for work queued on st so far
+    Status join_second_stream(cudaStream_t st);  // st waits for the second stream
+
 private:
+    static constexpr int kAux = 4;   // auxiliary streams per slot for overlapping size classes
+    static constexpr int64_t kZeroCopyMaxRecs = 8192;
+    struct Slot {                    // per in-flight batch: staging, records, accumulators, scratch, streams
+        KsgAcc* acc = nullptr;
+        int64_t acc_cap = 0;
+        char* dstage = nullptr;      // packed [pairs | wins | lists | items]
+        int64_t dstage_cap = 0;
+        char* hstage = nullptr;      // pinned mirror of dstage
+        int64_t hstage_cap = 0;
+        KsgRec* drec = nullptr;      // device alias of hrec
+        KsgRec* hrec = nullptr;      // mapped pinned (kernels write records here)
+        int64_t hrec_cap = 0;
+        KsgRec* ddrec = nullptr;     // device records for batches above kZeroCopyMaxRecs
+        int64_t ddrec_cap = 0;
+        char* sscratch = nullptr;    // sorted path scratch: [P2 | OX | YS | TX | TI | TY] per point
+        int64_t sscratch_cap = 0;
+        std::vector<cudaEvent_t> events;
+        cudaStream_t aux[kAux] = {};
+        cudaEvent_t fork_ev = nullptr;
+        cudaEvent_t join_ev[kAux] = {};
+        // the batch in flight
+        bool busy = false, profile = false;
+        cudaStream_t st = nullptr;
+        int64_t n = 0, pp = 0, brute_pairs = 0, probes = 0, sorted_windows = 0, spts = 0;
+        int n_ksg = 0, n_launch = 0;
+        std::vector<int> launch_cls;
+    };
+
     Status ensure_psi(int64_t w_max, cudaStream_t st);
-    Status ensure_capacity(int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists);
+    Status ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists);
 
     int dev_ = -1;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t stream2_ = nullptr;  // second slot's stream for the pipelined search
+    cudaEvent_t xev_ = nullptr;       // fork/join event between stream_/caller stream and stream2_
     // digamma tables
     double* psi_ = nullptr;
     long long* psiq_ = nullptr;
     double* lnc_ = nullptr;
     int64_t psi_max_ = 0;
     int32_t knn_mode_ = 1;
-    // batch buffers (device) and pinned staging (host)
-    KsgAcc* acc_ = nullptr;
-    int64_t acc_cap_ = 0;
-    char* dstage_ = nullptr;       // packed [pairs | wins | lists | items]
-    int64_t dstage_cap_ = 0;
-    char* hstage_ = nullptr;       // pinned mirror of dstage_
-    int64_t hstage_cap_ = 0;
-    KsgRec* drec_ = nullptr;
-    int64_t drec_cap_ = 0;
-    KsgRec* hrec_ = nullptr;       // pinned
-    int64_t hrec_cap_ = 0;
     int* dflag_ = nullptr;
-    std::vector<cudaEvent_t> events_;
-    // sorted path scratch: [P2 float2 | OX int32 | YS float] per point, + step counter
-    char* sscratch_ = nullptr;
-    int64_t sscratch_cap_ = 0;
-    unsigned long long* dsteps_ = nullptr;
+    Slot slots_[2];
     bool sorted_on_ = true;
+    bool fused_on_ = true;           // sorted windows w <= kFusedMaxW: fused sort+scan kernel ...
+    int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
     int32_t sorted_min_w_ = 257;
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
-    static constexpr int kAux = 4;   // auxiliary streams for overlapping size classes
-    cudaStream_t aux_[kAux] = {};
-    cudaEvent_t fork_ev_ = nullptr;
-    cudaEvent_t join_ev_[kAux] = {};
 };
 
 // ---------------------------------------------------------------- search driver
@@ -192,10 +221,12 @@ struct SearchParams {
     int32_t p = 3;
     double sigma = 0.2;
     int64_t delta_td = 0, delta_bu = 0;
-    int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 64;
+    int32_t t_max_idle = 3, h = 5, n_chunks = 1, lookahead = 32;
     int64_t spec_cap_mult = 4;   // BU: speculative climbs pause beyond this many s_min
     int32_t anchor_lookahead = 64;  // BU: climbs started at the predicted re-anchor point
     int32_t bu_depth = 4;           // BU: iterations of delta-neighbourhood requested per round
+    int32_t trend_depth = 32;       // BU: positions requested along a climb's current direction (head climbs)
+    bool pipeline = true;           // two batches in flight (host advance overlaps GPU evaluation)
     uint64_t seed = 0;
     uint32_t flags = 0;          // ISYCOS_F_PROFILE | ISYCOS_F_BRUTE
 };

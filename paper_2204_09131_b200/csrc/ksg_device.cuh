@@ -1,4 +1,5 @@
-// sm_100a KSG window kernels — steps a2-a6 of SURVEY §8(a).
+// ksg_device.cuh — device helpers shared by the sm_100a KSG window kernels (ksg_*.cu), steps a2-a6 of
+// SURVEY §8(a).  Each kernel family lives in its own translation unit (parallel builds).
 //
 // Per window W = [t0, t1) of w points of a series pair (Def 4.2):
 //   a2  stage x[t0:t1], y[t0:t1] into shared memory (cp.async.bulk + mbarrier for the tile
@@ -16,6 +17,7 @@
 // No tensor cores: this is compare/count ALU work, not a contraction (north star).
 // Compile with -fmad=false is NOT required: every fp64 op below is an explicit _rn
 // intrinsic, and the fp32 inner loops contain no multiply-add.
+#pragma once
 
 #include <climits>
 #include <cmath>
@@ -23,17 +25,6 @@
 #include "engine.h"
 
 namespace isy {
-
-int small_class_R(int w) {
-    if (w <= 32) return 1;
-    if (w <= 64) return 2;
-    if (w <= 128) return 4;
-    if (w <= 256) return 8;
-    return 0;
-}
-
-int tile_R(int w) { return w <= 2 * kTileThreads ? 2 : 4; }
-
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
@@ -71,7 +62,7 @@ __device__ __forceinline__ long long q32(double v) { return __double2ll_rn(__dmu
 
 // LN(v), v > 0 normal: frexp -> [sqrt(1/2), sqrt(2)) -> 2 atanh(s) series to s^19, fixed op order.
 // c[j] = 1/(2j+1) (j = 1..9) are computed once by psi_scan_kernel with __ddiv_rn.
-__device__ double canon_ln(double v, const double* __restrict__ c) {
+__device__ inline double canon_ln(double v, const double* __restrict__ c) {
     const long long bits = __double_as_longlong(v);
     int e = (int)((bits >> 52) & 0x7FF) - 1022;
     double m = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FE0000000000000LL);  // [0.5, 1)
@@ -90,7 +81,8 @@ __device__ double canon_ln(double v, const double* __restrict__ c) {
     return __dadd_rn(__dmul_rn((double)e, 0.69314718055994530942), r);
 }
 
-__device__ void finalize(const KsgLaunch& L, int w, long long s_psi, long long s_log, int zero, KsgRec* o) {
+__device__ inline void finalize(const KsgLaunch& L, int w, long long s_psi, long long s_log, int zero, KsgRec* o,
+                         unsigned long long steps = 0) {
     const double kQ = 2.3283064365386962890625e-10;  // 2^-32
     const double dw = (double)w;
     double a;
@@ -124,6 +116,7 @@ __device__ void finalize(const KsgLaunch& L, int w, long long s_psi, long long s
     o->s_log = s_log;
     o->zero_eps = zero;
     o->pad = 0;
+    o->steps = steps;
 }
 
 // ------------------------------------------------------------------ inner loops
@@ -272,75 +265,6 @@ __device__ __forceinline__ void warp_sum(long long& a, long long& b, int& c) {
     }
 }
 
-// ------------------------------------------------------------------ small windows: one warp per window
-template <int K1, int R, bool BL, bool V2>
-__global__ void __launch_bounds__(kSmallWarps * 32)
-    ksg_small_kernel(const KsgLaunch L, const int32_t* __restrict__ list, int32_t n) {
-    constexpr int CAP = 32 * R + 4;
-    __shared__ __align__(16) float sbuf[kSmallWarps][2][CAP];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int idx = blockIdx.x * kSmallWarps + warp;
-    if (idx >= n) return;  // warp-uniform
-    const int q = list[idx];
-    const KsgWin W = L.wins[q];
-    const int w = W.w;
-    const int wpad = (w + 3) & ~3;
-    const float* gx = L.pairs[W.pair].x + W.t0;
-    const float* gy = L.pairs[W.pair].y + W.t0;
-    float* sx = sbuf[warp][0];
-    float* sy = sbuf[warp][1];
-    for (int j = lane; j < wpad; j += 32) {  // a2: coalesced loads, +inf sentinels past w
-        sx[j] = j < w ? gx[j] : kInf;
-        sy[j] = j < w ? gy[j] : kInf;
-    }
-    __syncwarp();
-    float xi[R], yi[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        xi[r] = i < w ? sx[i] : 0.0f;
-        yi[r] = i < w ? sy[i] : 0.0f;
-    }
-    float rk[R][K1];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int m = 0; m < K1; ++m) rk[r][m] = kInf;
-    const float4* sx4 = reinterpret_cast<const float4*>(sx);
-    const float4* sy4 = reinterpret_cast<const float4*>(sy);
-    const int ng = wpad >> 2;
-    for (int g = 0; g < ng; ++g) knn_step<K1, R, BL>(xi, yi, rk, sx4[g], sy4[g]);
-    float eps[R], ex[R], ey[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) ex[r] = ey[r] = eps[r] = rk[r][K1 - 1];
-    if (V2) {  // KSG-2: d_x, d_y over kNN(i), one more pass in ascending j
-        int need[R], taken[R];
-        float mx[R], my[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            need[r] = ksg2_need<K1>(rk[r]);
-            taken[r] = 0;
-            mx[r] = my[r] = 0.0f;
-        }
-        for (int g = 0; g < ng; ++g) ksg2_step<R>(xi, yi, eps, need, taken, mx, my, sx4[g], sy4[g]);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            ex[r] = nextup(mx[r]);
-            ey[r] = nextup(my[r]);
-        }
-    }
-    unsigned cx[R], cy[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
-    const unsigned two = (unsigned)L.two;
-    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], two);
-    long long sp = 0, sl = 0;
-    int z = 0;
-    point_terms<R, V2>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
-    warp_sum(sp, sl, z);
-    if (lane == 0) finalize(L, w, sp, sl, z, &L.out[q]);
-}
-
 // ------------------------------------------------------------------ large windows: (window, i-tile) per CTA
 // a2 via cp.async.bulk of the 16-B aligned superset [a & ~3, ceil4(a + len)) into SMEM, completion on an
 // mbarrier; series buffers are 16-B aligned and padded to a multiple of 4 floats so the superset is in bounds.
@@ -373,143 +297,13 @@ __device__ __forceinline__ int stage_tile(const float* gx, const float* gy, int6
     return nfl >> 2;
 }
 
-template <int K1, int R, bool V2>
-__global__ void __launch_bounds__(kTileThreads)
-    ksg_tile_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items) {
-    extern __shared__ __align__(16) float dyn[];
-    __shared__ __align__(8) unsigned long long mbar;
-    __shared__ long long red_sp[kTileThreads / 32], red_sl[kTileThreads / 32];
-    __shared__ int red_z[kTileThreads / 32];
-
-    const KsgItem it = items[blockIdx.x];
-    const int q = it.win;
-    const KsgWin W = L.wins[q];
-    const int w = W.w;
-    const float* gx = L.pairs[W.pair].x;
-    const float* gy = L.pairs[W.pair].y;
-    const int64_t t0 = W.t0;
-    float* sx = dyn;
-    float* sy = dyn + (kTileJ + 8);
-    const uint32_t bar = smem_u32(&mbar);
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    uint32_t phase = 0;
-
-    float xi[R], yi[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int i = it.i0 + threadIdx.x + kTileThreads * r;
-        xi[r] = i < w ? gx[t0 + i] : 0.0f;
-        yi[r] = i < w ? gy[t0 + i] : 0.0f;
-    }
-    float rk[R][K1];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int m = 0; m < K1; ++m) rk[r][m] = kInf;
-
-    const int nj = (w + kTileJ - 1) / kTileJ;
-    int ng = 0;
-    for (int jt = 0; jt < nj; ++jt) {
-        const int j0 = jt * kTileJ;
-        ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
-        const float4* sx4 = reinterpret_cast<const float4*>(sx);
-        const float4* sy4 = reinterpret_cast<const float4*>(sy);
-        for (int g = 0; g < ng; ++g) knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
-        if (nj > 1) __syncthreads();
-    }
-    float eps[R], ex[R], ey[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) ex[r] = ey[r] = eps[r] = rk[r][K1 - 1];
-    if (V2) {  // KSG-2: d_x, d_y over kNN(i); j-tiles in ascending order (tie rule)
-        int need[R], taken[R];
-        float mx[R], my[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            need[r] = ksg2_need<K1>(rk[r]);
-            taken[r] = 0;
-            mx[r] = my[r] = 0.0f;
-        }
-        for (int jt = 0; jt < nj; ++jt) {
-            if (nj > 1) {
-                const int j0 = jt * kTileJ;
-                ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
-            }
-            const float4* sx4 = reinterpret_cast<const float4*>(sx);
-            const float4* sy4 = reinterpret_cast<const float4*>(sy);
-            for (int g = 0; g < ng; ++g) ksg2_step<R>(xi, yi, eps, need, taken, mx, my, sx4[g], sy4[g]);
-            if (nj > 1) __syncthreads();
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            ex[r] = nextup(mx[r]);
-            ey[r] = nextup(my[r]);
-        }
-    }
-    unsigned cx[R], cy[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
-    for (int jt = 0; jt < nj; ++jt) {
-        if (nj > 1) {
-            const int j0 = jt * kTileJ;
-            ng = stage_tile(gx, gy, t0 + j0, min(kTileJ, w - j0), sx, sy, bar, phase);
-        }
-        const float4* sx4 = reinterpret_cast<const float4*>(sx);
-        const float4* sy4 = reinterpret_cast<const float4*>(sy);
-        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], (unsigned)L.two);
-        if (nj > 1) __syncthreads();
-    }
-
-    long long sp = 0, sl = 0;
-    int z = 0;
-    point_terms<R, V2>(L, w, W.dbg_off, it.i0 + threadIdx.x, kTileThreads, eps, cx, cy, sp, sl, z);
-    warp_sum(sp, sl, z);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-        red_sp[warp] = sp;
-        red_sl[warp] = sl;
-        red_z[warp] = z;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int v = 1; v < kTileThreads / 32; ++v) {
-            sp += red_sp[v];
-            sl += red_sl[v];
-            z += red_z[v];
-        }
-        const int ntiles = (w + kTileThreads * R - 1) / (kTileThreads * R);
-        if (ntiles == 1) {
-            finalize(L, w, sp, sl, z, &L.out[q]);
-        } else {
-            KsgAcc* A = &L.acc[q];
-            atomicAdd(&A->s_psi, (unsigned long long)sp);
-            atomicAdd(&A->s_log, (unsigned long long)sl);
-            atomicAdd(&A->zero, (unsigned)z);
-            __threadfence();
-            const unsigned ticket = atomicAdd(&A->done, 1u);
-            if (ticket == (unsigned)(ntiles - 1)) {  // last tile of the window: finalize + reset
-                __threadfence();
-                const long long tp = (long long)atomicExch(&A->s_psi, 0ull);
-                const long long tl = (long long)atomicExch(&A->s_log, 0ull);
-                const int tz = (int)atomicExch(&A->zero, 0u);
-                atomicExch(&A->done, 0u);
-                finalize(L, w, tp, tl, tz, &L.out[q]);
-            }
-        }
-    }
-}
-
 // ------------------------------------------------------------------ CTA reduce + window accumulate/finalize
-template <int NT>
 __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int ntiles, long long sp, long long sl,
                                            int z, unsigned long long steps) {
-    __shared__ long long r_sp[NT / 32], r_sl[NT / 32];
-    __shared__ int r_z[NT / 32];
-    __shared__ unsigned long long r_st[NT / 32];
+    __shared__ long long r_sp[32], r_sl[32];
+    __shared__ int r_z[32];
+    __shared__ unsigned long long r_st[32];
+    const int nw = blockDim.x >> 5;
     warp_sum(sp, sl, z);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) steps += __shfl_down_sync(0xffffffffu, steps, off);
@@ -522,22 +316,21 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-#pragma unroll
-    for (int v = 1; v < NT / 32; ++v) {
+    for (int v = 1; v < nw; ++v) {
         sp += r_sp[v];
         sl += r_sl[v];
         z += r_z[v];
         steps += r_st[v];
     }
-    if (L.scan_steps) atomicAdd(L.scan_steps, steps);
     if (ntiles == 1) {
-        finalize(L, w, sp, sl, z, &L.out[q]);
+        finalize(L, w, sp, sl, z, &L.out[q], steps);
         return;
     }
     KsgAcc* A = &L.acc[q];
     atomicAdd(&A->s_psi, (unsigned long long)sp);
     atomicAdd(&A->s_log, (unsigned long long)sl);
     atomicAdd(&A->zero, (unsigned)z);
+    atomicAdd(&A->steps, steps);
     __threadfence();
     const unsigned ticket = atomicAdd(&A->done, 1u);
     if (ticket == (unsigned)(ntiles - 1)) {  // last tile of the window: finalize + reset the slot
@@ -545,8 +338,9 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
         const long long tp = (long long)atomicExch(&A->s_psi, 0ull);
         const long long tl = (long long)atomicExch(&A->s_log, 0ull);
         const int tz = (int)atomicExch(&A->zero, 0u);
+        const unsigned long long ts = atomicExch(&A->steps, 0ull);
         atomicExch(&A->done, 0u);
-        finalize(L, w, tp, tl, tz, &L.out[q]);
+        finalize(L, w, tp, tl, tz, &L.out[q], ts);
     }
 }
 
@@ -603,58 +397,6 @@ __device__ __forceinline__ void bitonic_smem(K* key, int n2) {
 // A window that is one segment writes the scan layout directly: P2[m] = (x, y) of the m-th point in x
 // order, OX[m] = its original index, YS = sorted y.  Segments of an XL window write sorted runs to
 // TX/TI/TY instead; rank_merge_kernel then places every element by its rank across the runs.
-__global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
-                                   const int64_t* __restrict__ soff, const KsgItem* __restrict__ segs,
-                                   float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
-                                   float* __restrict__ TX, int32_t* __restrict__ TI, float* __restrict__ TY,
-                                   int W2) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const KsgItem sg = segs[blockIdx.x];  // win = position in the sorted list, i0 = segment start
-    const int b = sg.win;
-    const int q = list[b];
-    const KsgWin W = L.wins[q];
-    const int w = W.w;
-    const int s0 = sg.i0;
-    const int len = min(kSortedMaxW, w - s0);
-    const bool whole = (s0 == 0 && len == w);
-    int n2 = 1;
-    while (n2 < len) n2 <<= 1;
-    const float* gx = L.pairs[W.pair].x + W.t0;
-    const float* gy = L.pairs[W.pair].y + W.t0;
-    const int64_t o = soff[b];
-    // pass 0: x with the index packed into one 64-bit word (sortable float bits << 32 | index): one
-    // compare/swap per exchange, ties broken by index.  pass 1: y keys alone (32-bit).
-    unsigned long long* k64 = reinterpret_cast<unsigned long long*>(sm);
-    unsigned* k32 = reinterpret_cast<unsigned*>(sm);
-    for (int i = threadIdx.x; i < n2; i += blockDim.x)
-        k64[i] = i < len ? ((unsigned long long)sortable(gx[s0 + i]) << 32) | (unsigned)(s0 + i) : ~0ull;
-    __syncthreads();
-    bitonic_smem(k64, n2);
-    for (int m = threadIdx.x; m < len; m += blockDim.x) {
-        const unsigned long long v = k64[m];
-        const float xv = unsortable((unsigned)(v >> 32));
-        const int32_t idx = (int32_t)(v & 0xffffffffu);
-        if (whole) {
-            P2[o + m] = make_float2(xv, gy[idx]);
-            OX[o + m] = idx;
-        } else {
-            TX[o + s0 + m] = xv;
-            TI[o + s0 + m] = idx;
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) k32[i] = i < len ? sortable(gy[s0 + i]) : ~0u;
-    __syncthreads();
-    bitonic_smem(k32, n2);
-    for (int m = threadIdx.x; m < len; m += blockDim.x) {
-        const float yv = unsortable(k32[m]);
-        if (whole)
-            YS[o + m] = yv;
-        else
-            TY[o + s0 + m] = yv;
-    }
-}
-
 // count of elements < v (strict) or <= v in a sorted run s[0..n)
 __device__ __forceinline__ int count_below(const float* s, int n, float v, bool inclusive) {
     int lo = 0, hi = n;
@@ -667,38 +409,6 @@ __device__ __forceinline__ int count_below(const float* s, int n, float v, bool 
 
 // XL windows: element p of run c goes to rank = (p - start(c)) + sum_{c' < c} #{run c' <= v}
 // + sum_{c' > c} #{run c' < v}: a total order (ties by run), so ranks are a permutation.
-__global__ void rank_merge_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
-                                  const int64_t* __restrict__ soff, const KsgItem* __restrict__ blocks,
-                                  float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
-                                  const float* __restrict__ TX, const int32_t* __restrict__ TI,
-                                  const float* __restrict__ TY) {
-    const KsgItem bk = blocks[blockIdx.x];  // win = list position, i0 = first element of this block
-    const int b = bk.win;
-    const KsgWin W = L.wins[list[b]];
-    const int w = W.w;
-    const int p = bk.i0 + threadIdx.x;
-    if (p >= w) return;
-    const int64_t o = soff[b];
-    const float* gy = L.pairs[W.pair].y + W.t0;
-    const int c = p / kSortedMaxW;
-    const int nruns = (w + kSortedMaxW - 1) / kSortedMaxW;
-    const float vx = TX[o + p], vy = TY[o + p];
-    int rx = p - c * kSortedMaxW, ry = rx;
-    for (int c2 = 0; c2 < nruns; ++c2) {
-        if (c2 == c) continue;
-        const int st = c2 * kSortedMaxW;
-        const int n = min(kSortedMaxW, w - st);
-        rx += count_below(TX + o + st, n, vx, c2 < c);
-        ry += count_below(TY + o + st, n, vy, c2 < c);
-    }
-    const int32_t idx = TI[o + p];
-    P2[o + rx] = make_float2(vx, gy[idx]);
-    OX[o + rx] = idx;
-    YS[o + ry] = vy;
-}
-
-// first index in [lo, hi) where pred is false, for pred true...true false...false
-// left side: smallest j in [0, m] with fl(v - s[j]) < eps (pred false...true)
 __device__ __forceinline__ int left_bound(const float* s, int m, float v, float eps) {
     int lo = 0, hi = m;  // answer in [lo, hi]; s[hi]... pred(m) true iff eps > 0 (checked by caller)
     while (lo < hi) {
@@ -731,7 +441,7 @@ __device__ __forceinline__ int left_bound_f(const float* s, int m, float v, floa
 // interval takes the "<" members and counts the eps-ties; if there are more ties than kNN(i) needs, the
 // `need` ties of smallest original index are selected (ascending (d, j) order, rule R1) by repeated minimum
 // search — rare for continuous data.  Returns ex = nextup(d_x), ey = nextup(d_y) for the "<=" counts.
-__device__ void ksg2_sorted_radii(const float2* __restrict__ P2, const float* __restrict__ XS,
+__device__ inline void ksg2_sorted_radii(const float2* __restrict__ P2, const float* __restrict__ XS,
                                   const int32_t* __restrict__ OX, int m, int w, float xv, float yv, float eps, int k,
                                   float* ex, float* ey) {
     float mx = 0.0f, my = 0.0f;
@@ -794,31 +504,20 @@ __device__ void ksg2_sorted_radii(const float2* __restrict__ P2, const float* __
     *ey = nextup(my);
 }
 
-// Scan kernel: a CTA owns kSortedPts consecutive x-sorted points, each warp a contiguous quarter.
-// Phase A (k-NN scan) runs a warp-local work queue: a lane that finishes its point takes the next one
-// (ballot + popc), so warps do not idle on their slowest lane (per-point scan lengths vary several-fold
-// with the local density ratio f_x/f_y).  The step itself is branch-free (select the nearer side, one
-// predicated load).  Phase B (binary-search counts, digamma/log terms) is uniform per point.
+// Scan of one CTA's slice [cta0, cta0 + cta_n) of a window's x-sorted points (arrays in global or shared
+// memory, generic pointers): P2[m] = (x, y) of the m-th point in x order, OX[m] its window index, YS the
+// sorted y.  Each warp owns a contiguous part of the slice.  Phase A (k-NN scan) runs a warp-local work
+// queue: a lane that finishes its point takes the next one (ballot + popc), so warps do not idle on their
+// slowest lane (per-point scan lengths vary several-fold with the local density ratio f_x/f_y).  Phase B
+// (binary-search counts, digamma/log terms) is uniform per point.  Ends with the CTA reduction.
 template <int K1, bool V2>
-__global__ void __launch_bounds__(kSortedThreads)
-    sorted_knn_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
-                      const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
-                      const KsgItem* __restrict__ items) {
-    const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
-    const int kPerWarp = ppc / (kSortedThreads / 32);
-    __shared__ float eps_s[kSortedPts];
-    const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list, it.i0 = first point
-    const int b = it.win;
-    const int q = list[b];
-    const int w = L.wins[q].w;
-    const int64_t o = soff[b];
-    const float2* P2 = P2g + o;
+__device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, int ntiles, const float2* P2,
+                                            const int32_t* OX, const float* YS, int cta0, int cta_n, float* eps_s) {
     const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
-    const float* YS = YSg + o;
-    const int cta0 = it.i0;
-    const int cta_n = min(ppc, w - cta0);
+    const int nwarps = blockDim.x >> 5;
+    const int kPerWarp = (cta_n + nwarps - 1) / nwarps;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wb = warp * kPerWarp;
+    const int wb = min(warp * kPerWarp, cta_n);
     const int we = min(wb + kPerWarp, cta_n);
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long steps = 0;
@@ -923,14 +622,14 @@ __global__ void __launch_bounds__(kSortedThreads)
     long long sp = 0, sl = 0;
     int z = 0;
     const int64_t dbg = L.wins[q].dbg_off;
-    for (int ml = threadIdx.x; ml < cta_n; ml += kSortedThreads) {
+    for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x) {
         const int m = cta0 + ml;
         const float2 me = P2[m];
         const float xv = me.x, yv = me.y;
         const float eps = eps_s[ml];
         int nx = 0, ny = 0;
         float ex = eps, ey = eps;
-        if (V2) ksg2_sorted_radii(P2, XS, OXg + o, m, w, xv, yv, eps, L.k, &ex, &ey);
+        if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
         if (V2 || eps > 0.0f) {
             // x: left part [0, m] uses fl(x_i - x_j) < ex, right part [m, w) uses fl(x_j - x_i) < ex
             int lo = 0, hi = m;
@@ -957,88 +656,17 @@ __global__ void __launch_bounds__(kSortedThreads)
         else
             z += 1;
         if (dbg >= 0) {
-            const int i = OXg[o + m];
+            const int i = OX[m];
             if (L.dbg_eps) L.dbg_eps[dbg + i] = eps;
             if (L.dbg_nx) L.dbg_nx[dbg + i] = nx;
             if (L.dbg_ny) L.dbg_ny[dbg + i] = ny;
         }
     }
-    const int ntiles = (w + ppc - 1) / ppc;
-    cta_finish<kSortedThreads>(L, q, w, ntiles, sp, sl, z, steps);
+    cta_finish(L, q, w, ntiles, sp, sl, z, steps);
 }
 
-// ------------------------------------------------------------------ digamma tables, input validation
-__global__ void inv_kernel(double* inv, int64_t m_max) {
-    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (m >= 1 && m <= m_max) inv[m] = __ddiv_rn(1.0, (double)m);
-}
-
-// psi(1) = -gamma; psi(m+1) = psi(m) + 1/m, strictly sequential (the canonical definition).
-__global__ void psi_scan_kernel(double* psi, const double* __restrict__ inv, int64_t m_max, double* lnc) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    lnc[0] = 0.0;
-    for (int j = 1; j <= 9; ++j) lnc[j] = __ddiv_rn(1.0, (double)(2 * j + 1));  // LN series coefficients
-    psi[0] = __longlong_as_double(0x7FF8000000000000LL);
-    double v = -0.57721566490153286061;
-    psi[1] = v;
-    for (int64_t m = 1; m < m_max; ++m) {
-        v = __dadd_rn(v, inv[m]);
-        psi[m + 1] = v;
-    }
-}
-
-__global__ void psiq_kernel(const double* psi, long long* psiq, int64_t m_max) {
-    const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (m == 0) psiq[0] = 0;
-    if (m >= 1 && m <= m_max) psiq[m] = q32(psi[m]);
-}
-
-__global__ void nonfinite_kernel(const float* __restrict__ p, int64_t n, int* flag) {
-    int bad = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        bad |= !isfinite(p[i]);
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
-}
-
-// ------------------------------------------------------------------ dispatch over (k, R)
-template <int K1, bool BL, bool V2>
-cudaError_t small_kb(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
-    const dim3 grid((n + kSmallWarps - 1) / kSmallWarps), block(kSmallWarps * 32);
-    switch (R) {
-        case 1: ksg_small_kernel<K1, 1, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
-        case 2: ksg_small_kernel<K1, 2, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
-        case 4: ksg_small_kernel<K1, 4, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
-        case 8: ksg_small_kernel<K1, 8, BL, V2><<<grid, block, 0, st>>>(L, list, n); break;
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-}
-
-// KSG-2 instantiates only the branch-free small kernel (its speed is secondary; halves the build)
-template <int K1>
-cudaError_t small_k(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
-    if (L.variant == 1) return small_kb<K1, true, true>(L, list, n, R, st);
-    return L.knn_mode == 1 ? small_kb<K1, true, false>(L, list, n, R, st)
-                           : small_kb<K1, false, false>(L, list, n, R, st);
-}
-
-template <int K1, bool V2>
-cudaError_t tile_kv(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, cudaStream_t st) {
-    const size_t smem = 2 * (kTileJ + 8) * sizeof(float);
-    switch (R) {
-        case 1: ksg_tile_kernel<K1, 1, V2><<<n, kTileThreads, smem, st>>>(L, items, n); break;  // latency mode
-        case 2: ksg_tile_kernel<K1, 2, V2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
-        case 4: ksg_tile_kernel<K1, 4, V2><<<n, kTileThreads, smem, st>>>(L, items, n); break;
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-}
-
-template <int K1>
-cudaError_t tile_k(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, cudaStream_t st) {
-    return L.variant == 1 ? tile_kv<K1, true>(L, items, n, R, st) : tile_kv<K1, false>(L, items, n, R, st);
-}
-
+// Throughput path scan kernel: the window was sorted by sort_window_kernel (+ rank_merge_kernel) into
+// global scratch; a CTA owns L.sorted_ppc consecutive x-sorted points.
 }  // namespace
 
 #define ISY_K_CASES(FN, ...)                   \
@@ -1061,69 +689,5 @@ cudaError_t tile_k(const KsgLaunch& L, const KsgItem* items, int32_t n, int R, c
         case 16: return FN<17>(__VA_ARGS__);   \
         default: return cudaErrorInvalidValue; \
     }
-
-cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
-    ISY_K_CASES(small_k, L, list, n, R, st)
-}
-
-cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st) {
-    if (n_items <= 0) return cudaSuccess;
-    ISY_K_CASES(tile_k, L, items, n_items, R, st)
-}
-
-namespace {
-template <int K1>
-cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const float2* P2,
-                     const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st) {
-    if (L.variant == 1)
-        sorted_knn_kernel<K1, true><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
-    else
-        sorted_knn_kernel<K1, false><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
-    return cudaGetLastError();
-}
-}  // namespace
-
-cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const KsgItem* segs,
-                          int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
-                          float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
-                          int32_t n_items, cudaStream_t st) {
-    static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
-    if (n_segs <= 0) return cudaSuccess;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSortedMaxW * 8);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    const int threads = std::min(1024, std::max(64, W2 / 2));
-    sort_window_kernel<<<n_segs, threads, (size_t)W2 * 8, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (n_mblocks > 0) {
-        rank_merge_kernel<<<n_mblocks, kMergeThreads, 0, st>>>(L, list, soff, mblocks, P2, OX, YS, TX, TI, TY);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st)
-}
-
-cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, double* lnc,
-                              cudaStream_t st) {
-    const int64_t blocks = (m_max + 1 + 255) / 256;
-    inv_kernel<<<(unsigned)blocks, 256, 0, st>>>(inv, m_max);
-    psi_scan_kernel<<<1, 32, 0, st>>>(psi, inv, m_max, lnc);
-    psiq_kernel<<<(unsigned)blocks, 256, 0, st>>>(psi, psiq, m_max);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
-    int64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    nonfinite_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, n, flag);
-    return cudaGetLastError();
-}
 
 }  // namespace isy

@@ -1,0 +1,196 @@
+// Sorted-marginal path, latency form: fused in-SMEM sort + scan per (window, slice).
+#include "ksg_device.cuh"
+
+namespace isy {
+namespace {
+
+// ------------------------------------------------------------------ fused latency path (w <= kFusedMaxW)
+// One CTA per (window, slice): load the window, sort it in shared memory, then scan the slice's points
+// from shared memory.  Every slice CTA of a window sorts the whole window (redundant work, no scratch
+// round trip and no second launch: search rounds are latency-bound).  The sort: each warp sorts 256
+// keys held 8 per lane with a register/shuffle bitonic network, then merge-path merges in shared
+// memory double the run length up to n2 (next power of two >= w).  x keys carry the window index in
+// the low 32 bits (sortable x bits << 32 | index: unique keys, ties of x broken by index); y keys are
+// the sortable y bits alone.
+template <typename T>
+__device__ __forceinline__ void warp_sort256(T (&v)[8], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 256; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 8) {
+                const int lm = j >> 3;
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const bool up = ((((unsigned)lane << 3) | (unsigned)e) & (unsigned)k) == 0;
+                    const T pv = __shfl_xor_sync(0xffffffffu, v[e], lm);
+                    const T mn = pv < v[e] ? pv : v[e];
+                    const T mx = pv < v[e] ? v[e] : pv;
+                    v[e] = (lower == up) ? mn : mx;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if ((e & j) == 0) {
+                        const bool up = ((((unsigned)lane << 3) | (unsigned)e) & (unsigned)k) == 0;
+                        const T a = v[e], c = v[e | j];
+                        const bool sw = up ? (c < a) : (a < c);
+                        v[e] = sw ? c : a;
+                        v[e | j] = sw ? a : c;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// merge adjacent sorted runs of length r (src) into runs of 2r (dst); thread t < n2/8 writes outputs
+// [8t, 8t+8).  Merge path: the co-rank i (outputs taken from run A) is found by binary search, A first
+// on ties.
+template <typename T>
+__device__ __forceinline__ void merge_level(const T* __restrict__ src, T* __restrict__ dst, int n2, int r) {
+    const int t = threadIdx.x;
+    if (t * 8 < n2) {
+        const int g = t * 8;
+        const int base = (g / (2 * r)) * (2 * r);
+        const T* A = src + base;
+        const T* Bv = src + base + r;
+        const int o = g - base;
+        int lo = max(0, o - r), hi = min(o, r);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (A[mid] <= Bv[o - mid - 1]) lo = mid + 1; else hi = mid;
+        }
+        int ia = lo, ib = o - lo;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const bool takeA = ib >= r || (ia < r && A[ia] <= Bv[ib]);
+            dst[base + o + e] = takeA ? A[ia] : Bv[ib];
+            ia += takeA ? 1 : 0;
+            ib += takeA ? 0 : 1;
+        }
+    }
+}
+
+// fused items: {list position, slice start}; a window of w points has slices of fused_ppc(w, gmax) points
+__device__ __host__ __forceinline__ int fused_ppc_of(int w, int gmax) {
+    int g = (w + kFusedThreads - 1) / kFusedThreads;  // at most one point per thread per slice ...
+    g = g < gmax ? g : gmax;                          // ... unless the batch already fills the GPU
+    g = g < 1 ? 1 : g;
+    const int ppc = (w + g - 1) / g;
+    return (ppc + 31) & ~31;
+}
+
+template <int K1, bool V2>
+__global__ void __launch_bounds__(kFusedThreads)
+    fused_sorted_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const KsgItem* __restrict__ items,
+                        int gmax) {
+    extern __shared__ __align__(16) unsigned long long fsm[];
+    const KsgItem it = items[blockIdx.x];
+    const int q = list[it.win];
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    int n2 = 256;
+    while (n2 < w) n2 <<= 1;
+    const int maxn2 = L.fused_n2;  // shared-memory layout stride (batch maximum)
+    unsigned long long* X0 = fsm;
+    unsigned long long* X1 = fsm + maxn2;
+    unsigned* Y0 = reinterpret_cast<unsigned*>(fsm + 2 * maxn2);
+    unsigned* Y1 = Y0 + maxn2;
+    float* eps_s = reinterpret_cast<float*>(Y1 + maxn2);  // maxn2 floats (a slice can be the whole window)
+    const float* gx = L.pairs[W.pair].x + W.t0;
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    // a2 + sort, step 1: each warp sorts 256-key chunks in registers (8 consecutive keys per lane)
+    for (int c = warp; c * 256 < n2; c += kFusedThreads / 32) {
+        unsigned long long vx[8];
+        unsigned vy[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int i = c * 256 + lane * 8 + e;
+            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
+            vy[e] = i < w ? sortable(gy[i]) : ~0u;
+        }
+        warp_sort256(vx, lane);
+        warp_sort256(vy, lane);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            X0[c * 256 + lane * 8 + e] = vx[e];
+            Y0[c * 256 + lane * 8 + e] = vy[e];
+        }
+    }
+    __syncthreads();
+    // step 2: merge-path levels 256 -> n2 (ping-pong)
+    unsigned long long* xs = X0;
+    unsigned long long* xd = X1;
+    unsigned* ys = Y0;
+    unsigned* yd = Y1;
+    for (int r = 256; r < n2; r <<= 1) {
+        merge_level(xs, xd, n2, r);
+        merge_level(ys, yd, n2, r);
+        __syncthreads();
+        unsigned long long* tx = xs;
+        xs = xd;
+        xd = tx;
+        unsigned* ty = ys;
+        ys = yd;
+        yd = ty;
+    }
+    // step 3: scan layout: P2 (x, y) in x order -> the free x buffer, OX -> the free y buffer, YS in place
+    float2* P2 = reinterpret_cast<float2*>(xd);
+    int32_t* OX = reinterpret_cast<int32_t*>(yd);
+    float* YS = reinterpret_cast<float*>(ys);
+    for (int m = threadIdx.x; m < w; m += kFusedThreads) {
+        const unsigned long long v = xs[m];
+        const int32_t idx = (int32_t)(v & 0xffffffffu);
+        P2[m] = make_float2(unsortable((unsigned)(v >> 32)), gy[idx]);
+        OX[m] = idx;
+        YS[m] = unsortable(ys[m]);
+    }
+    __syncthreads();
+    const int ppc = fused_ppc_of(w, gmax);
+    sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2, OX, YS, it.i0, min(ppc, w - it.i0), eps_s);
+}
+
+template <int K1>
+cudaError_t fused_k(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
+                    cudaStream_t st) {
+    const size_t smem = (size_t)L.fused_n2 * 28;
+    if (L.variant == 1)
+        fused_sorted_kernel<K1, true><<<n_items, kFusedThreads, smem, st>>>(L, list, items, gmax);
+    else
+        fused_sorted_kernel<K1, false><<<n_items, kFusedThreads, smem, st>>>(L, list, items, gmax);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+template <int K1, bool V2>
+cudaError_t fused_attr() {
+    return cudaFuncSetAttribute(fused_sorted_kernel<K1, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kFusedMaxW * 28);
+}
+template <int K1>
+cudaError_t fused_attr_k(const KsgLaunch&) {
+    cudaError_t e = fused_attr<K1, false>();
+    return e != cudaSuccess ? e : fused_attr<K1, true>();
+}
+
+cudaError_t launch_fused(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
+                         cudaStream_t st) {
+    if (n_items <= 0) return cudaSuccess;
+    static bool attr[17] = {};
+    if (L.k < 1 || L.k > 16) return cudaErrorInvalidValue;
+    if (!attr[L.k]) {
+        cudaError_t e = [&]() -> cudaError_t { ISY_K_CASES(fused_attr_k, L) }();
+        if (e != cudaSuccess) return e;
+        attr[L.k] = true;
+    }
+    ISY_K_CASES(fused_k, L, list, items, n_items, gmax, st)
+}
+
+int fused_ppc(int w, int gmax) { return fused_ppc_of(w, gmax); }
+
+}  // namespace isy

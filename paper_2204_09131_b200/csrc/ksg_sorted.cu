@@ -1,0 +1,144 @@
+// Sorted-marginal path, throughput form: sort kernel (+ XL rank merge) into
+// global scratch, then the scan kernel.
+#include "ksg_device.cuh"
+
+namespace isy {
+namespace {
+
+__global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
+                                   const int64_t* __restrict__ soff, const KsgItem* __restrict__ segs,
+                                   float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
+                                   float* __restrict__ TX, int32_t* __restrict__ TI, float* __restrict__ TY,
+                                   int W2) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const KsgItem sg = segs[blockIdx.x];  // win = position in the sorted list, i0 = segment start
+    const int b = sg.win;
+    const int q = list[b];
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    const int s0 = sg.i0;
+    const int len = min(kSortedMaxW, w - s0);
+    const bool whole = (s0 == 0 && len == w);
+    int n2 = 1;
+    while (n2 < len) n2 <<= 1;
+    const float* gx = L.pairs[W.pair].x + W.t0;
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    const int64_t o = soff[b];
+    // pass 0: x with the index packed into one 64-bit word (sortable float bits << 32 | index): one
+    // compare/swap per exchange, ties broken by index.  pass 1: y keys alone (32-bit).
+    unsigned long long* k64 = reinterpret_cast<unsigned long long*>(sm);
+    unsigned* k32 = reinterpret_cast<unsigned*>(sm);
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        k64[i] = i < len ? ((unsigned long long)sortable(gx[s0 + i]) << 32) | (unsigned)(s0 + i) : ~0ull;
+    __syncthreads();
+    bitonic_smem(k64, n2);
+    for (int m = threadIdx.x; m < len; m += blockDim.x) {
+        const unsigned long long v = k64[m];
+        const float xv = unsortable((unsigned)(v >> 32));
+        const int32_t idx = (int32_t)(v & 0xffffffffu);
+        if (whole) {
+            P2[o + m] = make_float2(xv, gy[idx]);
+            OX[o + m] = idx;
+        } else {
+            TX[o + s0 + m] = xv;
+            TI[o + s0 + m] = idx;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) k32[i] = i < len ? sortable(gy[s0 + i]) : ~0u;
+    __syncthreads();
+    bitonic_smem(k32, n2);
+    for (int m = threadIdx.x; m < len; m += blockDim.x) {
+        const float yv = unsortable(k32[m]);
+        if (whole)
+            YS[o + m] = yv;
+        else
+            TY[o + s0 + m] = yv;
+    }
+}
+
+__global__ void rank_merge_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
+                                  const int64_t* __restrict__ soff, const KsgItem* __restrict__ blocks,
+                                  float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
+                                  const float* __restrict__ TX, const int32_t* __restrict__ TI,
+                                  const float* __restrict__ TY) {
+    const KsgItem bk = blocks[blockIdx.x];  // win = list position, i0 = first element of this block
+    const int b = bk.win;
+    const KsgWin W = L.wins[list[b]];
+    const int w = W.w;
+    const int p = bk.i0 + threadIdx.x;
+    if (p >= w) return;
+    const int64_t o = soff[b];
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    const int c = p / kSortedMaxW;
+    const int nruns = (w + kSortedMaxW - 1) / kSortedMaxW;
+    const float vx = TX[o + p], vy = TY[o + p];
+    int rx = p - c * kSortedMaxW, ry = rx;
+    for (int c2 = 0; c2 < nruns; ++c2) {
+        if (c2 == c) continue;
+        const int st = c2 * kSortedMaxW;
+        const int n = min(kSortedMaxW, w - st);
+        rx += count_below(TX + o + st, n, vx, c2 < c);
+        ry += count_below(TY + o + st, n, vy, c2 < c);
+    }
+    const int32_t idx = TI[o + p];
+    P2[o + rx] = make_float2(vx, gy[idx]);
+    OX[o + rx] = idx;
+    YS[o + ry] = vy;
+}
+
+// first index in [lo, hi) where pred is false, for pred true...true false...false
+// left side: smallest j in [0, m] with fl(v - s[j]) < eps (pred false...true)
+template <int K1, bool V2>
+__global__ void __launch_bounds__(kSortedThreads)
+    sorted_knn_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
+                      const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
+                      const KsgItem* __restrict__ items) {
+    const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
+    __shared__ float eps_s[kSortedPts];
+    const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list, it.i0 = first point
+    const int b = it.win;
+    const int q = list[b];
+    const int w = L.wins[q].w;
+    const int64_t o = soff[b];
+    sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2g + o, OXg + o, YSg + o, it.i0, min(ppc, w - it.i0), eps_s);
+}
+
+template <int K1>
+cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const float2* P2,
+                     const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st) {
+    if (L.variant == 1)
+        sorted_knn_kernel<K1, true><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+    else
+        sorted_knn_kernel<K1, false><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const KsgItem* segs,
+                          int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
+                          float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
+                          int32_t n_items, cudaStream_t st) {
+    static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
+    if (n_segs <= 0) return cudaSuccess;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kSortedMaxW * 8);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int threads = std::min(1024, std::max(64, W2 / 2));
+    sort_window_kernel<<<n_segs, threads, (size_t)W2 * 8, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (n_mblocks > 0) {
+        rank_merge_kernel<<<n_mblocks, kMergeThreads, 0, st>>>(L, list, soff, mblocks, P2, OX, YS, TX, TI, TY);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st)
+}
+
+
+}  // namespace isy

@@ -34,6 +34,7 @@ struct Eval {
 };
 
 struct Entry {
+    uint64_t key = 0;  // 0 = empty slot (a window key is never 0: w >= 2)
     Eval e{0, 0, 0};
     bool ready = false;
     bool consumed = false;
@@ -43,56 +44,80 @@ inline uint64_t wkey(int64_t t0, int64_t t1) { return ((uint64_t)t0 << 20) | (ui
 inline int64_t key_t0(uint64_t k) { return (int64_t)(k >> 20); }
 inline int64_t key_w(uint64_t k) { return (int64_t)(k & ((1u << 20) - 1)); }
 
-// Open-addressing window cache: keys -> index into a stable arena (entry pointers never move).
-struct FlatMap {
-    std::vector<uint64_t> keys;  // 0 = empty (a window key is never 0: w >= 2)
-    std::vector<uint32_t> slot;
-    std::deque<Entry> arena;
-    std::vector<uint64_t> arena_keys;
-    size_t mask = 0;
+// Window cache: open addressing over (key, arena index), sharded by t0 >> 8 so the windows one climb or
+// one TD layer touches (nearby t0) share a few small tables that stay cache-resident (the driver does ~1e6
+// lookups per cfg2 search).  Entries live in a block arena and never move: an Entry* stays valid for the
+// life of the cache (batches in flight keep pointers to the entries they will fill).
+struct SmallMap {
+    struct Slot {
+        uint64_t key;
+        uint32_t idx;
+    };
+    std::vector<Slot> tab;
+    uint32_t mask = 0, count = 0;
 
-    static size_t hash(uint64_t k) {
-        k ^= k >> 33;
-        k *= 0xff51afd7ed558ccdull;
-        k ^= k >> 33;
-        return (size_t)k;
+    static uint32_t hash(uint64_t k) {
+        k ^= k >> 29;
+        k *= 0xbf58476d1ce4e5b9ull;
+        return (uint32_t)(k >> 32);
     }
     void grow() {
-        const size_t cap = keys.empty() ? 4096 : keys.size() * 2;
-        std::vector<uint64_t> nk(cap, 0);
-        std::vector<uint32_t> ns(cap, 0);
-        const size_t m = cap - 1;
-        for (size_t a = 0; a < arena_keys.size(); ++a) {
-            size_t i = hash(arena_keys[a]) & m;
-            while (nk[i]) i = (i + 1) & m;
-            nk[i] = arena_keys[a];
-            ns[i] = (uint32_t)a;
+        const size_t cap = tab.empty() ? 64 : tab.size() * 2;
+        std::vector<Slot> nt(cap, Slot{0, 0});
+        const uint32_t m = (uint32_t)cap - 1;
+        for (const Slot& e : tab) {
+            if (!e.key) continue;
+            uint32_t i = hash(e.key) & m;
+            while (nt[i].key) i = (i + 1) & m;
+            nt[i] = e;
         }
-        keys.swap(nk);
-        slot.swap(ns);
+        tab.swap(nt);
         mask = m;
     }
+};
+
+struct FlatMap {
+    static constexpr int kShift = 8;  // shard = t0 >> 8
+    static constexpr uint32_t kBlock = 4096;
+    std::vector<SmallMap> shards;
+    std::vector<std::unique_ptr<Entry[]>> blocks;
+    uint32_t size = 0;
+
+    Entry& at(uint32_t i) { return blocks[i / kBlock][i % kBlock]; }
+    const Entry& at(uint32_t i) const { return blocks[i / kBlock][i % kBlock]; }
     std::pair<Entry*, bool> try_emplace(uint64_t k) {
-        if ((arena.size() + 1) * 2 > keys.size()) grow();
-        size_t i = hash(k) & mask;
-        while (keys[i]) {
-            if (keys[i] == k) return {&arena[slot[i]], false};
-            i = (i + 1) & mask;
+        const size_t sh = (size_t)(key_t0(k) >> kShift);
+        if (sh >= shards.size()) shards.resize(sh + 1);
+        SmallMap& m = shards[sh];
+        if ((m.count + 1) * 2 > m.tab.size()) m.grow();
+        uint32_t i = SmallMap::hash(k) & m.mask;
+        while (m.tab[i].key) {
+            if (m.tab[i].key == k) return {&at(m.tab[i].idx), false};
+            i = (i + 1) & m.mask;
         }
-        keys[i] = k;
-        slot[i] = (uint32_t)arena.size();
-        arena.emplace_back();
-        arena_keys.push_back(k);
-        return {&arena.back(), true};
+        if (size % kBlock == 0) blocks.emplace_back(new Entry[kBlock]);
+        const uint32_t idx = size++;
+        m.tab[i] = SmallMap::Slot{k, idx};
+        ++m.count;
+        Entry& e = at(idx);
+        e.key = k;
+        return {&e, true};
     }
     Entry* find(uint64_t k) {
-        if (keys.empty()) return nullptr;
-        size_t i = hash(k) & mask;
-        while (keys[i]) {
-            if (keys[i] == k) return &arena[slot[i]];
-            i = (i + 1) & mask;
+        const size_t sh = (size_t)(key_t0(k) >> kShift);
+        if (sh >= shards.size()) return nullptr;
+        SmallMap& m = shards[sh];
+        if (m.tab.empty()) return nullptr;
+        uint32_t i = SmallMap::hash(k) & m.mask;
+        while (m.tab[i].key) {
+            if (m.tab[i].key == k) return &at(m.tab[i].idx);
+            i = (i + 1) & m.mask;
         }
         return nullptr;
+    }
+    template <typename F>
+    void for_each(F&& f) const {
+        for (uint32_t i = 0; i < size; ++i) f(at(i));
     }
 };
 
@@ -302,24 +327,68 @@ struct Climb {
     bool finished = false;
     Eval fin{0, 0, 0};
     int64_t ring_t0 = -1, ring_t1 = -1;  // last depth-speculation request (want_ring)
+    int last_da = 0, last_db = 0, run = 0;  // last move (in delta steps) and how many times in a row
+    // values gathered for the current (position, pruned) state: reused by idle iterations
+    int64_t it_t0 = -1, it_t1 = -1, it_b0 = 0, it_b1 = 0;
+    int it_pf = -1, it_nc = 0;
+    double it_bmi = 0.0;
+    bool it_app[2] = {false, false};
+    double it_ee_nmi[2] = {0.0, 0.0}, it_me_mi[2] = {0.0, 0.0};
     int ring_pf = -1;
 
     // Depth speculation: request every window the next bu_depth iterations could need — the rings
     // N_1..N_D of the delta-neighbourhood (Defs 5.2-5.3, Fig. 4's N_1/N_2) plus their noise extensions —
     // so a climb advances up to bu_depth iterations per round.  Requests only; nothing is consumed.
+    // Trend speculation: a climb that has moved the same way twice in a row (e.g. a window growing to the
+    // right inside a planted relation, one delta per iteration) will most likely keep going; request the
+    // iteration windows (N_1 + noise extensions) of the next trend_depth positions on that line, so a long
+    // monotone climb advances up to trend_depth iterations per round instead of bu_depth.  Requests only.
+    void want_trend(View& v, const SearchParams& P, int64_t hi, int64_t d) {
+        if (P.trend_depth <= 0 || run < 2) return;
+        for (int m = 1; m <= P.trend_depth; ++m) {
+            const int64_t p0 = t0 + (int64_t)m * last_da * d, p1 = t1 + (int64_t)m * last_db * d;
+            if (p0 < lo || p1 > hi || p1 - p0 < P.s_min || p1 - p0 > P.s_max) break;
+            for (int a = -1; a <= 1; ++a) {
+                if (a < 0 && pruned[0]) continue;
+                for (int b = -1; b <= 1; ++b) {
+                    if ((a == 0 && b == 0) || (b > 0 && pruned[1])) continue;
+                    const int64_t c0 = p0 + a * d, c1 = p1 + b * d;
+                    if (c0 < lo || c1 > hi || c1 - c0 < P.s_min || c1 - c0 > P.s_max) continue;
+                    v.want(c0, c1);
+                }
+            }
+            if (P.noise && d > P.k) {
+                if (!pruned[0] && p0 - d >= lo) v.want(p0 - d, p0);
+                if (!pruned[1] && p1 + d <= hi) v.want(p1, p1 + d);
+            }
+        }
+    }
+
     void want_ring(View& v, const SearchParams& P, int64_t hi, int64_t d) {
         const int D = P.bu_depth;
         if (D <= 1) return;
         // already requested around this window with the same pruned directions
         const int pf = (pruned[0] ? 1 : 0) | (pruned[1] ? 2 : 0);
         if (ring_t0 == t0 && ring_t1 == t1 && ring_pf == pf) return;
+        // Incremental: after a move by (sa, sb) steps with the same pruned directions, the windows the
+        // previous request already covered (old ring, old centre, old noise extensions) are skipped; the
+        // validity tests are absolute, so a covered window was requested then.  (Optimisation only:
+        // want() of a cached window is a no-op.)
+        int64_t sa = 0, sb = 0;
+        bool inc = ring_t0 >= 0 && ring_pf == pf && (t0 - ring_t0) % d == 0 && (t1 - ring_t1) % d == 0;
+        if (inc) {
+            sa = (t0 - ring_t0) / d;
+            sb = (t1 - ring_t1) / d;
+            inc = sa >= -D && sa <= D && sb >= -D && sb <= D;
+        }
         ring_t0 = t0;
         ring_t1 = t1;
         ring_pf = pf;
+        auto in_old = [&](int64_t a, int64_t b) { return inc && a + sa >= -D && a + sa <= D && b + sb >= -D && b + sb <= D; };
         for (int a = -D; a <= D; ++a) {
             if (a < 0 && pruned[0]) continue;
             for (int b = -D; b <= D; ++b) {
-                if ((a == 0 && b == 0) || (b > 0 && pruned[1])) continue;
+                if ((a == 0 && b == 0) || (b > 0 && pruned[1]) || in_old(a, b)) continue;
                 const int64_t c0 = t0 + a * d, c1 = t1 + b * d;
                 if (c0 < lo || c1 > hi || c1 - c0 < P.s_min || c1 - c0 > P.s_max) continue;
                 v.want(c0, c1);
@@ -328,8 +397,10 @@ struct Climb {
         if (!(P.noise && d > P.k)) return;
         for (int a = -(D - 1); a <= D - 1; ++a) {
             const int64_t l0 = t0 + a * d - d, r0 = t1 + a * d;
-            if (!pruned[0] && l0 >= lo && l0 + d <= hi) v.want(l0, l0 + d);
-            if (!pruned[1] && r0 >= lo && r0 + d <= hi) v.want(r0, r0 + d);
+            const bool lo_cov = inc && a + sa >= -(D - 1) && a + sa <= D - 1;
+            const bool ro_cov = inc && a + sb >= -(D - 1) && a + sb <= D - 1;
+            if (!pruned[0] && !lo_cov && l0 >= lo && l0 + d <= hi) v.want(l0, l0 + d);
+            if (!pruned[1] && !ro_cov && r0 >= lo && r0 + d <= hi) v.want(r0, r0 + d);
         }
     }
 
@@ -362,69 +433,86 @@ struct Climb {
                     continue;
                 }
                 if (t1 - t0 > cap) return false;
-                // gather the iteration's windows: N1 (Def 5.2-5.3) in (t0,t1) order + noise windows
-                int64_t c0s[8], c1s[8];
-                int nc = 0;
-                for (int da = -1; da <= 1; ++da)
-                    for (int db = -1; db <= 1; ++db) {
-                        if (da == 0 && db == 0) continue;
-                        if (da == -1 && pruned[0]) continue;
-                        if (db == 1 && pruned[1]) continue;
-                        const int64_t c0 = t0 + da * d, c1 = t1 + db * d;
-                        if (c0 < lo || c1 > hi) continue;
-                        const int64_t sz = c1 - c0;
-                        if (sz < smin || sz > smax) continue;
-                        c0s[nc] = c0;
-                        c1s[nc] = c1;
-                        ++nc;
+                const int pf = (pruned[0] ? 1 : 0) | (pruned[1] ? 2 : 0);
+                if (!(it_t0 == t0 && it_t1 == t1 && it_pf == pf)) {
+                    // gather the iteration's windows: N1 (Def 5.2-5.3) in (t0,t1) order + noise windows
+                    int64_t c0s[8], c1s[8];
+                    int nc = 0;
+                    for (int da = -1; da <= 1; ++da)
+                        for (int db = -1; db <= 1; ++db) {
+                            if (da == 0 && db == 0) continue;
+                            if (da == -1 && pruned[0]) continue;
+                            if (db == 1 && pruned[1]) continue;
+                            const int64_t c0 = t0 + da * d, c1 = t1 + db * d;
+                            if (c0 < lo || c1 > hi) continue;
+                            const int64_t sz = c1 - c0;
+                            if (sz < smin || sz > smax) continue;
+                            c0s[nc] = c0;
+                            c1s[nc] = c1;
+                            ++nc;
+                        }
+                    if (nc == 0) {
+                        state = 2;
+                        continue;
                     }
-                if (nc == 0) {
-                    state = 2;
-                    continue;
-                }
-                bool applicable[2] = {false, false};
-                int64_t e0[2], e1[2], m0[2], m1[2];
-                const bool nz = P.noise && d > P.k;
-                for (int dir = 0; dir < 2 && nz; ++dir) {
-                    if (pruned[dir]) continue;
-                    if (dir == 0) {
-                        e0[0] = t0 - d; e1[0] = t0; m0[0] = t0 - d; m1[0] = t1;
-                    } else {
-                        e0[1] = t1; e1[1] = t1 + d; m0[1] = t0; m1[1] = t1 + d;
+                    bool applicable[2] = {false, false};
+                    int64_t e0[2], e1[2], m0[2], m1[2];
+                    const bool nz = P.noise && d > P.k;
+                    for (int dir = 0; dir < 2 && nz; ++dir) {
+                        if (pruned[dir]) continue;
+                        if (dir == 0) {
+                            e0[0] = t0 - d; e1[0] = t0; m0[0] = t0 - d; m1[0] = t1;
+                        } else {
+                            e0[1] = t1; e1[1] = t1 + d; m0[1] = t0; m1[1] = t1 + d;
+                        }
+                        applicable[dir] = !(e0[dir] < lo || e1[dir] > hi || m1[dir] - m0[dir] > smax);
                     }
-                    applicable[dir] = !(e0[dir] < lo || e1[dir] > hi || m1[dir] - m0[dir] > smax);
+                    const size_t mark = touched.size();
+                    bool missing = false;
+                    const Eval* ce[8];
+                    for (int i = 0; i < nc; ++i) {
+                        ce[i] = v.get(c0s[i], c1s[i]);
+                        missing |= (ce[i] == nullptr);
+                    }
+                    const Eval* ee[2] = {nullptr, nullptr};
+                    const Eval* me[2] = {nullptr, nullptr};
+                    for (int dir = 0; dir < 2; ++dir) {
+                        if (!applicable[dir]) continue;
+                        ee[dir] = v.get(e0[dir], e1[dir]);
+                        me[dir] = v.get(m0[dir], m1[dir]);
+                        missing |= (ee[dir] == nullptr) | (me[dir] == nullptr);
+                    }
+                    if (missing) {
+                        touched.resize(mark);
+                        if (cap == INT64_MAX && !(ring_t0 == t0 && ring_t1 == t1)) want_trend(v, P, hi, d);
+                        want_ring(v, P, hi, d);
+                        return false;
+                    }
+                    // best neighbour: first maximum of MI in (t0, t1) order (R15)
+                    int best = 0;
+                    for (int i = 1; i < nc; ++i)
+                        if (ce[i]->mi > ce[best]->mi) best = i;
+                    it_t0 = t0;
+                    it_t1 = t1;
+                    it_pf = pf;
+                    it_nc = nc;
+                    it_b0 = c0s[best];
+                    it_b1 = c1s[best];
+                    it_bmi = ce[best]->mi;
+                    for (int dir = 0; dir < 2; ++dir) {
+                        it_app[dir] = applicable[dir];
+                        it_ee_nmi[dir] = applicable[dir] ? ee[dir]->nmi : 0.0;
+                        it_me_mi[dir] = applicable[dir] ? me[dir]->mi : 0.0;
+                    }
                 }
-                const size_t mark = touched.size();
-                bool missing = false;
-                const Eval* ce[8];
-                for (int i = 0; i < nc; ++i) {
-                    ce[i] = v.get(c0s[i], c1s[i]);
-                    missing |= (ce[i] == nullptr);
-                }
-                const Eval* ee[2] = {nullptr, nullptr};
-                const Eval* me[2] = {nullptr, nullptr};
-                for (int dir = 0; dir < 2; ++dir) {
-                    if (!applicable[dir]) continue;
-                    ee[dir] = v.get(e0[dir], e1[dir]);
-                    me[dir] = v.get(m0[dir], m1[dir]);
-                    missing |= (ee[dir] == nullptr) | (me[dir] == nullptr);
-                }
-                if (missing) {
-                    touched.resize(mark);
-                    want_ring(v, P, hi, d);
-                    return false;
-                }
-                // the iteration, exactly as Alg. 2 lines 7-21
-                int best = 0;
-                for (int i = 0; i < nc; ++i) {
-                    st.bu_neighbors += 1;
-                    if (i > 0 && ce[i]->mi > ce[best]->mi) best = i;
-                }
+                // the iteration, exactly as Alg. 2 lines 7-21 (an idle iteration at the same position and
+                // pruned state reuses the gathered values: the LAHC draw and the noise streaks still advance)
+                st.bu_neighbors += it_nc;
                 st.bu_iterations += 1;
                 for (int dir = 0; dir < 2; ++dir) {
-                    if (!applicable[dir]) continue;
+                    if (!it_app[dir]) continue;
                     st.bu_noise_checks += 1;
-                    const bool noisy = ee[dir]->nmi < tau && me[dir]->mi < Iw && Iw > 0.0;
+                    const bool noisy = it_ee_nmi[dir] < tau && it_me_mi[dir] < Iw && Iw > 0.0;
                     streak[dir] = noisy ? streak[dir] + 1 : 0;
                     if (streak[dir] >= P.p) {
                         pruned[dir] = true;
@@ -433,14 +521,19 @@ struct Climb {
                 }
                 const int r = (int)((rng.next() >> 32) % (uint64_t)P.h);
                 const double Ih = L[r];
-                const double bI = ce[best]->mi;
+                const double bI = it_bmi;
                 if (bI > Ih || bI > Iw) {
-                    t0 = c0s[best];
-                    t1 = c1s[best];
+                    const int da = (int)((it_b0 - t0) / d), db = (int)((it_b1 - t1) / d);
+                    run = (da == last_da && db == last_db) ? run + 1 : 1;
+                    last_da = da;
+                    last_db = db;
+                    t0 = it_b0;
+                    t1 = it_b1;
                     Iw = bI;
                     idle = 0;
                 } else {
                     idle += 1;
+                    run = 0;
                 }
                 if (Iw > Ih) L[r] = Iw;
                 continue;
@@ -471,7 +564,7 @@ struct BuJob {
     void init() { chain = lo_c; }
 
     void ensure_lookahead() {
-        const int la = P->lookahead > 0 ? P->lookahead : 64;
+        const int la = P->lookahead > 0 ? P->lookahead : 32;
         for (int j = 0; j < la; ++j) {
             const int64_t l = chain + (int64_t)j * P->s_min;
             if (l + P->s_min > hi) break;
@@ -511,9 +604,14 @@ struct BuJob {
         }
     }
 
-    void advance() {
+    // Pipelined driver: climbs belong to one of two groups by the parity of lo / s_min (neighbours on the
+    // chain alternate); advance(g) advances group g's climbs (g < 0: all) plus the chain bookkeeping.
+    int group_of(int64_t l) const { return (int)((l / P->s_min) & 1); }
+
+    void advance(int g = -1) {
         if (done) return;
-        for (auto& kv : climbs) kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first));
+        for (auto& kv : climbs)
+            if (g < 0 || group_of(kv.first) == g) kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first));
         ensure_lookahead();
         for (;;) {
             if (chain + P->s_min > hi) {
@@ -592,6 +690,7 @@ std::vector<isycos_result_window> merge_windows(std::vector<isycos_result_window
 }
 
 struct PairWork {
+    int32_t inflight = 0;  // batches in flight holding entries of this pair
     int32_t slot = -1;  // index into the active PairPtrs table
     int32_t pair_id = 0;
     PairPtrs ptrs{};
@@ -623,7 +722,6 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     int32_t next_pair = 0;
     std::vector<KsgWin> batch;
     std::vector<KsgRec> recs;
-    std::vector<Entry*> owners;
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
@@ -638,137 +736,187 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         }
     } closer{trace};
 
+    // Two batches in flight (P.pipeline): while the GPU evaluates one group's batch, the host advances
+    // the other group's jobs and submits its batch, so host time and GPU time overlap.  Group 0 = TD jobs
+    // + even BU climbs, group 1 = odd BU climbs.  Results never depend on this schedule: every decision
+    // reads canonical cached records only.
+    struct Flight {
+        bool busy = false;
+        std::vector<Entry*> owners;
+        std::vector<PairWork*> pws;
+    };
+    Flight fl[2];
+    const int n_groups = P.pipeline ? 2 : 1;
+    cudaStream_t sts[2] = {st, eng->second_stream()};
+    if (n_groups == 2) {  // the second slot's stream starts after everything already queued on st
+        Status s = eng->fork_second_stream(st);
+        if (!s.ok()) return s;
+    }
+    auto deliver = [&](int g) -> Status {
+        Flight& F = fl[g];
+        if (!F.busy) return Status{};
+        recs.resize(F.owners.size());
+        const auto t_ev = clk::now();
+        Status s = eng->collect(g, recs.data(), &bs);
+        eval_ms += std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
+        if (!s.ok()) return s;
+        for (size_t i = 0; i < F.owners.size(); ++i) {
+            Entry& e = *F.owners[i];
+            e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
+            e.ready = true;
+        }
+        for (PairWork* pw : F.pws) pw->inflight -= 1;
+        F.busy = false;
+        F.owners.clear();
+        F.pws.clear();
+        return Status{};
+    };
+
     for (;;) {
-        // admit pairs
-        while ((int)active.size() < max_active && next_pair < n_pairs) {
-            auto pw = std::make_unique<PairWork>();
-            pw->pair_id = pair_ids[next_pair];
-            pw->ptrs = pair_ptrs[next_pair];
-            for (auto [lo, hi] : plan) {
-                if (P.method & 1) {
-                    TdJob j;
-                    j.P = &P;
-                    j.cache = &pw->cache;
-                    j.pair_id = pw->pair_id;
-                    j.lo = lo;
-                    j.hi = hi;
-                    pw->td.push_back(std::move(j));
-                }
-                if (P.method & 2) {
-                    BuJob j;
-                    j.P = &P;
-                    j.cache = &pw->cache;
-                    j.pair_id = pw->pair_id;
-                    j.lo_c = lo;
-                    j.hi = hi;
-                    pw->bu.push_back(std::move(j));
-                }
+        bool submitted = false;
+        for (int g = 0; g < n_groups; ++g) {
+            {
+                Status s = deliver(g);
+                if (!s.ok()) return s;
             }
-            for (auto& j : pw->td) {
-                j.cache = &pw->cache;
-                j.init();
-            }
-            for (auto& j : pw->bu) {
-                j.cache = &pw->cache;
-                j.init();
-            }
-            active.push_back(std::move(pw));
-            ++next_pair;
-        }
-        if (active.empty()) break;
-        // advance every job
-        const auto t_adv = clk::now();
-        for (auto& pw : active) {
-            for (auto& j : pw->td) j.advance();
-            const auto t_bu = clk::now();
-            for (auto& j : pw->bu) j.advance();
-            bu_ms += std::chrono::duration<double, std::milli>(clk::now() - t_bu).count();
-        }
-        adv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_adv).count();
-        // retire finished pairs
-        for (size_t i = 0; i < active.size();) {
-            PairWork* pw = active[i].get();
-            if (pw->finished()) {
-                pw->cache.pending.clear();  // leftover speculative requests of discarded climbs
-                AlgStats ps;
-                for (int m = 1; m <= 2; ++m) {
-                    std::vector<isycos_result_window> per;
-                    if (m == 1)
-                        for (auto& j : pw->td) {
-                            per.insert(per.end(), j.results.begin(), j.results.end());
-                            ps.add(j.stats);
-                        }
-                    else
-                        for (auto& j : pw->bu) {
-                            per.insert(per.end(), j.results.begin(), j.results.end());
-                            ps.add(j.stats);
-                        }
-                    if (!(P.method & m)) continue;
-                    auto merged = merge_windows(per);
-                    all.insert(all.end(), merged.begin(), merged.end());
-                }
-                total.add(ps);
-                const FlatMap& fm = pw->cache.map;
-                for (size_t a = 0; a < fm.arena.size(); ++a)
-                    if (fm.arena[a].consumed) {
-                        const int64_t w = key_w(fm.arena_keys[a]);
-                        distinct_w += 1;
-                        distinct_pp += w * (w - 1);
+            // admit pairs
+            while ((int)active.size() < max_active && next_pair < n_pairs) {
+                auto pw = std::make_unique<PairWork>();
+                pw->pair_id = pair_ids[next_pair];
+                pw->ptrs = pair_ptrs[next_pair];
+                for (auto [lo, hi] : plan) {
+                    if (P.method & 1) {
+                        TdJob j;
+                        j.P = &P;
+                        j.cache = &pw->cache;
+                        j.pair_id = pw->pair_id;
+                        j.lo = lo;
+                        j.hi = hi;
+                        pw->td.push_back(std::move(j));
                     }
-                active.erase(active.begin() + i);
-            } else {
-                ++i;
+                    if (P.method & 2) {
+                        BuJob j;
+                        j.P = &P;
+                        j.cache = &pw->cache;
+                        j.pair_id = pw->pair_id;
+                        j.lo_c = lo;
+                        j.hi = hi;
+                        pw->bu.push_back(std::move(j));
+                    }
+                }
+                for (auto& j : pw->td) {
+                    j.cache = &pw->cache;
+                    j.init();
+                }
+                for (auto& j : pw->bu) {
+                    j.cache = &pw->cache;
+                    j.init();
+                }
+                active.push_back(std::move(pw));
+                ++next_pair;
             }
-        }
-        // one batch of every pending window of every active pair
-        std::vector<PairPtrs> table;
-        batch.clear();
-        owners.clear();
-        for (auto& pw : active) {
-            if (pw->cache.pending.empty()) continue;
-            pw->slot = (int32_t)table.size();
-            table.push_back(pw->ptrs);
-            for (uint64_t k : pw->cache.pending) {
-                const int64_t t0 = key_t0(k), w = key_w(k);
-                if (t0 < 0 || t0 + w > n || w <= P.k)  // never hand the kernels an out-of-range window
-                    return make_err(ISYCOS_E_RANGE, "internal: search requested window [" + std::to_string(t0) +
-                                                        ", " + std::to_string(t0 + w) + ")");
-                batch.push_back(KsgWin{t0, (int32_t)w, pw->slot, -1});
-                owners.push_back(pw->cache.map.find(k));
+            // advance this group's jobs
+            const auto t_adv = clk::now();
+            for (auto& pw : active) {
+                if (g == 0)
+                    for (auto& j : pw->td) j.advance();
+                const auto t_bu = clk::now();
+                for (auto& j : pw->bu) j.advance(n_groups == 1 ? -1 : g);
+                bu_ms += std::chrono::duration<double, std::milli>(clk::now() - t_bu).count();
             }
-            pw->cache.pending.clear();
+            adv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_adv).count();
+            // retire finished pairs (none of their entries may be in flight)
+            for (size_t i = 0; i < active.size();) {
+                PairWork* pw = active[i].get();
+                if (pw->finished() && pw->inflight == 0) {
+                    pw->cache.pending.clear();  // leftover speculative requests of discarded climbs
+                    AlgStats ps;
+                    for (int m = 1; m <= 2; ++m) {
+                        std::vector<isycos_result_window> per;
+                        if (m == 1)
+                            for (auto& j : pw->td) {
+                                per.insert(per.end(), j.results.begin(), j.results.end());
+                                ps.add(j.stats);
+                            }
+                        else
+                            for (auto& j : pw->bu) {
+                                per.insert(per.end(), j.results.begin(), j.results.end());
+                                ps.add(j.stats);
+                            }
+                        if (!(P.method & m)) continue;
+                        auto merged = merge_windows(per);
+                        all.insert(all.end(), merged.begin(), merged.end());
+                    }
+                    total.add(ps);
+                    pw->cache.map.for_each([&](const Entry& en) {
+                        if (en.consumed) {
+                            const int64_t w = key_w(en.key);
+                            distinct_w += 1;
+                            distinct_pp += w * (w - 1);
+                        }
+                    });
+                    active.erase(active.begin() + i);
+                } else {
+                    ++i;
+                }
+            }
+            // one batch of every pending window of every active pair (finished pairs: leftovers dropped)
+            std::vector<PairPtrs> table;
+            batch.clear();
+            Flight& F = fl[g];
+            for (auto& pw : active) {
+                if (pw->cache.pending.empty()) continue;
+                if (pw->finished()) {
+                    pw->cache.pending.clear();
+                    continue;
+                }
+                pw->slot = (int32_t)table.size();
+                table.push_back(pw->ptrs);
+                for (uint64_t k : pw->cache.pending) {
+                    const int64_t t0 = key_t0(k), w = key_w(k);
+                    if (t0 < 0 || t0 + w > n || w <= P.k)  // never hand the kernels an out-of-range window
+                        return make_err(ISYCOS_E_RANGE, "internal: search requested window [" + std::to_string(t0) +
+                                                            ", " + std::to_string(t0 + w) + ")");
+                    batch.push_back(KsgWin{t0, (int32_t)w, pw->slot, -1});
+                    F.owners.push_back(pw->cache.map.find(k));
+                }
+                pw->cache.pending.clear();
+                pw->inflight += 1;
+                F.pws.push_back(pw.get());
+            }
+            if (batch.empty()) continue;
+            const auto t_ev = clk::now();
+            Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
+                                   P.variant, DebugOut{}, sts[g], P.flags, &bs);
+            const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
+            eval_ms += ev_ms;
+            if (!s.ok()) return s;
+            F.busy = true;
+            submitted = true;
+            if (trace) {  // per-round trace (ISYCOS_TRACE=<path>): round, host ms since last submit, submit ms, batch
+                int64_t sw2 = 0, wmax = 0;
+                for (const KsgWin& kw : batch) {
+                    sw2 += (int64_t)kw.w * kw.w;
+                    wmax = std::max<int64_t>(wmax, kw.w);
+                }
+                const double host = std::chrono::duration<double, std::milli>(t_ev - t_last).count();
+                std::fprintf(trace, "%lld %.4f %.4f %zu %lld %lld\n", (long long)round_no, host, ev_ms, batch.size(),
+                             (long long)sw2, (long long)wmax);
+            }
+            ++round_no;
+            t_last = clk::now();
         }
-        if (batch.empty()) {
+        if (active.empty() && !fl[0].busy && !fl[1].busy) break;
+        if (!submitted && !fl[0].busy && !fl[1].busy) {
             bool any_active = false;
             for (auto& pw : active)
                 if (!pw->finished()) any_active = true;
             if (any_active) return make_err(ISYCOS_E_CUDA, "search driver stalled (internal error)");
-            continue;
         }
-        recs.resize(batch.size());
-        const auto t_ev = clk::now();
-        Status s = eng->evaluate(table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
-                                 P.variant, recs.data(), DebugOut{}, st, P.flags, &bs);
-        const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
-        eval_ms += ev_ms;
+    }
+    if (n_groups == 2) {
+        Status s = eng->join_second_stream(st);
         if (!s.ok()) return s;
-        if (trace) {  // per-round trace (ISYCOS_TRACE=<path>): round, host ms since last eval, eval ms, batch
-            int64_t sw2 = 0, wmax = 0;
-            for (const KsgWin& kw : batch) {
-                sw2 += (int64_t)kw.w * kw.w;
-                wmax = std::max<int64_t>(wmax, kw.w);
-            }
-            const double host = std::chrono::duration<double, std::milli>(t_ev - t_last).count();
-            std::fprintf(trace, "%lld %.4f %.4f %zu %lld %lld\n", (long long)round_no, host, ev_ms, batch.size(),
-                         (long long)sw2, (long long)wmax);
-        }
-        ++round_no;
-        t_last = clk::now();
-        for (size_t i = 0; i < batch.size(); ++i) {
-            Entry& e = *owners[i];
-            e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
-            e.ready = true;
-        }
     }
     std::stable_sort(all.begin(), all.end(), [](const isycos_result_window& a, const isycos_result_window& b) {
         if (a.pair != b.pair) return a.pair < b.pair;

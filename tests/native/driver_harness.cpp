@@ -6,6 +6,7 @@
 // oracle search exactly (results and algorithm-level counters), and profile its host time.  The
 // product library never links this file or the oracle.
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -37,6 +38,9 @@ struct KeyHash {
 };
 std::unordered_map<Key, isy::KsgRec, KeyHash> g_cache;
 bool g_use_cache = false;
+bool g_parallel = false;  // OpenMP over the batch's missing windows (profiling runs)
+std::vector<isy::KsgRec> g_slot_recs[2];
+bool g_slot_busy[2] = {false, false};
 }  // namespace
 
 namespace isy {
@@ -60,6 +64,7 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
 Status Engine::evaluate(const PairPtrs* pairs, int32_t, const KsgWin* wins, int64_t n, int32_t k, int32_t variant,
                         KsgRec* recs_host, const DebugOut&, cudaStream_t, uint32_t, BatchStats* bs) {
     const auto t = std::chrono::steady_clock::now();
+    std::vector<int64_t> miss;
     for (int64_t i = 0; i < n; ++i) {
         const PairPtrs& p = pairs[wins[i].pair];
         const Key key{p.x, wins[i].t0, wins[i].w};
@@ -70,14 +75,30 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t, const KsgWin* wins, int6
                 continue;
             }
         }
+        miss.push_back(i);
+    }
+    // the oracle's psi table grows lazily (not thread-safe): evaluate the widest window first, serially
+    int64_t widest = -1;
+    for (int64_t i : miss)
+        if (widest < 0 || wins[i].w > wins[widest].w) widest = i;
+    int bad = 0;
+    auto eval_one = [&](int64_t i) {
+        const PairPtrs& p = pairs[wins[i].pair];
         int64_t w2[2] = {wins[i].t0, wins[i].t0 + wins[i].w};
         double mi, h, nmi;
         int64_t sp, sl;
         int32_t z;
         int rc = oracle_mi_batch(p.x, p.y, g_n, w2, 1, k, variant, &mi, &h, &nmi, &sp, &sl, &z);
-        if (rc) return make_err(ISYCOS_E_INVAL, "oracle_mi_batch failed");
+        if (rc) bad = 1;
         recs_host[i] = KsgRec{mi, h, nmi, sp, sl, z, 0};
-        if (g_use_cache) g_cache[key] = recs_host[i];
+    };
+    if (widest >= 0) eval_one(widest);
+#pragma omp parallel for schedule(dynamic, 1) if (g_parallel)
+    for (int64_t m = 0; m < (int64_t)miss.size(); ++m)
+        if (miss[m] != widest) eval_one(miss[m]);
+    if (bad) return make_err(ISYCOS_E_INVAL, "oracle_mi_batch failed");
+    for (int64_t i : miss) {
+        if (g_use_cache) g_cache[Key{pairs[wins[i].pair].x, wins[i].t0, wins[i].w}] = recs_host[i];
         bs->point_pairs += (int64_t)wins[i].w * (wins[i].w - 1);
     }
     bs->windows += n;
@@ -86,19 +107,37 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t, const KsgWin* wins, int6
     g_eval_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
     return Status{};
 }
+Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
+                      int32_t variant, const DebugOut& dbg, cudaStream_t st, uint32_t flags, BatchStats* bs) {
+    // the stub evaluates at submit time and hands the records out at collect (same observable order)
+    g_slot_recs[si].resize(n);
+    g_slot_busy[si] = true;
+    return evaluate(pairs, n_pairs, wins, n, k, variant, g_slot_recs[si].data(), dbg, st, flags, bs);
+}
+Status Engine::collect(int si, KsgRec* recs_host, BatchStats*) {
+    if (!g_slot_busy[si]) return Status{};
+    g_slot_busy[si] = false;
+    std::memcpy(recs_host, g_slot_recs[si].data(), g_slot_recs[si].size() * sizeof(KsgRec));
+    return Status{};
+}
+Status Engine::fork_second_stream(cudaStream_t) { return Status{}; }
+Status Engine::join_second_stream(cudaStream_t) { return Status{}; }
 Engine::~Engine() {}
 }  // namespace isy
 
 extern "C" {
 
 // keep evaluated records across calls (same series buffers) so profiling re-runs skip the oracle
+void harness_parallel(int on) { g_parallel = on != 0; }
+
 void harness_use_cache(int on) {
     g_use_cache = on != 0;
     if (!on) g_cache.clear();
 }
 
 struct HarnessParams {
-    int32_t k, method, noise, p, h, t_max_idle, n_chunks, lookahead, bu_depth, anchor, spec_cap, _pad;
+    int32_t k, method, noise, p, h, t_max_idle, n_chunks, lookahead, bu_depth, anchor, spec_cap, trend, pipeline,
+        _pad;
     int64_t s_min, s_max, delta_td, delta_bu;
     double sigma, tau_ratio;
     uint64_t seed;
@@ -120,6 +159,8 @@ int harness_search(const float* const* series, int64_t n, const int32_t* pairs, 
     P.n_chunks = hp->n_chunks;
     if (hp->lookahead > 0) P.lookahead = hp->lookahead;
     if (hp->bu_depth > 0) P.bu_depth = hp->bu_depth;
+    if (hp->trend >= 0) P.trend_depth = hp->trend;
+    if (hp->pipeline >= 0) P.pipeline = hp->pipeline != 0;
     if (hp->anchor >= 0) P.anchor_lookahead = hp->anchor;
     if (hp->spec_cap >= 0) P.spec_cap_mult = hp->spec_cap;
     P.s_min = hp->s_min;
@@ -150,4 +191,28 @@ int harness_search(const float* const* series, int64_t n, const int32_t* pairs, 
     *evaluated = g_evaluated;
     return 0;
 }
+}
+
+// profiling helpers: persist the record cache of a single-pair run (keys re-bound to `x` on load)
+extern "C" int harness_cache_save(const char* path) {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return -1;
+    for (auto& kv : g_cache) {
+        std::fwrite(&kv.first.t0, 8, 1, f);
+        std::fwrite(&kv.first.w, 4, 1, f);
+        std::fwrite(&kv.second, sizeof(isy::KsgRec), 1, f);
+    }
+    std::fclose(f);
+    return 0;
+}
+extern "C" int harness_cache_load(const char* path, const float* x) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return -1;
+    int64_t t0;
+    int32_t w;
+    isy::KsgRec r;
+    while (std::fread(&t0, 8, 1, f) == 1 && std::fread(&w, 4, 1, f) == 1 && std::fread(&r, sizeof(r), 1, f) == 1)
+        g_cache[Key{x, t0, w}] = r;
+    std::fclose(f);
+    return 0;
 }

@@ -21,7 +21,7 @@ def build():
     if os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(f) for f in deps):
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
+    subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
                            "-I", os.path.join(ROOT, "include"), "-I",
                            os.path.join(ROOT, "paper_2204_09131_b200", "csrc"), "-I", "/usr/local/cuda/include",
                            "-o", tmp, *SRCS])
@@ -31,7 +31,7 @@ def build():
 
 class HarnessParams(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("k", "method", "noise", "p", "h", "t_max_idle", "n_chunks", "lookahead",
-                                         "bu_depth", "anchor", "spec_cap", "_pad")] + \
+                                         "bu_depth", "anchor", "spec_cap", "trend", "pipeline", "_pad")] + \
                [("s_min", C.c_int64), ("s_max", C.c_int64), ("delta_td", C.c_int64), ("delta_bu", C.c_int64),
                 ("sigma", C.c_double), ("tau_ratio", C.c_double), ("seed", C.c_uint64),
                 ("sizes", C.POINTER(C.c_int64)), ("n_sizes", C.c_int64)]
@@ -47,6 +47,7 @@ def lib():
         from paper_2204_09131_b200._capi import ResultWindow, SearchStats
 
         _lib.harness_use_cache.argtypes = [C.c_int]
+        _lib.harness_parallel.argtypes = [C.c_int]
         _lib.harness_search.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.POINTER(HarnessParams),
                                         C.POINTER(ResultWindow), C.c_int64, C.POINTER(C.c_int64),
                                         C.POINTER(SearchStats), C.POINTER(C.c_double), C.POINTER(C.c_int64)]
@@ -65,7 +66,7 @@ def search(series, pairs, sc, **kw):
     P3 = np.asarray(pr, np.int32)
     hp = HarnessParams()
     d = dict(k=sc.k, method=sc.method, noise=int(sc.noise), p=sc.p, h=sc.h, t_max_idle=sc.t_max_idle,
-             n_chunks=sc.n_chunks, lookahead=0, bu_depth=0, anchor=-1, spec_cap=-1, s_min=sc.s_min, s_max=sc.s_max,
+             n_chunks=sc.n_chunks, lookahead=0, bu_depth=0, anchor=-1, spec_cap=-1, trend=-1, pipeline=-1, s_min=sc.s_min, s_max=sc.s_max,
              delta_td=sc.delta_td, delta_bu=sc.delta_bu, sigma=sc.sigma, tau_ratio=sc.tau_ratio, seed=sc.seed)
     d.update(kw)
     for key, v in d.items():
