@@ -186,6 +186,56 @@ def cpu_baseline(args, wl, desc):
             "windows_per_s": st["distinct_windows"] / dt}
 
 
+def sweep_cfg3(isy, stream, reps: int):
+    """Secondary line: the configs[2] estimator sweep (17,460 windows, w = 1,024 / 4,096 / 16,384, k = 3/4/8)
+    through isycos_mi_batch_ex with device-resident series and windows — the throughput form of the
+    kernels, next to the latency-bound search step.  Timed on the device (CUDA events on `stream`) after
+    one warm-up pass; per-path kernel time from ISYCOS_F_PROFILE events."""
+    import torch
+
+    import datagen
+
+    wl = datagen.cfg3()
+    dx, dy = (torch.from_numpy(s).cuda() for s in wl.series)
+    W = datagen.sweep_windows(len(wl.series[0]), wl.sweep["sizes"], wl.sweep["stride"])
+    dW = torch.from_numpy(W).cuda()
+    out = {"mi": torch.empty(len(W), dtype=torch.float64, device="cuda")}
+    ks = wl.sweep["ks"]
+    bf = 2.0 * float(((W[:, 1] - W[:, 0]) * (W[:, 1] - W[:, 0] - 1)).sum()) * len(ks)
+
+    def one(profile):
+        agg = {}
+        for k in ks:
+            r = isy.isycos_mi_batch_ex(dx, dy, dW, k, outputs=("mi",), out=out, stream=stream, profile=profile)
+            for f, v in r["stats"].items():
+                agg[f] = agg.get(f, 0) + v
+        return agg
+
+    one(False)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    st = {}
+    for _ in range(reps):
+        for f, v in one(True).items():
+            st[f] = st.get(f, 0) + v
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / reps
+    peak = peak_compares(1965.0)
+    alg = (st["scan_steps"] + st["search_probes"]) / reps
+    kms = st["sorted_kernel_ms"] / reps
+    return {"workload": "cfg3 sweep (configs[2]): 17,460 windows x k in {3,4,8} per step",
+            "ms_per_step": ms, "windows_per_s": len(W) * len(ks) / (ms / 1e3),
+            "bruteforce_equivalent_compares_per_s": bf / (ms / 1e3),
+            "roofline": {"bound": "alu", "kernel": "sort_window_kernel + sorted_knn_kernel (+ rank_merge_kernel)",
+                         "achieved": alg / (kms / 1e3) / 1e12 if kms else None, "peak": peak / 1e12,
+                         "unit": "Tcompare/s", "frac": alg / (kms / 1e3) / peak if kms else None,
+                         "kernel_share_of_step": kms / ms if ms else None,
+                         "algorithmic_compares_per_step": alg,
+                         "scan_steps_per_point": st["scan_steps"] / max(1, st["sorted_points"])}}
+
+
 # ----------------------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -196,6 +246,7 @@ def main():
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--ref-prefix", type=int, default=25_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the secondary configs[2] throughput line")
     ap.add_argument("--lookahead", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -362,6 +413,8 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args, wl, desc)
+        if not args.no_sweep:
+            line["throughput_sweep"] = sweep_cfg3(isy, stream, max(1, args.steps // 2))
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

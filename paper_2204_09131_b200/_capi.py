@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libisycos.so")
 ISYCOS_OK, E_INVAL, E_RANGE, E_TOO_FEW, E_TRUNC, E_CUDA, E_NOMEM, E_NCCL = 0, -1, -2, -3, -4, -5, -6, -7
 F_PROFILE = 1
 F_BRUTE = 2   # force the brute-force kernels (A/B and test knob; results identical)
+F_UNFUSED = 4  # sorted path in its throughput form only (no fused latency kernel)
 MAX_K = 16
 MAX_W = 262144
 ERROR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_RANGE", -3: "E_TOO_FEW", -4: "E_TRUNC", -5: "E_CUDA",
@@ -176,7 +177,7 @@ def isycos_mi_batch(x, y, windows, k: int = 4):
 
 def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", "s_psi", "s_log", "zero_eps"),
                        debug: bool = False, profile: bool = False, stream=None, out=None, variant: int = 0,
-                       brute: bool = False):
+                       brute: bool = False, unfused: bool = False):
     """Full per-window records (and optional per-point eps/n_x/n_y).  variant 0 = KSG-1, 1 = KSG-2.
 
     x, y: float32 numpy arrays or torch tensors (CPU or CUDA); windows: (n, 2) int64 array/tensor.
@@ -189,7 +190,7 @@ def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", 
     res = {}
     o = MiOpts()
     o.variant = int(variant)
-    o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0)
+    o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
     o.stream = _stream_ptr(stream)
     keep = []
 
@@ -231,8 +232,8 @@ def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", 
 def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=None, noise: bool = True,
                   tau_ratio: float = 0.25, p: int = 3, sigma: float = 0.2, method: int = 3, delta_td: int = 0,
                   delta_bu: int = 0, t_max_idle: int = 3, h: int = 5, n_chunks: int = 1, lookahead: int = 0,
-                  seed: int = 0, variant: int = 0, profile: bool = False, brute: bool = False, stream=None,
-                  capacity: int = 1 << 16):
+                  seed: int = 0, variant: int = 0, profile: bool = False, brute: bool = False,
+                  unfused: bool = False, stream=None, capacity: int = 1 << 16):
     """SYCOS search over series pairs.  Returns (results, stats).
 
     series: list of float32 arrays / tensors (host or CUDA, all alike, same length)
@@ -259,7 +260,7 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
     o.sigma, o.method, o.variant = float(sigma), int(method), int(variant)
     o.delta_td, o.delta_bu, o.t_max_idle, o.h = int(delta_td), int(delta_bu), int(t_max_idle), int(h)
     o.n_chunks, o.lookahead, o.seed = int(n_chunks), int(lookahead), int(seed) & ((1 << 64) - 1)
-    o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0)
+    o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
     o.stream = _stream_ptr(stream)
     while True:
         outw = (ResultWindow * max(1, capacity))()

@@ -66,6 +66,8 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
     int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
     int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
+    int32_t scan_mode;       // sorted path phase A: 0 two-sided blocks, 1 nearer-side blocks
+    int32_t pad3_;
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -202,6 +204,7 @@ private:
     double* lnc_ = nullptr;
     int64_t psi_max_ = 0;
     int32_t knn_mode_ = 1;
+    int32_t scan_mode_ = 1;
     int* dflag_ = nullptr;
     Slot slots_[2];
     bool sorted_on_ = true;

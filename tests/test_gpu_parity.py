@@ -43,9 +43,9 @@ def assert_records_equal(got, ref, label=""):
     assert np.max(np.abs(np.asarray(got["mi"]) - np.asarray(ref["mi"]))) <= 1e-9
 
 
-def check_windows(isy, orc, x, y, W, k, debug=False, label="", variant=0, brute=False):
+def check_windows(isy, orc, x, y, W, k, debug=False, label="", variant=0, brute=False, unfused=False):
     W = np.asarray(W, np.int64).reshape(-1, 2)
-    got = isy.isycos_mi_batch_ex(x, y, W, k, debug=debug, variant=variant, brute=brute)
+    got = isy.isycos_mi_batch_ex(x, y, W, k, debug=debug, variant=variant, brute=brute, unfused=unfused)
     ref = orc.mi_batch(x, y, W, k, variant=variant)
     assert_records_equal(got, ref, label)
     if debug:
@@ -82,7 +82,8 @@ SIZES = [5, 17, 32, 33, 64, 65, 100, 128, 129, 255, 256, 257, 300, 512, 513, 777
 
 
 @pytest.mark.parametrize("k", [1, 3, 4, 8, 16])
-def test_size_classes_random_windows(isy, orc, k):
+@pytest.mark.parametrize("unfused", [False, True])
+def test_size_classes_random_windows(isy, orc, k, unfused):
     wl = datagen.cfg2(n=20_000)
     x, y = wl.series
     rng = np.random.default_rng(k)
@@ -95,7 +96,7 @@ def test_size_classes_random_windows(isy, orc, k):
     n = len(x)
     W += [(0, 37), (n - 41, n), (n - 4100, n), (1, 1 + 4099), (2, 2 + 515), (3, 3 + 130)]
     W = [(a, b) for (a, b) in W if b - a > k]
-    check_windows(isy, orc, x, y, W, k, debug=(k == 4), label=f"k={k}")
+    check_windows(isy, orc, x, y, W, k, debug=(k == 4), label=f"k={k} unfused={unfused}", unfused=unfused)
 
 
 def test_tie_torture(isy, orc):
@@ -111,9 +112,10 @@ def test_tie_torture(isy, orc):
     yd = np.repeat(datagen.f32(st.normal(n // 4)), 4)[:n]
     W = [(0, 64), (10, 300), (100, 1100), (0, 4500), (1000, 1400), (990, 1500), (1100, 1200), (1, 5000)]
     for k in (1, 4, 8):
-        check_windows(isy, orc, xi, yi, W, k, debug=(k == 4), label=f"int k={k}")
-        check_windows(isy, orc, xc, yc, W, k, label=f"const k={k}")
-        check_windows(isy, orc, xd, yd, W, k, debug=(k == 4), label=f"dup k={k}")
+        for uf in (False, True):
+            check_windows(isy, orc, xi, yi, W, k, debug=(k == 4), label=f"int k={k} uf={uf}", unfused=uf)
+            check_windows(isy, orc, xc, yc, W, k, label=f"const k={k} uf={uf}", unfused=uf)
+            check_windows(isy, orc, xd, yd, W, k, debug=(k == 4), label=f"dup k={k} uf={uf}", unfused=uf)
 
 
 def test_extreme_magnitudes(isy, orc):
@@ -232,7 +234,7 @@ def test_brute_path_large_windows(isy, orc):
 
 # ---------------------------------------------------------------- KSG-2 (paper's literal Eq. 2; NEXT-1)
 @pytest.mark.parametrize("k", [1, 4, 8])
-@pytest.mark.parametrize("brute", [False, True])
+@pytest.mark.parametrize("brute", [False, True, "unfused"])
 def test_ksg2_size_classes(isy, orc, k, brute):
     """KSG-2 through every kernel: warp (w <= 256), tile (brute), sorted (w >= 257) incl. a multi-j-tile
     window; per-point eps, n_x, n_y bit-exact (n = the closed <= d_x counts)."""
@@ -245,7 +247,8 @@ def test_ksg2_size_classes(isy, orc, k, brute):
             continue
         t0 = int(rng.integers(0, len(x) - w))
         W.append((t0, t0 + w))
-    check_windows(isy, orc, x, y, W, k, debug=True, label=f"ksg2 k={k} brute={brute}", variant=1, brute=brute)
+    check_windows(isy, orc, x, y, W, k, debug=True, label=f"ksg2 k={k} brute={brute}", variant=1,
+                  brute=brute is True, unfused=brute == "unfused")
 
 
 def test_ksg2_ties(isy, orc):
@@ -262,11 +265,12 @@ def test_ksg2_ties(isy, orc):
     yc[2000:2300] = 2.0
     W = [(0, 40), (5, 200), (50, 700), (0, 4500), (2000, 2300), (1990, 2400)]
     for k in (1, 3, 4):
-        for brute in (False, True):
+        for brute in (False, True, "unfused"):
             lab = f"k={k} brute={brute}"
-            check_windows(isy, orc, xi, yi, W, k, debug=True, label="ksg2 int " + lab, variant=1, brute=brute)
-            check_windows(isy, orc, xd, yd, W, k, debug=True, label="ksg2 dup " + lab, variant=1, brute=brute)
-            check_windows(isy, orc, xc, yc, W, k, debug=True, label="ksg2 const " + lab, variant=1, brute=brute)
+            kw = dict(debug=True, variant=1, brute=brute is True, unfused=brute == "unfused")
+            check_windows(isy, orc, xi, yi, W, k, label="ksg2 int " + lab, **kw)
+            check_windows(isy, orc, xd, yd, W, k, label="ksg2 dup " + lab, **kw)
+            check_windows(isy, orc, xc, yc, W, k, label="ksg2 const " + lab, **kw)
 
 
 def test_ksg2_cfg1_sweep_and_xl(isy, orc):
