@@ -115,10 +115,14 @@ class SearchConfig:
     delta_td: int = 0  # 0 => max(1, s/4) per layer
     delta_bu: int = 0  # 0 => max(1, s_min/3)
     n_chunks: int = 1
-    method: int = 3  # 1 TD, 2 BU, 3 BOTH
+    method: int = 3  # 1 TD, 2 BU, 3 BOTH, 4 AUTO (iSYCOS, Alg. 3)
     noise: bool = True
     seed: int = 0
     sizes: list = field(default_factory=list)  # explicit TD layer sizes; [] => halving
+    auto_M: int = 0  # AUTO: partitions (0 => 20)
+    auto_m: int = 0  # AUTO: sampled partitions (0 => 6)
+    auto_alpha: float = 0.0  # AUTO: runtime weight (0 => 0.5)
+    auto_rho: float = 0.0  # AUTO: small-window cut rho * s_max (0 => 0.5)
 
 
 @dataclass
@@ -296,6 +300,42 @@ def cfg5(seed: int = 5, n: int = 10_000_000, n_series: int = 16, n_chunks: int =
         planted[pairs.index((xi, yi))] = sorted(placed)
     sc = SearchConfig(k=4, s_min=128, s_max=65_536, seed=seed, method=1, noise=True, n_chunks=n_chunks)
     return Workload(name="cfg5", series=[f32(s) for s in series], pairs=pairs, search=sc, planted=planted)
+
+
+def scenario(kind: str, seed: int = 0, n: int = 8192) -> Workload:
+    """Fig. 1 scenarios (the figures are missing, the text defines them): "dense" = large
+    correlated windows located close or next to each other (the top-down case); "sparse" = small
+    correlated windows sparsely distributed (the bottom-up case).  x, e ~ N(0,1); outside the planted
+    windows y ~ N(0,1) independent; inside y = x + 0.3 e.  Search: s_min 64, s_max 1024, method AUTO with
+    M = 8 partitions of 1024 samples, m = 4 sampled."""
+    st = Stream(seed, 21 if kind == "dense" else 22)
+    x = st.normal(n)
+    y = st.normal(n)
+    e = st.normal(n)
+    planted = []
+    if kind == "dense":      # blocks of 1024-2048 separated by gaps of 64-192 samples
+        t = st.integer(0, 128)
+        while True:
+            L = st.integer(1024, 2048)
+            if t + L > n:
+                break
+            planted.append((t, t + L))
+            t += L + st.integer(64, 192)
+    elif kind == "sparse":   # windows of 64-128 samples, 600-1000 apart
+        t = st.integer(100, 400)
+        while True:
+            L = st.integer(64, 128)
+            if t + L > n:
+                break
+            planted.append((t, t + L))
+            t += L + st.integer(600, 1000)
+    else:
+        raise ValueError(kind)
+    for (a, b) in planted:
+        y[a:b] = x[a:b] + 0.3 * e[a:b]
+    sc = SearchConfig(k=4, s_min=64, s_max=1024, seed=seed, method=4, auto_M=8, auto_m=4)
+    return Workload(name=f"scenario-{kind}", series=[f32(x), f32(y)], pairs=[(0, 1)], search=sc,
+                    planted={0: [(a, b, "linear") for (a, b) in planted]})
 
 
 def sweep_windows(n: int, sizes, stride: int):

@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define ISYCOS_ABI_VERSION 1
+#define ISYCOS_ABI_VERSION 2
 #define ISYCOS_MAX_K 16
 #define ISYCOS_MAX_W 262144 /* 2^18: int64 fixed-point bound of the digamma sums */
 
@@ -157,7 +157,7 @@ typedef struct {
 
 typedef struct {
     double sigma;         /* correlation threshold on normalized MI (default 0.2) */
-    int32_t method;       /* 1 = TD, 2 = BU, 3 = both (results tagged per method) */
+    int32_t method;       /* 1 = TD, 2 = BU, 3 = both (results tagged per method), 4 = AUTO (below) */
     int32_t variant;      /* 0 = KSG-1 (default), 1 = KSG-2 (Eq. 2 literal) */
     int64_t delta_td;     /* TD sliding step; 0 => max(1, s/4) per layer */
     int64_t delta_bu;     /* BU neighbour step; 0 => max(1, s_min/3) */
@@ -168,6 +168,13 @@ typedef struct {
     uint64_t seed;        /* LAHC random streams: SplitMix64 keyed by (seed, pair id, climb start) */
     uint32_t flags;       /* ISYCOS_F_* */
     void* stream;         /* cudaStream_t; NULL = the library's own stream */
+    /* method 4 (AUTO, iSYCOS Alg. 3): M partitions of floor(n/M) samples, m of them sampled
+     * (SplitMix64 keyed by (seed, pair id)); SYCOS_TD and SYCOS_BU run alone on each; runtime proxy
+     * t = eval_cost of the run; windows small iff |w| <= rho * s_max; Eqs. 6-9 with weight alpha;
+     * TD iff nscore_TD > nscore_BU; the chosen method then runs on the whole series (results tagged
+     * with it).  Zero => defaults M = 20, m = 6, alpha = 0.5, rho = 0.5.  Needs m <= M, n / M >= s_min. */
+    int32_t auto_M, auto_m;
+    double auto_alpha, auto_rho;
 } isycos_search_opts;
 
 /* One accepted window (Def 3.5).  Records are sorted by (pair, method, t0); per (pair,
@@ -184,6 +191,9 @@ typedef struct {
     int64_t td_windows, td_noise_checks, td_skips, td_accepted;
     int64_t bu_climbs, bu_iterations, bu_neighbors, bu_noise_checks, bu_prunes, bu_accepted;
     int64_t distinct_windows, distinct_pairs; /* per pair, union over chunks and methods */
+    int64_t eval_cost;      /* sum over distinct windows computed of w * ceil(log2 w) (t_w ~ w log w) */
+    int64_t auto_td, auto_bu;               /* method AUTO: pairs for which Alg. 3 chose TD / BU */
+    double auto_nscore_td, auto_nscore_bu;  /* method AUTO: sums over pairs of nscore_TD / nscore_BU (Eqs. 8-9) */
     isycos_kernel_stats kernel;
 } isycos_search_stats;
 
@@ -197,7 +207,8 @@ typedef struct {
  *   out_count    number of records found (also set on E_TRUNC)
  *   out_stats    optional counters
  * Errors: E_INVAL (bad params: 2 <= s_min <= s_max <= n, k < s_min, 0 < sigma <= 1,
- *   0 <= tau_ratio < 1, h >= 1, p >= 1, t_max_idle >= 0, method in 1..3, n_chunks >= 1),
+ *   0 <= tau_ratio < 1, h >= 1, p >= 1, t_max_idle >= 0, method in 1..4, n_chunks >= 1; AUTO:
+ *   m <= M, n / M >= s_min, alpha and rho in [0, 1]),
  *   E_TRUNC (first out_capacity records written, *out_count = required), E_CUDA, E_NOMEM.
  */
 int isycos_search(const float* const* series, int32_t n_series, int64_t n, const isycos_pair* pairs,

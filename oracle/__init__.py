@@ -34,6 +34,7 @@ class OParams(C.Structure):
         ("s_min", C.c_int64), ("s_max", C.c_int64), ("delta_td", C.c_int64), ("delta_bu", C.c_int64),
         ("sigma", C.c_double), ("tau_ratio", C.c_double), ("seed", C.c_uint64),
         ("sizes", C.POINTER(C.c_int64)), ("n_sizes", C.c_int32), ("_pad", C.c_int32),
+        ("auto_M", C.c_int32), ("auto_m", C.c_int32), ("auto_alpha", C.c_double), ("auto_rho", C.c_double),
     ]
 
 
@@ -44,11 +45,12 @@ class OResult(C.Structure):
 
 STAT_FIELDS = ["td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs",
                "bu_iterations", "bu_neighbors", "bu_noise_checks", "bu_prunes", "bu_accepted",
-               "distinct_windows", "distinct_pairs"]
+               "distinct_windows", "distinct_pairs", "eval_cost", "auto_td", "auto_bu"]
+STAT_FIELDS_F = ["auto_nscore_td", "auto_nscore_bu"]
 
 
 class OStats(C.Structure):
-    _fields_ = [(f, C.c_int64) for f in STAT_FIELDS]
+    _fields_ = [(f, C.c_int64) for f in STAT_FIELDS] + [(f, C.c_double) for f in STAT_FIELDS_F]
 
 
 MIFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_double),
@@ -154,12 +156,14 @@ def mi_batch(x, y, windows, k: int = 4, variant: int = 0):
 
 def make_params(sc=None, **kw) -> OParams:
     d = dict(k=4, variant=0, method=3, noise=1, p=3, h=5, t_max_idle=3, n_chunks=1, s_min=64,
-             s_max=512, delta_td=0, delta_bu=0, sigma=0.2, tau_ratio=0.25, seed=0, sizes=None)
+             s_max=512, delta_td=0, delta_bu=0, sigma=0.2, tau_ratio=0.25, seed=0, sizes=None,
+             auto_M=0, auto_m=0, auto_alpha=0.0, auto_rho=0.0)
     if sc is not None:
         d.update(k=sc.k, method=sc.method, noise=int(sc.noise), p=sc.p, h=sc.h, t_max_idle=sc.t_max_idle,
                  n_chunks=sc.n_chunks, s_min=sc.s_min, s_max=sc.s_max, delta_td=sc.delta_td,
                  delta_bu=sc.delta_bu, sigma=sc.sigma, tau_ratio=sc.tau_ratio, seed=sc.seed,
-                 sizes=list(sc.sizes) or None)
+                 sizes=list(sc.sizes) or None, auto_M=sc.auto_M, auto_m=sc.auto_m, auto_alpha=sc.auto_alpha,
+                 auto_rho=sc.auto_rho)
     d.update(kw)
     P = OParams()
     sizes = d.pop("sizes")
@@ -193,7 +197,7 @@ def search(series, pairs, params: OParams, cap: int = 1 << 16):
                              C.cast(out, C.c_void_p), cap, C.byref(count), C.byref(st))
     if rc != 0:
         raise ValueError(f"oracle_search rc={rc}")
-    return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS}
+    return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS + STAT_FIELDS_F}
 
 
 def search_mock(fn, n: int, params: OParams, cap: int = 1 << 14):
@@ -214,7 +218,7 @@ def search_mock(fn, n: int, params: OParams, cap: int = 1 << 14):
                                   C.byref(count), C.byref(st))
     if rc != 0:
         raise ValueError(f"oracle_search_mock rc={rc}")
-    return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS}, calls
+    return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS + STAT_FIELDS_F}, calls
 
 
 def point(x, y, i: int, k: int = 4, variant: int = 0):
@@ -245,3 +249,25 @@ def chunk_plan(n: int, n_p: int, s_max: int):
     out = np.zeros(2 * max(n_p, 1), np.int64)
     c = lib().oracle_chunk_plan(n, n_p, s_max, _p(out), n_p)
     return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(c)]
+
+
+def auto_scores(cost_td: int, cost_bu: int, m: int, nL_td: int, nS_bu: int, alpha: float = 0.5):
+    """Eqs. 6-9 (iSYCOS, Alg. 3): returns (chosen method 1 TD / 2 BU, nscore_TD, nscore_BU)."""
+    L = lib()
+    L.oracle_auto_scores.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_double,
+                                     C.POINTER(C.c_double)]
+    out = (C.c_double * 2)()
+    rc = L.oracle_auto_scores(int(cost_td), int(cost_bu), int(m), int(nL_td), int(nS_bu), float(alpha), out)
+    if rc < 0:
+        raise ValueError("oracle_auto_scores")
+    return rc, out[0], out[1]
+
+
+def auto_sample(M: int, m: int, seed: int, pair_id: int):
+    """Alg. 3 line 1: the m partition indices sampled from M for a pair."""
+    L = lib()
+    L.oracle_auto_sample.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.POINTER(C.c_int32)]
+    out = (C.c_int32 * max(1, m))()
+    if L.oracle_auto_sample(M, m, seed & ((1 << 64) - 1), pair_id, out) != 0:
+        raise ValueError("oracle_auto_sample")
+    return list(out[:m])

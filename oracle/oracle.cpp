@@ -230,13 +230,15 @@ using Provider = std::function<int(int64_t t0, int64_t t1, Eval* out)>;
 extern "C" {
 
 struct OParams {
-    int32_t k, variant, method, noise;     // method: 1 TD, 2 BU, 3 BOTH
+    int32_t k, variant, method, noise;     // method: 1 TD, 2 BU, 3 BOTH, 4 AUTO (iSYCOS, Alg. 3)
     int32_t p, h, t_max_idle, n_chunks;
     int64_t s_min, s_max, delta_td, delta_bu;   // 0 => defaults s/4, s_min/3
     double sigma, tau_ratio;
     uint64_t seed;
     const int64_t* sizes;                  // explicit TD layer sizes or NULL (halving)
     int32_t n_sizes, _pad;
+    int32_t auto_M, auto_m;                // Alg. 3: M partitions, m sampled (0 => 20, 6)
+    double auto_alpha, auto_rho;           // Eqs. 4-9 weight alpha, small/large cut rho (0 => 0.5, 0.5)
 };
 
 struct OResult {
@@ -249,6 +251,9 @@ struct OStats {
     int64_t td_windows, td_noise_checks, td_skips, td_accepted;
     int64_t bu_climbs, bu_iterations, bu_neighbors, bu_noise_checks, bu_prunes, bu_accepted;
     int64_t distinct_windows, distinct_pairs;   // per pair, union over chunks/methods
+    int64_t eval_cost;                     // sum over distinct windows of w * ceil(log2 w) (Alg. 3 runtime proxy)
+    int64_t auto_td, auto_bu;              // AUTO: pairs for which Alg. 3 chose TD / BU
+    double auto_nscore_td, auto_nscore_bu; // AUTO: sums over pairs of nscore_TD, nscore_BU (Eqs. 8-9)
 };
 
 }  // extern "C"
@@ -266,6 +271,13 @@ struct Searcher {
     Searcher(const OParams& p, Provider prov, int32_t id, OStats* s)
         : P(p), provider(std::move(prov)), pair_id(id), st(s) {}
 
+    // Computing the MI of a window costs t_w ~ w log w; a run computes each distinct window once
+    // (this memo); the sum over them is the deterministic runtime proxy of Alg. 3 (reading R24).
+    static int64_t clog2(int64_t w) {
+        int64_t L = 0;
+        while ((int64_t(1) << L) < w) ++L;
+        return L;
+    }
     Eval I(int64_t t0, int64_t t1) {
         auto key = std::make_pair(t0, t1);
         auto it = memo.find(key);
@@ -275,6 +287,7 @@ struct Searcher {
         if (rc != 0 && err == 0) err = rc;
         memo[key] = e;
         st->distinct_windows += 1;
+        st->eval_cost += (t1 - t0) * clog2(t1 - t0);
         st->distinct_pairs += (t1 - t0) * (t1 - t0 - 1);
         return e;
     }
@@ -458,7 +471,89 @@ std::vector<OResult> merge(std::vector<OResult> all) {
 }
 
 int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats* st,
+             std::vector<OResult>& out);
+
+void add_stats(OStats* a, const OStats& b) {
+    a->td_windows += b.td_windows; a->td_noise_checks += b.td_noise_checks; a->td_skips += b.td_skips;
+    a->td_accepted += b.td_accepted; a->bu_climbs += b.bu_climbs; a->bu_iterations += b.bu_iterations;
+    a->bu_neighbors += b.bu_neighbors; a->bu_noise_checks += b.bu_noise_checks; a->bu_prunes += b.bu_prunes;
+    a->bu_accepted += b.bu_accepted; a->distinct_windows += b.distinct_windows;
+    a->distinct_pairs += b.distinct_pairs; a->eval_cost += b.eval_cost;
+}
+
+// Eqs. 6-9: average runtimes t_bar over the m trials, normalized t~ (Eq. 6), n~ (Eq. 7),
+// nscore = alpha / t~ + (1 - alpha) n~ (Eqs. 8-9).  No windows at all: n~ = 0.5 each.
+void auto_scores(int64_t cost_td, int64_t cost_bu, int32_t m, int64_t nL_td, int64_t nS_bu, double alpha,
+                 double* nscore_td, double* nscore_bu) {
+    const double tbar_td = (double)cost_td / (double)m;
+    const double tbar_bu = (double)cost_bu / (double)m;
+    const double tt_td = tbar_td / (tbar_bu + tbar_td);
+    const double tt_bu = tbar_bu / (tbar_bu + tbar_td);
+    double nl = 0.5, ns = 0.5;
+    if (nS_bu + nL_td > 0) {
+        nl = (double)nL_td / (double)(nS_bu + nL_td);
+        ns = (double)nS_bu / (double)(nS_bu + nL_td);
+    }
+    const double beta = 1.0 - alpha;
+    *nscore_td = alpha * (1.0 / tt_td) + beta * nl;
+    *nscore_bu = alpha * (1.0 / tt_bu) + beta * ns;
+}
+
+// iSYCOS (Alg. 3; Eqs. 4-9), with the deterministic readings R24-R26:
+//   random sampling (§5.3.1): M partitions of length floor(N/M); m of them drawn without replacement by a
+//     partial Fisher-Yates shuffle on a SplitMix64 stream keyed by (seed, pair id);
+//   runtime t_TD^i, t_BU^i := eval_cost of SYCOS_TD / SYCOS_BU run alone on partition i (a fresh window
+//     memo per run), the sum of w*ceil(log2 w) over the run's MI requests (t_w ~ O(w log w));
+//   countWindows: |w| <= rho * s_max is small, else large.
+// The trial runs' counters are included in the pair's stats; their windows are not results.
+int run_auto(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats* st, std::vector<OResult>& out) {
+    const int32_t M = P.auto_M > 0 ? P.auto_M : 20;
+    const int32_t m = P.auto_m > 0 ? P.auto_m : 6;
+    const double alpha = P.auto_alpha > 0.0 ? P.auto_alpha : 0.5;
+    const double rho = P.auto_rho > 0.0 ? P.auto_rho : 0.5;
+    const int64_t Lp = n / M;
+    // line 1: randomSampling(M)
+    std::vector<int32_t> idx(M);
+    for (int32_t i = 0; i < M; ++i) idx[i] = i;
+    Searcher::Rng rng{P.seed ^ ((uint64_t)(uint32_t)pair_id * 0x9E3779B97F4A7C15ull) ^ 0xA0761D6478BD642Full};
+    for (int32_t i = 0; i < m; ++i) {
+        const int32_t j = i + (int32_t)((rng.next() >> 32) % (uint64_t)(M - i));
+        std::swap(idx[i], idx[j]);
+    }
+    // lines 2-5: SYCOS_TD and SYCOS_BU on each sampled partition
+    int64_t cost_td = 0, cost_bu = 0, nL_td = 0, nS_bu = 0;
+    for (int32_t i = 0; i < m; ++i) {
+        const int64_t lo = (int64_t)idx[i] * Lp, hi = lo + Lp;
+        for (int meth = 1; meth <= 2; ++meth) {
+            OStats ts{};
+            Searcher S(P, prov, pair_id, &ts);
+            std::vector<OResult> R;
+            if (meth == 1) S.td(lo, hi, R); else S.bu(lo, hi, R);
+            if (S.err) return S.err;
+            add_stats(st, ts);
+            for (auto& r : R) {
+                const bool small = (double)(r.t1 - r.t0) <= rho * (double)P.s_max;
+                if (meth == 1 && !small) nL_td += 1;
+                if (meth == 2 && small) nS_bu += 1;
+            }
+            (meth == 1 ? cost_td : cost_bu) += ts.eval_cost;
+        }
+    }
+    // lines 6-10: Eqs. 6-9
+    double nscore_td, nscore_bu;
+    auto_scores(cost_td, cost_bu, m, nL_td, nS_bu, alpha, &nscore_td, &nscore_bu);
+    st->auto_nscore_td += nscore_td;
+    st->auto_nscore_bu += nscore_bu;
+    // lines 11-15: strict ">" selects TD; ties select BU
+    OParams Q = P;
+    Q.method = nscore_td > nscore_bu ? 1 : 2;
+    (Q.method == 1 ? st->auto_td : st->auto_bu) += 1;
+    return run_pair(Q, prov, pair_id, n, st, out);
+}
+
+int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats* st,
              std::vector<OResult>& out) {
+    if (P.method == 4) return run_auto(P, prov, pair_id, n, st, out);
     Searcher S(P, std::move(prov), pair_id, st);
     auto chunks = chunk_plan(n, P.n_chunks < 1 ? 1 : P.n_chunks, P.s_max);
     for (int m = 1; m <= 2; ++m) {
@@ -482,7 +577,12 @@ bool params_ok(const OParams& P, int64_t n) {
     if (!(P.sigma > 0.0 && P.sigma <= 1.0)) return false;
     if (!(P.tau_ratio >= 0.0 && P.tau_ratio < 1.0)) return false;
     if (P.h < 1 || P.p < 1 || P.t_max_idle < 0) return false;
-    if (P.method < 1 || P.method > 3) return false;
+    if (P.method < 1 || P.method > 4) return false;
+    if (P.method == 4) {
+        const int32_t M = P.auto_M > 0 ? P.auto_M : 20, m = P.auto_m > 0 ? P.auto_m : 6;
+        if (m > M || n / M < P.s_min) return false;
+        if (P.auto_alpha < 0.0 || P.auto_alpha > 1.0 || P.auto_rho < 0.0 || P.auto_rho > 1.0) return false;
+    }
     return true;
 }
 
@@ -662,6 +762,26 @@ int oracle_finish(int64_t s_psi, int64_t s_log, int32_t zeros, int64_t w, int32_
     out3[0] = mi;
     out3[1] = h;
     out3[2] = normalized(mi, h, zeros);
+    return 0;
+}
+
+// Alg. 3 pieces for tests: Eqs. 6-9 on given trial totals; the sampled partition indices of a pair.
+int oracle_auto_scores(int64_t cost_td, int64_t cost_bu, int32_t m, int64_t nL_td, int64_t nS_bu, double alpha,
+                       double* out2) {
+    if (m < 1 || cost_td < 0 || cost_bu < 0 || cost_td + cost_bu == 0 || !out2) return -1;
+    auto_scores(cost_td, cost_bu, m, nL_td, nS_bu, alpha, &out2[0], &out2[1]);
+    return out2[0] > out2[1] ? 1 : 2;
+}
+int oracle_auto_sample(int32_t M, int32_t m, uint64_t seed, int32_t pair_id, int32_t* out) {
+    if (m < 1 || m > M || !out) return -1;
+    std::vector<int32_t> idx(M);
+    for (int32_t i = 0; i < M; ++i) idx[i] = i;
+    Searcher::Rng rng{seed ^ ((uint64_t)(uint32_t)pair_id * 0x9E3779B97F4A7C15ull) ^ 0xA0761D6478BD642Full};
+    for (int32_t i = 0; i < m; ++i) {
+        const int32_t j = i + (int32_t)((rng.next() >> 32) % (uint64_t)(M - i));
+        std::swap(idx[i], idx[j]);
+    }
+    for (int32_t i = 0; i < m; ++i) out[i] = idx[i];
     return 0;
 }
 

@@ -73,7 +73,8 @@ class SearchOpts(C.Structure):
     _fields_ = [("sigma", C.c_double), ("method", C.c_int32), ("variant", C.c_int32),
                 ("delta_td", C.c_int64), ("delta_bu", C.c_int64), ("t_max_idle", C.c_int32),
                 ("h", C.c_int32), ("n_chunks", C.c_int32), ("lookahead", C.c_int32), ("seed", C.c_uint64),
-                ("flags", C.c_uint32), ("stream", C.c_void_p)]
+                ("flags", C.c_uint32), ("stream", C.c_void_p), ("auto_M", C.c_int32), ("auto_m", C.c_int32),
+                ("auto_alpha", C.c_double), ("auto_rho", C.c_double)]
 
 
 class ResultWindow(C.Structure):
@@ -83,14 +84,16 @@ class ResultWindow(C.Structure):
 
 SEARCH_STAT_FIELDS = ["td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs",
                       "bu_iterations", "bu_neighbors", "bu_noise_checks", "bu_prunes", "bu_accepted",
-                      "distinct_windows", "distinct_pairs"]
+                      "distinct_windows", "distinct_pairs", "eval_cost", "auto_td", "auto_bu"]
+SEARCH_STAT_FIELDS_F = ["auto_nscore_td", "auto_nscore_bu"]
 
 
 class SearchStats(C.Structure):
-    _fields_ = [(f, C.c_int64) for f in SEARCH_STAT_FIELDS] + [("kernel", KernelStats)]
+    _fields_ = ([(f, C.c_int64) for f in SEARCH_STAT_FIELDS] + [(f, C.c_double) for f in SEARCH_STAT_FIELDS_F]
+                + [("kernel", KernelStats)])
 
     def as_dict(self):
-        d = {f: getattr(self, f) for f in SEARCH_STAT_FIELDS}
+        d = {f: getattr(self, f) for f in SEARCH_STAT_FIELDS + SEARCH_STAT_FIELDS_F}
         d["kernel"] = self.kernel.as_dict()
         return d
 
@@ -233,7 +236,8 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
                   tau_ratio: float = 0.25, p: int = 3, sigma: float = 0.2, method: int = 3, delta_td: int = 0,
                   delta_bu: int = 0, t_max_idle: int = 3, h: int = 5, n_chunks: int = 1, lookahead: int = 0,
                   seed: int = 0, variant: int = 0, profile: bool = False, brute: bool = False,
-                  unfused: bool = False, stream=None, capacity: int = 1 << 16):
+                  unfused: bool = False, stream=None, capacity: int = 1 << 16, auto_M: int = 0, auto_m: int = 0,
+                  auto_alpha: float = 0.0, auto_rho: float = 0.0):
     """SYCOS search over series pairs.  Returns (results, stats).
 
     series: list of float32 arrays / tensors (host or CUDA, all alike, same length)
@@ -260,6 +264,7 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
     o.sigma, o.method, o.variant = float(sigma), int(method), int(variant)
     o.delta_td, o.delta_bu, o.t_max_idle, o.h = int(delta_td), int(delta_bu), int(t_max_idle), int(h)
     o.n_chunks, o.lookahead, o.seed = int(n_chunks), int(lookahead), int(seed) & ((1 << 64) - 1)
+    o.auto_M, o.auto_m, o.auto_alpha, o.auto_rho = int(auto_M), int(auto_m), float(auto_alpha), float(auto_rho)
     o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
     o.stream = _stream_ptr(stream)
     while True:
@@ -283,7 +288,8 @@ def search_workload(wl, *, series=None, pairs=None, **kw):
     sc = wl.search
     args = dict(s_min=sc.s_min, s_max=sc.s_max, k=sc.k, sizes=list(sc.sizes) or None, noise=sc.noise,
                 tau_ratio=sc.tau_ratio, p=sc.p, sigma=sc.sigma, method=sc.method, delta_td=sc.delta_td,
-                delta_bu=sc.delta_bu, t_max_idle=sc.t_max_idle, h=sc.h, n_chunks=sc.n_chunks, seed=sc.seed)
+                delta_bu=sc.delta_bu, t_max_idle=sc.t_max_idle, h=sc.h, n_chunks=sc.n_chunks, seed=sc.seed,
+                auto_M=sc.auto_M, auto_m=sc.auto_m, auto_alpha=sc.auto_alpha, auto_rho=sc.auto_rho)
     args.update(kw)
     return isycos_search(series if series is not None else wl.series,
                          pairs if pairs is not None else wl.pairs, **args)

@@ -242,6 +242,10 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     P.k = k;
     P.variant = opts->variant;
     P.method = opts->method;
+    P.auto_M = opts->auto_M;
+    P.auto_m = opts->auto_m;
+    P.auto_alpha = opts->auto_alpha;
+    P.auto_rho = opts->auto_rho;
     P.s_min = scales->s_min;
     P.s_max = scales->s_max;
     if (scales->sizes && scales->n_sizes > 0) P.sizes.assign(scales->sizes, scales->sizes + scales->n_sizes);
@@ -273,7 +277,14 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     if (!(P.sigma > 0.0 && P.sigma <= 1.0)) return bad("need 0 < sigma <= 1");
     if (!(P.tau_ratio >= 0.0 && P.tau_ratio < 1.0)) return bad("need 0 <= tau_ratio < 1");
     if (P.h < 1 || P.p < 1 || P.t_max_idle < 0) return bad("need h >= 1, p >= 1, t_max_idle >= 0");
-    if (P.method < 1 || P.method > 3) return bad("method must be 1 (TD), 2 (BU) or 3 (both)");
+    if (P.method < 1 || P.method > 4) return bad("method must be 1 (TD), 2 (BU), 3 (both) or 4 (AUTO)");
+    if (P.method == 4) {
+        const int32_t M = P.auto_M > 0 ? P.auto_M : 20, m = P.auto_m > 0 ? P.auto_m : 6;
+        if (m > M) return bad("AUTO: auto_m must be <= auto_M");
+        if (n / M < P.s_min) return bad("AUTO: partitions floor(n / auto_M) shorter than s_min");
+        if (P.auto_alpha < 0.0 || P.auto_alpha > 1.0 || P.auto_rho < 0.0 || P.auto_rho > 1.0)
+            return bad("AUTO: auto_alpha and auto_rho must be in [0, 1]");
+    }
     if (P.n_chunks < 1) return bad("n_chunks must be >= 1");
     if (P.delta_td < 0 || P.delta_bu < 0) return bad("delta must be >= 0");
     for (size_t i = 0; i < P.sizes.size(); ++i) {

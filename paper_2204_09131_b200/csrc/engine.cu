@@ -121,7 +121,6 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
-    if (const char* m = std::getenv("ISYCOS_SCAN_MODE")) scan_mode_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
@@ -412,7 +411,6 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     L.two = 2;
     L.sorted_ppc = ppc;
     L.fused_n2 = fused_n2;
-    L.scan_mode = scan_mode_;
     L.pad3_ = 0;
     const int32_t* dlists = reinterpret_cast<const int32_t*>(S.dstage + off_lists);
     const KsgItem* ditems = reinterpret_cast<const KsgItem*>(S.dstage + off_items);

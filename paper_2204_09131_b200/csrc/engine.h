@@ -66,7 +66,6 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
     int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
     int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
-    int32_t scan_mode;       // sorted path phase A: 0 two-sided blocks, 1 nearer-side blocks
     int32_t pad3_;
 };
 
@@ -204,7 +203,6 @@ private:
     double* lnc_ = nullptr;
     int64_t psi_max_ = 0;
     int32_t knn_mode_ = 1;
-    int32_t scan_mode_ = 1;
     int* dflag_ = nullptr;
     Slot slots_[2];
     bool sorted_on_ = true;
@@ -230,6 +228,8 @@ struct SearchParams {
     int32_t bu_depth = 4;           // BU: iterations of delta-neighbourhood requested per round
     int32_t trend_depth = 32;       // BU: positions requested along a climb's current direction (head climbs)
     bool pipeline = true;           // two batches in flight (host advance overlaps GPU evaluation)
+    int32_t auto_M = 0, auto_m = 0;  // method 4 (AUTO): Alg. 3 sampling (0 => 20, 6)
+    double auto_alpha = 0.0, auto_rho = 0.0;  // Eqs. 4-9 weights (0 => 0.5, 0.5)
     uint64_t seed = 0;
     uint32_t flags = 0;          // ISYCOS_F_PROFILE | ISYCOS_F_BRUTE
 };

@@ -556,60 +556,6 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
         }
     };
     if (act) start(mloc);
-    if (L.scan_mode == 1) {
-        // Nearer-side variant: each iteration takes one block of B candidates from the side whose next
-        // candidate has the smaller |dx| (a merge of the two runs in |dx| order), so every active lane runs
-        // the same instructions; a side is exhausted once its next |dx| >= r_{k+1}.
-        while (__any_sync(0xffffffffu, act)) {
-            bool fin = false;
-            if (act) {
-                const float r = rk[K1 - 1];
-                const float dl = lj >= 0 ? xi - P2[lj].x : kInf;
-                const float dr = rj < w ? P2[rj].x - xi : kInf;
-                if (!(dl < r) && !(dr < r)) {
-                    fin = true;
-                    eps_s[mloc] = r;
-                } else {
-                    const bool right = dr < dl;
-                    const int base = right ? rj : lj;
-                    const int dir = right ? 1 : -1;
-                    float d[B];
-                    int nv = 0;
-#pragma unroll
-                    for (int u = 0; u < B; ++u) {
-                        const int j = base + dir * u;
-                        if (j >= 0 && j < w) {
-                            const float2 c = P2[j];
-                            const float dx = right ? c.x - xi : xi - c.x;
-                            d[u] = fmaxf(dx, fabsf(yi - c.y));
-                            ++nv;
-                        } else {
-                            d[u] = kInf;
-                        }
-                    }
-                    visit(d);
-                    steps += nv;
-                    if (right)
-                        rj += B;
-                    else
-                        lj -= B;
-                }
-            }
-            const unsigned fm = __ballot_sync(0xffffffffu, fin);
-            if (fm) {
-                if (fin) {
-                    const int idx = next + __popc(fm & lt_mask);
-                    if (idx < we) {
-                        mloc = idx;
-                        start(mloc);
-                    } else {
-                        act = false;
-                    }
-                }
-                next += __popc(fm);
-            }
-        }
-    }
     while (__any_sync(0xffffffffu, act)) {
         bool fin = false;
         if (act) {

@@ -126,10 +126,18 @@ struct PairCache {
     std::vector<uint64_t> pending;
 };
 
+// t_w ~ w log w per MI request: Alg. 3's deterministic runtime proxy (DESIGN reading R24)
+inline int64_t wcost(int64_t w) {
+    int64_t L = 0;
+    while ((int64_t(1) << L) < w) ++L;
+    return w * L;
+}
+
 struct AlgStats {
     int64_t td_windows = 0, td_noise_checks = 0, td_skips = 0, td_accepted = 0;
     int64_t bu_climbs = 0, bu_iterations = 0, bu_neighbors = 0, bu_noise_checks = 0, bu_prunes = 0,
             bu_accepted = 0;
+    int64_t eval_cost = 0;  // sum over the distinct windows consumed of w * ceil(log2 w) (set at retire)
     void add(const AlgStats& o) {
         td_windows += o.td_windows;
         td_noise_checks += o.td_noise_checks;
@@ -141,6 +149,7 @@ struct AlgStats {
         bu_noise_checks += o.bu_noise_checks;
         bu_prunes += o.bu_prunes;
         bu_accepted += o.bu_accepted;
+        eval_cost += o.eval_cost;
     }
 };
 
@@ -691,6 +700,9 @@ std::vector<isycos_result_window> merge_windows(std::vector<isycos_result_window
 
 struct PairWork {
     int32_t inflight = 0;  // batches in flight holding entries of this pair
+    int32_t method = 3;    // 1 TD, 2 BU, 3 both
+    int32_t kind = 0;      // 0: a search whose windows are results; 1: an iSYCOS trial run (Alg. 3 l.3-4)
+    int32_t auto_id = -1;  // trial runs: index of the pair's selection state
     int32_t slot = -1;  // index into the active PairPtrs table
     int32_t pair_id = 0;
     PairPtrs ptrs{};
@@ -719,7 +731,44 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     int64_t distinct_w = 0, distinct_pp = 0;
     std::vector<isycos_result_window> all;
     std::vector<std::unique_ptr<PairWork>> active;
-    int32_t next_pair = 0;
+    // work units: a (pair, method, ranges) search; AUTO (iSYCOS, Alg. 3) pairs first queue 2m trial units
+    // (SYCOS_TD and SYCOS_BU alone on each sampled partition, own window cache each, like the oracle's
+    // fresh Searcher per trial), then, when the last trial retires, the chosen method over the full series
+    struct Unit {
+        int32_t pair_idx, method, kind, auto_id;
+        std::vector<std::pair<int64_t, int64_t>> ranges;
+    };
+    struct AutoState {
+        int32_t pair_idx, left;
+        int64_t cost_td = 0, cost_bu = 0, nL_td = 0, nS_bu = 0;
+        double nscore_td = 0.0, nscore_bu = 0.0;
+        int32_t chosen = 0;
+    };
+    std::deque<Unit> queue;
+    std::vector<AutoState> autos;
+    const int32_t aM = P.auto_M > 0 ? P.auto_M : 20, am = P.auto_m > 0 ? P.auto_m : 6;
+    for (int32_t p = 0; p < n_pairs; ++p) {
+        if (P.method != 4) {
+            queue.push_back(Unit{p, P.method, 0, -1, plan});
+            continue;
+        }
+        // Alg. 3 line 1, randomSampling(M): partial Fisher-Yates on a SplitMix64 stream keyed by (seed, pair)
+        const int64_t Lp = n / aM;
+        std::vector<int32_t> idx(aM);
+        for (int32_t i = 0; i < aM; ++i) idx[i] = i;
+        Rng rng{P.seed ^ ((uint64_t)(uint32_t)pair_ids[p] * 0x9E3779B97F4A7C15ull) ^ 0xA0761D6478BD642Full};
+        for (int32_t i = 0; i < am; ++i) {
+            const int32_t j = i + (int32_t)((rng.next() >> 32) % (uint64_t)(aM - i));
+            std::swap(idx[i], idx[j]);
+        }
+        const int32_t aid = (int32_t)autos.size();
+        autos.push_back(AutoState{p, 2 * am});
+        for (int32_t i = 0; i < am; ++i) {
+            const int64_t lo = (int64_t)idx[i] * Lp;
+            queue.push_back(Unit{p, 1, 1, aid, {{lo, lo + Lp}}});
+            queue.push_back(Unit{p, 2, 1, aid, {{lo, lo + Lp}}});
+        }
+    }
     std::vector<KsgWin> batch;
     std::vector<KsgRec> recs;
     using clk = std::chrono::steady_clock;
@@ -773,19 +822,25 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     };
 
     for (;;) {
-        bool submitted = false;
+        bool progress = false;  // any delivery, admission, retirement or submission this cycle
         for (int g = 0; g < n_groups; ++g) {
-            {
+            if (fl[g].busy) {
                 Status s = deliver(g);
                 if (!s.ok()) return s;
+                progress = true;
             }
             // admit pairs
-            while ((int)active.size() < max_active && next_pair < n_pairs) {
+            while ((int)active.size() < max_active && !queue.empty()) {
+                Unit u = std::move(queue.front());
+                queue.pop_front();
                 auto pw = std::make_unique<PairWork>();
-                pw->pair_id = pair_ids[next_pair];
-                pw->ptrs = pair_ptrs[next_pair];
-                for (auto [lo, hi] : plan) {
-                    if (P.method & 1) {
+                pw->pair_id = pair_ids[u.pair_idx];
+                pw->ptrs = pair_ptrs[u.pair_idx];
+                pw->method = u.method;
+                pw->kind = u.kind;
+                pw->auto_id = u.auto_id;
+                for (auto [lo, hi] : u.ranges) {
+                    if (u.method & 1) {
                         TdJob j;
                         j.P = &P;
                         j.cache = &pw->cache;
@@ -794,7 +849,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                         j.hi = hi;
                         pw->td.push_back(std::move(j));
                     }
-                    if (P.method & 2) {
+                    if (u.method & 2) {
                         BuJob j;
                         j.P = &P;
                         j.cache = &pw->cache;
@@ -813,7 +868,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                     j.init();
                 }
                 active.push_back(std::move(pw));
-                ++next_pair;
+                progress = true;
             }
             // advance this group's jobs
             const auto t_adv = clk::now();
@@ -843,19 +898,55 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                                 per.insert(per.end(), j.results.begin(), j.results.end());
                                 ps.add(j.stats);
                             }
-                        if (!(P.method & m)) continue;
+                        if (!(pw->method & m)) continue;
+                        if (pw->kind == 1) {  // trial run: countWindows, |w| <= rho * s_max is small
+                            AutoState& A = autos[pw->auto_id];
+                            const double rho = P.auto_rho > 0.0 ? P.auto_rho : 0.5;
+                            for (const auto& r : per) {
+                                const bool small = (double)(r.t1 - r.t0) <= rho * (double)P.s_max;
+                                if (m == 1 && !small) A.nL_td += 1;
+                                if (m == 2 && small) A.nS_bu += 1;
+                            }
+                            continue;
+                        }
                         auto merged = merge_windows(per);
                         all.insert(all.end(), merged.begin(), merged.end());
                     }
-                    total.add(ps);
                     pw->cache.map.for_each([&](const Entry& en) {
                         if (en.consumed) {
                             const int64_t w = key_w(en.key);
                             distinct_w += 1;
                             distinct_pp += w * (w - 1);
+                            ps.eval_cost += wcost(w);
                         }
                     });
+
+                    total.add(ps);
+                    if (pw->kind == 1) {
+                        AutoState& A = autos[pw->auto_id];
+                        (pw->method == 1 ? A.cost_td : A.cost_bu) += ps.eval_cost;
+                        if (--A.left == 0) {
+                            // Alg. 3 lines 6-15, Eqs. 6-9 (fixed fp64 op order, as the oracle)
+                            const double alpha = P.auto_alpha > 0.0 ? P.auto_alpha : 0.5;
+                            const double tbar_td = (double)A.cost_td / (double)am;
+                            const double tbar_bu = (double)A.cost_bu / (double)am;
+                            const double tt_td = tbar_td / (tbar_bu + tbar_td);
+                            const double tt_bu = tbar_bu / (tbar_bu + tbar_td);
+                            double nl = 0.5, ns = 0.5;
+                            if (A.nS_bu + A.nL_td > 0) {
+                                nl = (double)A.nL_td / (double)(A.nS_bu + A.nL_td);
+                                ns = (double)A.nS_bu / (double)(A.nS_bu + A.nL_td);
+                            }
+                            const double beta = 1.0 - alpha;
+                            A.nscore_td = alpha * (1.0 / tt_td) + beta * nl;
+                            A.nscore_bu = alpha * (1.0 / tt_bu) + beta * ns;
+                            A.chosen = A.nscore_td > A.nscore_bu ? 1 : 2;
+                            queue.push_front(Unit{A.pair_idx, A.chosen, 0, -1, plan});
+                        }
+                    }
+
                     active.erase(active.begin() + i);
+                    progress = true;
                 } else {
                     ++i;
                 }
@@ -892,7 +983,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             eval_ms += ev_ms;
             if (!s.ok()) return s;
             F.busy = true;
-            submitted = true;
+            progress = true;
             if (trace) {  // per-round trace (ISYCOS_TRACE=<path>): round, host ms since last submit, submit ms, batch
                 int64_t sw2 = 0, wmax = 0;
                 for (const KsgWin& kw : batch) {
@@ -906,13 +997,8 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             ++round_no;
             t_last = clk::now();
         }
-        if (active.empty() && !fl[0].busy && !fl[1].busy) break;
-        if (!submitted && !fl[0].busy && !fl[1].busy) {
-            bool any_active = false;
-            for (auto& pw : active)
-                if (!pw->finished()) any_active = true;
-            if (any_active) return make_err(ISYCOS_E_CUDA, "search driver stalled (internal error)");
-        }
+        if (active.empty() && queue.empty() && !fl[0].busy && !fl[1].busy) break;
+        if (!progress) return make_err(ISYCOS_E_CUDA, "search driver stalled (internal error)");
     }
     if (n_groups == 2) {
         Status s = eng->join_second_stream(st);
@@ -937,6 +1023,14 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         stats->bu_accepted = total.bu_accepted;
         stats->distinct_windows = distinct_w;
         stats->distinct_pairs = distinct_pp;
+        stats->eval_cost = total.eval_cost;
+        stats->auto_td = stats->auto_bu = 0;
+        stats->auto_nscore_td = stats->auto_nscore_bu = 0.0;
+        for (const AutoState& A : autos) {  // pair order (the oracle's summation order)
+            (A.chosen == 1 ? stats->auto_td : stats->auto_bu) += 1;
+            stats->auto_nscore_td += A.nscore_td;
+            stats->auto_nscore_bu += A.nscore_bu;
+        }
         const double wall = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
         bs.wall_ms = wall;
         bs.host_ms = wall - eval_ms;

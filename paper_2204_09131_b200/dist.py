@@ -133,7 +133,12 @@ def search_sharded(series, pairs, *, search=None, device=None, **kw):
     merged.sort(key=lambda r: (r[0], r[1], r[2]))
     stat_names = ["td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs", "bu_iterations",
                   "bu_neighbors", "bu_noise_checks", "bu_prunes", "bu_accepted", "distinct_windows",
-                  "distinct_pairs"]
-    vec = torch.tensor([float(st.get(k, 0)) for k in stat_names], dtype=torch.float64, device=dev)
+                  "distinct_pairs", "eval_cost", "auto_td", "auto_bu"]
+    fstat_names = ["auto_nscore_td", "auto_nscore_bu"]  # sums over pairs (rank order: not bitwise)
+    vec = torch.tensor([int(st.get(k, 0)) for k in stat_names], dtype=torch.int64, device=dev)
+    fvec = torch.tensor([float(st.get(k, 0.0)) for k in fstat_names], dtype=torch.float64, device=dev)
     dist.all_reduce(vec)
-    return merged, {k: int(v) for k, v in zip(stat_names, vec.cpu().tolist())}
+    dist.all_reduce(fvec)
+    out = {k: int(v) for k, v in zip(stat_names, vec.cpu().tolist())}
+    out.update({k: float(v) for k, v in zip(fstat_names, fvec.cpu().tolist())})
+    return merged, out

@@ -143,6 +143,8 @@ struct HarnessParams {
     uint64_t seed;
     const int64_t* sizes;
     int64_t n_sizes;
+    int32_t auto_M, auto_m;
+    double auto_alpha, auto_rho;
 };
 
 // Runs isy::run_search over (xs, ys, id) pairs of host series.  out/stats as in isycos_search.
@@ -170,6 +172,10 @@ int harness_search(const float* const* series, int64_t n, const int32_t* pairs, 
     P.sigma = hp->sigma;
     P.tau_ratio = hp->tau_ratio;
     P.seed = hp->seed;
+    P.auto_M = hp->auto_M;
+    P.auto_m = hp->auto_m;
+    P.auto_alpha = hp->auto_alpha;
+    P.auto_rho = hp->auto_rho;
     if (hp->sizes && hp->n_sizes > 0) P.sizes.assign(hp->sizes, hp->sizes + hp->n_sizes);
     std::vector<isy::PairPtrs> pp(n_pairs);
     std::vector<int32_t> ids(n_pairs);

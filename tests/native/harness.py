@@ -34,7 +34,8 @@ class HarnessParams(C.Structure):
                                          "bu_depth", "anchor", "spec_cap", "trend", "pipeline", "_pad")] + \
                [("s_min", C.c_int64), ("s_max", C.c_int64), ("delta_td", C.c_int64), ("delta_bu", C.c_int64),
                 ("sigma", C.c_double), ("tau_ratio", C.c_double), ("seed", C.c_uint64),
-                ("sizes", C.POINTER(C.c_int64)), ("n_sizes", C.c_int64)]
+                ("sizes", C.POINTER(C.c_int64)), ("n_sizes", C.c_int64), ("auto_M", C.c_int32), ("auto_m", C.c_int32),
+                ("auto_alpha", C.c_double), ("auto_rho", C.c_double)]
 
 
 _lib = None
@@ -67,7 +68,8 @@ def search(series, pairs, sc, **kw):
     hp = HarnessParams()
     d = dict(k=sc.k, method=sc.method, noise=int(sc.noise), p=sc.p, h=sc.h, t_max_idle=sc.t_max_idle,
              n_chunks=sc.n_chunks, lookahead=0, bu_depth=0, anchor=-1, spec_cap=-1, trend=-1, pipeline=-1, s_min=sc.s_min, s_max=sc.s_max,
-             delta_td=sc.delta_td, delta_bu=sc.delta_bu, sigma=sc.sigma, tau_ratio=sc.tau_ratio, seed=sc.seed)
+             delta_td=sc.delta_td, delta_bu=sc.delta_bu, sigma=sc.sigma, tau_ratio=sc.tau_ratio, seed=sc.seed,
+             auto_M=sc.auto_M, auto_m=sc.auto_m, auto_alpha=sc.auto_alpha, auto_rho=sc.auto_rho)
     d.update(kw)
     for key, v in d.items():
         setattr(hp, key, v)

@@ -55,7 +55,7 @@ def test_kernels_use_bulk_copy(capi):
 
 
 def test_abi_version(capi):
-    assert capi.isycos_abi_version() == 1
+    assert capi.isycos_abi_version() == 2
 
 
 def test_validation_before_gpu(capi):

@@ -67,3 +67,19 @@ def test_multi_pair_instance(hz, orc):
     wl = datagen.cfg4(n=8000, n_series=4, n_planted=1)
     pairs = [(a, b, 40 + i) for i, (a, b) in enumerate(wl.pairs)]
     check(hz, orc, wl, pairs=pairs, label="cfg4 instance", s_max=1024)
+
+
+@pytest.mark.parametrize("kw", [dict(auto_M=4, auto_m=2), dict(auto_M=8, auto_m=8, auto_alpha=0.2, auto_rho=0.3),
+                                dict(auto_M=16, auto_m=3, noise=False, seed=9)])
+def test_auto_selection_driver_equals_oracle(hz, orc, kw):
+    """iSYCOS (Alg. 3): trial runs on sampled partitions, Eqs. 6-9, then the chosen method; results, all
+    counters (incl. eval_cost) and the nscore sums bit-exact."""
+    res, st = check(hz, orc, datagen.cfg1(), method=4, label=f"auto {kw}", **kw)
+    assert st["auto_td"] + st["auto_bu"] == 1
+
+
+def test_auto_selection_multi_pair(hz, orc):
+    wl = datagen.cfg4(n=8000, n_series=4, n_planted=1)
+    pairs = [(a, b, 40 + i) for i, (a, b) in enumerate(wl.pairs)]
+    res, st = check(hz, orc, wl, pairs=pairs, label="cfg4 auto", s_max=1024, method=4, auto_M=5, auto_m=2)
+    assert st["auto_td"] + st["auto_bu"] == len(pairs)

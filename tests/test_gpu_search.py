@@ -112,3 +112,29 @@ def test_cfg1_search_ksg2(isy, orc, method):
     wl = datagen.cfg1()
     ores, ost, gres, gst = run_both(isy, orc, wl, method=method, variant=1)
     assert_same(ores, ost, gres, gst, f"cfg1 ksg2 m={method}")
+
+
+@pytest.mark.parametrize("kw", [dict(auto_M=4, auto_m=2), dict(auto_M=8, auto_m=8, auto_alpha=0.2, auto_rho=0.3)])
+def test_cfg1_auto_selection(isy, orc, kw):
+    """iSYCOS (Alg. 3): sampled trial runs, Eqs. 6-9, then the chosen method — results, counters (incl.
+    eval_cost, the runtime proxy) and the nscore sums bit-exact against the oracle."""
+    wl = datagen.cfg1()
+    ores, ost, gres, gst = run_both(isy, orc, wl, method=4, **kw)
+    assert_same(ores, ost, gres, gst, f"cfg1 auto {kw}")
+    assert gst["auto_td"] + gst["auto_bu"] == 1
+
+
+@pytest.mark.parametrize("kind", ["dense", "sparse"])
+def test_scenario_auto_selection(isy, orc, kind):
+    wl = datagen.scenario(kind, seed=0)
+    ores, ost, gres, gst = run_both(isy, orc, wl)
+    assert_same(ores, ost, gres, gst, f"scenario {kind}")
+    assert (gst["auto_td"], gst["auto_bu"]) == ((1, 0) if kind == "dense" else (0, 1))
+
+
+def test_multi_pair_auto_selection(isy, orc):
+    wl = datagen.cfg4(n=8000, n_series=4, n_planted=1)
+    pairs = [(a, b, 40 + i) for i, (a, b) in enumerate(wl.pairs)]
+    ores, ost, gres, gst = run_both(isy, orc, wl, pairs=pairs, s_max=1024, method=4, auto_M=5, auto_m=2)
+    assert_same(ores, ost, gres, gst, "cfg4 auto")
+    assert gst["auto_td"] + gst["auto_bu"] == len(pairs)

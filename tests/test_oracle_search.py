@@ -219,3 +219,80 @@ def test_cfg1_search_invariants_and_recovery(orc, noise):
         # planted recovery: union coverage >= 0.8 per planted block (S:331 form)
         for (a, b, _) in wl.planted[0]:
             assert _coverage(rs, (a, b)) >= 0.8, (method, a, b, rs)
+
+
+# ------------------------------------------------------------------ iSYCOS selection (Alg. 3, Eqs. 4-9)
+def test_auto_scores_worked_example(orc):
+    # SPEC S:455-457 (Eqs. 6-8 arithmetic): equal runtimes -> t~ = 0.5 each; alpha = 0.5, n~L_TD = 3/5 = 0.6
+    # -> nscore_TD = 0.5 * (1/0.5) + 0.5 * 0.6 = 1.3, nscore_BU = 0.5 * 2 + 0.5 * 0.4 = 1.2 -> TD.
+    chosen, td, bu = orc.auto_scores(1000, 1000, 6, 3, 2, 0.5)
+    assert chosen == 1
+    assert td == pytest.approx(1.3, abs=1e-15) and bu == pytest.approx(1.2, abs=1e-15)
+    # Eq. 6 symmetry: equal runtimes give equal runtime terms (alpha * 2)
+    c2, td2, bu2 = orc.auto_scores(777, 777, 3, 0, 0, 0.3)
+    assert td2 == bu2 == pytest.approx(0.3 * 2 + 0.7 * 0.5, abs=1e-15)
+
+
+def test_auto_scores_rules(orc):
+    # ties select BU (Alg. 3 line 11 is a strict ">")
+    assert orc.auto_scores(500, 500, 6, 4, 4)[0] == 2
+    # no windows at all: n~ = 0.5 each, the runtime alone decides
+    c, td, bu = orc.auto_scores(100, 300, 6, 0, 0, 0.5)
+    assert c == 1 and td == pytest.approx(0.5 * 4 + 0.25) and bu == pytest.approx(0.5 / 0.75 + 0.25)
+    # monotonicity: decreasing t_TD strictly increases nscore_TD, windows fixed
+    prev = -1.0
+    for cost_td in (5000, 2000, 1000, 500, 100):
+        _, td, _ = orc.auto_scores(cost_td, 1000, 6, 3, 5, 0.5)
+        assert td > prev
+        prev = td
+    # alpha-robustness on extremes: TD faster AND more large windows -> TD for alpha in 0.2..0.8
+    for a in (0.2, 0.4, 0.5, 0.6, 0.8):
+        assert orc.auto_scores(100, 900, 6, 9, 1, a)[0] == 1
+        assert orc.auto_scores(900, 100, 6, 1, 9, a)[0] == 2
+
+
+def test_auto_sampling(orc):
+    # m = M -> every partition exactly once; fixed seed reproduces; m of M distinct
+    assert sorted(orc.auto_sample(20, 20, 123, 7)) == list(range(20))
+    assert orc.auto_sample(20, 6, 5, 3) == orc.auto_sample(20, 6, 5, 3)
+    s = orc.auto_sample(10, 4, 0, 0)
+    assert len(set(s)) == 4 and all(0 <= i < 10 for i in s)
+    # streams are keyed by (seed, pair): different pairs draw different samples (w.h.p.)
+    assert len({tuple(orc.auto_sample(50, 5, 1, p)) for p in range(8)}) == 8
+
+
+def test_auto_runs_the_chosen_method(orc):
+    """AUTO's windows are those of the chosen method run alone on the whole series; its counters are the
+    trial runs' plus that run's; TD trial counters equal TD run on the sampled partitions alone."""
+    wl = datagen.cfg1()
+    x, y = wl.series
+    M, m = 4, 2
+    pa = orc.make_params(wl.search, method=4, auto_M=M, auto_m=m)
+    res, st = orc.search(wl.series, wl.pairs, pa)
+    chosen = 1 if st["auto_td"] == 1 else 2
+    assert st["auto_td"] + st["auto_bu"] == 1
+    ref, rst = orc.search(wl.series, wl.pairs, orc.make_params(wl.search, method=chosen))
+    assert res == ref
+    # TD on each sampled partition alone (TD has no random stream: position-shift invariant counters)
+    L = len(x) // M
+    td = dict(td_windows=0, td_noise_checks=0, td_skips=0, td_accepted=0)
+    for i in orc.auto_sample(M, m, wl.search.seed, 0):
+        _, s = orc.search([x[i * L:(i + 1) * L], y[i * L:(i + 1) * L]], [(0, 1)],
+                          orc.make_params(wl.search, method=1))
+        for f in td:
+            td[f] += s[f]
+    for f in td:
+        assert st[f] == td[f] + (rst[f] if chosen == 1 else 0), f
+
+
+def test_auto_scenarios(orc):
+    """Fig. 1 scenarios: long dense correlated stretches favour SYCOS_TD (cheap large accepts,
+    many large windows); short sparse relations favour SYCOS_BU (many small windows)."""
+    chosen = {"dense": [], "sparse": []}
+    for seed in range(4):
+        for kind in ("dense", "sparse"):
+            wl = datagen.scenario(kind, seed=seed)
+            _, st = orc.search(wl.series, wl.pairs, orc.make_params(wl.search))
+            chosen[kind].append(1 if st["auto_td"] else 2)
+    assert chosen["dense"].count(1) >= 3, chosen
+    assert chosen["sparse"].count(2) >= 3, chosen
