@@ -121,6 +121,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
@@ -259,6 +260,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     std::vector<int32_t> sorted;
     std::vector<int64_t> soff;
     std::vector<int32_t> fused;  // sorted path, fused sort+scan kernel (w <= kFusedMaxW)
+    std::vector<int32_t> wsorted[3];  // sorted path, warp per window, E = 2, 4, 8
     int fused_n2 = 256;
     int64_t n_items = 0, n_sitems = 0, spts = 0, n_segs = 0, n_mblocks = 0;
     int W2 = 0;
@@ -276,7 +278,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         const int w = wins[i].w;
         pp += (int64_t)w * (w - 1);
         const int R = small_class_R(w);
-        if (R && !(use_sorted && w >= sorted_min_w_)) {
+        if (R >= 2 && use_sorted && w >= wsorted_min_w_) {
+            wsorted[R == 2 ? 0 : R == 4 ? 1 : 2].push_back((int32_t)i);
+        } else if (R && !(use_sorted && w >= sorted_min_w_)) {
             small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
         } else if (fuse && w >= sorted_min_w_ && w <= kFusedMaxW) {
             fused.push_back((int32_t)i);
@@ -317,6 +321,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     }
     int64_t n_lists = (int64_t)sorted.size() + (int64_t)fused.size();
     for (auto& v : small) n_lists += (int64_t)v.size();
+    int64_t n_wlist = 0;
+    for (auto& v : wsorted) n_wlist += (int64_t)v.size();
+    n_lists += n_wlist;
     {
         Status s = ensure_capacity(S, n + 1, n_items + n_sitems + n_segs + n_mblocks + n_fitems, n_pairs,
                                    n_lists + 2 * (int64_t)sorted.size() + 16);
@@ -334,7 +341,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const int64_t off_pairs = 0;
     const int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
     const int64_t off_lists = align64(off_wins + n * (int64_t)sizeof(KsgWin));
-    const int64_t off_flist = align64(off_lists + (n_lists - (int64_t)sorted.size() - (int64_t)fused.size()) * 4);
+    const int64_t off_wlist = align64(off_lists + (n_lists - n_wlist - (int64_t)sorted.size() - (int64_t)fused.size()) * 4);
+    const int64_t off_flist = align64(off_wlist + n_wlist * 4);
     const int64_t off_fitems = align64(off_flist + (int64_t)fused.size() * 4);
     const int64_t off_slist = align64(off_fitems + n_fitems * (int64_t)sizeof(KsgItem));
     const int64_t off_soff = align64(off_slist + (int64_t)sorted.size() * 4);
@@ -345,7 +353,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const int64_t total = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
     std::memcpy(S.hstage + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
     std::memcpy(S.hstage + off_wins, wins, n * sizeof(KsgWin));
-    int64_t list_off[4];
+    int64_t list_off[4], wlist_off[3];
     {
         int32_t* lp = reinterpret_cast<int32_t*>(S.hstage + off_lists);
         int64_t c = 0;
@@ -353,6 +361,13 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             list_off[s] = c;
             std::memcpy(lp + c, small[s].data(), small[s].size() * 4);
             c += (int64_t)small[s].size();
+        }
+        int32_t* wl = reinterpret_cast<int32_t*>(S.hstage + off_wlist);
+        int64_t cw = 0;
+        for (int e = 0; e < 3; ++e) {
+            wlist_off[e] = cw;
+            std::memcpy(wl + cw, wsorted[e].data(), wsorted[e].size() * 4);
+            cw += (int64_t)wsorted[e].size();
         }
         std::memcpy(S.hstage + off_flist, fused.data(), fused.size() * 4);
         KsgItem* fp = reinterpret_cast<KsgItem*>(S.hstage + off_fitems);
@@ -429,6 +444,12 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         while ((1 << lg) < wins[q].w) ++lg;
         probes += (int64_t)wins[q].w * 5 * lg;
     }
+    for (auto& v : wsorted)
+        for (int32_t q : v) {
+            int lg = 0;
+            while ((1 << lg) < wins[q].w) ++lg;
+            probes += (int64_t)wins[q].w * 5 * lg;
+        }
     for (int32_t q : sorted) {
         int lg = 0;
         while ((1 << lg) < wins[q].w) ++lg;
@@ -475,6 +496,14 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         const KsgItem* dfi = reinterpret_cast<const KsgItem*>(S.dstage + off_fitems);
         launch_cls.push_back(0);
         Status r = launch(1, [&](cudaStream_t sg) { return launch_fused(L, dfl, dfi, (int32_t)n_fitems, gmax, sg); });
+        if (!r.ok()) return r;
+    }
+    for (int e = 2; e >= 0; --e) {
+        if (wsorted[e].empty()) continue;
+        const int32_t* wlp = reinterpret_cast<const int32_t*>(S.dstage + off_wlist) + wlist_off[e];
+        const int32_t cnt = (int32_t)wsorted[e].size();
+        launch_cls.push_back(0);
+        Status r = launch(1, [&](cudaStream_t sg) { return launch_wsorted(L, wlp, cnt, 2 << e, sg); });
         if (!r.ok()) return r;
     }
     if (!sorted.empty()) {
@@ -531,7 +560,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.n_launch = n_launch;
     S.brute_pairs = brute_pairs;
     S.probes = probes;
-    S.sorted_windows = (int64_t)sorted.size() + (int64_t)fused.size();
+    S.sorted_windows = (int64_t)sorted.size() + (int64_t)fused.size() + n_wlist;
+    for (auto& v : wsorted)
+        for (int32_t q : v) spts += wins[q].w;
     S.spts = spts;
     return Status{};
 }

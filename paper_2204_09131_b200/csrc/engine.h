@@ -90,6 +90,8 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
                           int32_t n_items, cudaStream_t st);
+// small windows on the sorted path: one warp per window, E = 2, 4, 8 keys per lane (w <= 32 E)
+cudaError_t launch_wsorted(const KsgLaunch& L, const int32_t* list, int32_t n, int E, cudaStream_t st);
 // fused latency path: items {list pos, slice start}; slices of fused_ppc(w, gmax) points
 cudaError_t launch_fused(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
                          cudaStream_t st);
@@ -209,6 +211,7 @@ private:
     bool fused_on_ = true;           // sorted windows w <= kFusedMaxW: fused sort+scan kernel ...
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
     int32_t sorted_min_w_ = 257;
+    int32_t wsorted_min_w_ = 65;     // small windows w in [this, 256]: warp-per-window sorted kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
 };
 

@@ -504,28 +504,52 @@ __device__ inline void ksg2_sorted_radii(const float2* __restrict__ P2, const fl
     *ey = nextup(my);
 }
 
-// Scan of one CTA's slice [cta0, cta0 + cta_n) of a window's x-sorted points (arrays in global or shared
-// memory, generic pointers): P2[m] = (x, y) of the m-th point in x order, OX[m] its window index, YS the
-// sorted y.  Each warp owns a contiguous part of the slice.  Phase A (k-NN scan) runs a warp-local work
-// queue: a lane that finishes its point takes the next one (ballot + popc), so warps do not idle on their
-// slowest lane (per-point scan lengths vary several-fold with the local density ratio f_x/f_y).  Phase B
-// (binary-search counts, digamma/log terms) is uniform per point.  Ends with the CTA reduction.
-template <int K1, bool V2>
-__device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, int ntiles, const float2* P2,
-                                            const int32_t* OX, const float* YS, int cta0, int cta_n, float* eps_s) {
-    const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
-    const int nwarps = blockDim.x >> 5;
-    const int kPerWarp = (cta_n + nwarps - 1) / nwarps;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wb = min(warp * kPerWarp, cta_n);
-    const int we = min(wb + kPerWarp, cta_n);
-    const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned long long steps = 0;
+// Warp-level bitonic sort of 32*E keys held E per lane (blocked: lane l holds keys [E l, E l + E)),
+// ascending.  Exchange distances j < E stay in registers; j >= E swap with lane l ^ (j / E) by shuffle.
+template <typename T, int E>
+__device__ __forceinline__ void warp_sort(T (&v)[E], int lane) {
+    constexpr int LE = E == 1 ? 0 : E == 2 ? 1 : E == 4 ? 2 : 3;  // log2(E)
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+                const int lm = j >> LE;
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const bool up = ((((unsigned)lane << LE) | (unsigned)e) & (unsigned)k) == 0;
+                    const T pv = __shfl_xor_sync(0xffffffffu, v[e], lm);
+                    const T mn = pv < v[e] ? pv : v[e];
+                    const T mx = pv < v[e] ? v[e] : pv;
+                    v[e] = (lower == up) ? mn : mx;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & j) == 0) {
+                        const bool up = ((((unsigned)lane << LE) | (unsigned)e) & (unsigned)k) == 0;
+                        const T a = v[e], c = v[e | j];
+                        const bool sw = up ? (c < a) : (a < c);
+                        v[e] = sw ? c : a;
+                        v[e | j] = sw ? a : c;
+                    }
+                }
+            }
+        }
+    }
+}
 
-    // ---- phase A: exact k-NN radius by outward scan in x order (a3)
-    // Blocked scan: each iteration visits the next 4 candidates on each side (independent loads).  A side
-    // stops once the farthest candidate it visited has |dx| >= r_{k+1}: every unvisited candidate beyond
-    // it has a larger |dx| (x-sorted, fl monotone), hence d_ij >= r_{k+1}, and cannot change eps.
+
+// Phase A of the sorted path for the points [wb, we) (positions relative to cta0) of one warp: exact
+// k-NN radius by outward scan in x order (a3).  Writes eps_s[ml]; adds the candidate visits to `steps`.
+// Warp-local work queue: a lane that finishes its point takes the next one (ballot + popc), so warps do
+// not idle on their slowest lane (per-point scan lengths vary several-fold with the local density ratio).
+template <int K1>
+__device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0, int wb, int we, float* eps_s,
+                                               unsigned long long& steps) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
     constexpr int B = 4;
     int mloc = wb + lane;
     bool act = mloc < we;
@@ -616,52 +640,72 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
             next += __popc(fm);
         }
     }
-    __syncthreads();
+}
 
-    // ---- phase B: interval counts by binary search with the identical predicates (a4) and terms (a5)
+// Phase B for one point at sorted position m (a4, a5): interval counts by binary search with the
+// identical predicates, digamma / log terms, debug outputs.
+template <bool V2>
+__device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_t dbg, const float2* P2,
+                                               const int32_t* OX, const float* YS, int m, float eps, long long& sp,
+                                               long long& sl, int& z) {
+    const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
+    const float2 me = P2[m];
+    const float xv = me.x, yv = me.y;
+    int nx = 0, ny = 0;
+    float ex = eps, ey = eps;
+    if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
+    if (V2 || eps > 0.0f) {
+        // x: left part [0, m] uses fl(x_i - x_j) < ex, right part [m, w) uses fl(x_j - x_i) < ex
+        int lo = 0, hi = m;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (xv - XS[2 * mid] < ex) hi = mid; else lo = mid + 1;
+        }
+        const int Lx = lo;
+        lo = m;
+        hi = w;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
+        }
+        nx = lo - Lx - 1;
+        const int p = lower_bound_f(YS, w, yv);
+        const int Ly = left_bound_f(YS, p, yv, ey);
+        const int Ry = right_bound(YS, p, w, yv, ey);
+        ny = Ry - Ly - 1;
+    }
+    sp += V2 ? L.psiq[nx] + L.psiq[ny] : L.psiq[nx + 1] + L.psiq[ny + 1];
+    if (eps > 0.0f)
+        sl += q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
+    else
+        z += 1;
+    if (dbg >= 0) {
+        const int i = OX[m];
+        if (L.dbg_eps) L.dbg_eps[dbg + i] = eps;
+        if (L.dbg_nx) L.dbg_nx[dbg + i] = nx;
+        if (L.dbg_ny) L.dbg_ny[dbg + i] = ny;
+    }
+}
+
+// Scan of one CTA's slice [cta0, cta0 + cta_n) of a window's x-sorted points (arrays in global or shared
+// memory, generic pointers): P2[m] = (x, y) of the m-th point in x order, OX[m] its window index, YS the
+// sorted y.  Each warp owns a contiguous part of the slice.  Ends with the CTA reduction.
+template <int K1, bool V2>
+__device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, int ntiles, const float2* P2,
+                                            const int32_t* OX, const float* YS, int cta0, int cta_n, float* eps_s) {
+    const int nwarps = blockDim.x >> 5;
+    const int kPerWarp = (cta_n + nwarps - 1) / nwarps;
+    const int warp = threadIdx.x >> 5;
+    const int wb = min(warp * kPerWarp, cta_n);
+    const int we = min(wb + kPerWarp, cta_n);
+    unsigned long long steps = 0;
+    sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps);
+    __syncthreads();
     long long sp = 0, sl = 0;
     int z = 0;
     const int64_t dbg = L.wins[q].dbg_off;
-    for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x) {
-        const int m = cta0 + ml;
-        const float2 me = P2[m];
-        const float xv = me.x, yv = me.y;
-        const float eps = eps_s[ml];
-        int nx = 0, ny = 0;
-        float ex = eps, ey = eps;
-        if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
-        if (V2 || eps > 0.0f) {
-            // x: left part [0, m] uses fl(x_i - x_j) < ex, right part [m, w) uses fl(x_j - x_i) < ex
-            int lo = 0, hi = m;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (xv - XS[2 * mid] < ex) hi = mid; else lo = mid + 1;
-            }
-            const int Lx = lo;
-            lo = m;
-            hi = w;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
-            }
-            nx = lo - Lx - 1;
-            const int p = lower_bound_f(YS, w, yv);
-            const int Ly = left_bound_f(YS, p, yv, ey);
-            const int Ry = right_bound(YS, p, w, yv, ey);
-            ny = Ry - Ly - 1;
-        }
-        sp += V2 ? L.psiq[nx] + L.psiq[ny] : L.psiq[nx + 1] + L.psiq[ny + 1];
-        if (eps > 0.0f)
-            sl += q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
-        else
-            z += 1;
-        if (dbg >= 0) {
-            const int i = OX[m];
-            if (L.dbg_eps) L.dbg_eps[dbg + i] = eps;
-            if (L.dbg_nx) L.dbg_nx[dbg + i] = nx;
-            if (L.dbg_ny) L.dbg_ny[dbg + i] = ny;
-        }
-    }
+    for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x)
+        sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z);
     cta_finish(L, q, w, ntiles, sp, sl, z, steps);
 }
 

@@ -12,39 +12,6 @@ namespace {
 // memory double the run length up to n2 (next power of two >= w).  x keys carry the window index in
 // the low 32 bits (sortable x bits << 32 | index: unique keys, ties of x broken by index); y keys are
 // the sortable y bits alone.
-template <typename T>
-__device__ __forceinline__ void warp_sort256(T (&v)[8], int lane) {
-#pragma unroll
-    for (int k = 2; k <= 256; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 8) {
-                const int lm = j >> 3;
-                const bool lower = (lane & lm) == 0;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const bool up = ((((unsigned)lane << 3) | (unsigned)e) & (unsigned)k) == 0;
-                    const T pv = __shfl_xor_sync(0xffffffffu, v[e], lm);
-                    const T mn = pv < v[e] ? pv : v[e];
-                    const T mx = pv < v[e] ? v[e] : pv;
-                    v[e] = (lower == up) ? mn : mx;
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if ((e & j) == 0) {
-                        const bool up = ((((unsigned)lane << 3) | (unsigned)e) & (unsigned)k) == 0;
-                        const T a = v[e], c = v[e | j];
-                        const bool sw = up ? (c < a) : (a < c);
-                        v[e] = sw ? c : a;
-                        v[e | j] = sw ? a : c;
-                    }
-                }
-            }
-        }
-    }
-}
-
 // merge adjacent sorted runs of length r (src) into runs of 2r (dst); thread t < n2/8 writes outputs
 // [8t, 8t+8).  Merge path: the co-rank i (outputs taken from run A) is found by binary search, A first
 // on ties.
@@ -113,8 +80,8 @@ __global__ void __launch_bounds__(kFusedThreads)
             vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
             vy[e] = i < w ? sortable(gy[i]) : ~0u;
         }
-        warp_sort256(vx, lane);
-        warp_sort256(vy, lane);
+        warp_sort<unsigned long long, 8>(vx, lane);
+        warp_sort<unsigned, 8>(vy, lane);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             X0[c * 256 + lane * 8 + e] = vx[e];

@@ -82,8 +82,10 @@ SIZES = [5, 17, 32, 33, 64, 65, 100, 128, 129, 255, 256, 257, 300, 512, 513, 777
 
 
 @pytest.mark.parametrize("k", [1, 3, 4, 8, 16])
-@pytest.mark.parametrize("unfused", [False, True])
-def test_size_classes_random_windows(isy, orc, k, unfused):
+@pytest.mark.parametrize("path", ["default", "unfused", "brute"])
+def test_size_classes_random_windows(isy, orc, k, path):
+    """Every kernel family: warp brute force (w <= 64), warp-sorted (65..256), fused / throughput sorted
+    (257..4096; 'unfused' forces the throughput form), XL runs + merge; 'brute' forces the brute force."""
     wl = datagen.cfg2(n=20_000)
     x, y = wl.series
     rng = np.random.default_rng(k)
@@ -96,7 +98,8 @@ def test_size_classes_random_windows(isy, orc, k, unfused):
     n = len(x)
     W += [(0, 37), (n - 41, n), (n - 4100, n), (1, 1 + 4099), (2, 2 + 515), (3, 3 + 130)]
     W = [(a, b) for (a, b) in W if b - a > k]
-    check_windows(isy, orc, x, y, W, k, debug=(k == 4), label=f"k={k} unfused={unfused}", unfused=unfused)
+    check_windows(isy, orc, x, y, W, k, debug=(k == 4), label=f"k={k} {path}", unfused=path == "unfused",
+                  brute=path == "brute")
 
 
 def test_tie_torture(isy, orc):
