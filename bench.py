@@ -121,11 +121,12 @@ def make_workload(name: str):
 
 
 def traffic_for(path):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture summary
-    (profiles/traffic.json, written by scripts/ncu_summary.py); None when absent."""
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/traffic.json, written by `scripts/ncu_summary.py traffic`); None when absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(path)
+            t = json.load(f).get(path)
+        return t["bytes_per_launch"] if isinstance(t, dict) else t
     except Exception:
         return None
 

@@ -287,8 +287,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             while (fused_n2 < w) fused_n2 <<= 1;
         } else if (use_sorted && w >= sorted_min_w_) {
             sorted.push_back((int32_t)i);
-            soff.push_back(spts);
-            spts += w;
+            soff.push_back(spts + 4);  // 4 sentinel entries on either side of the window's region
+            spts += w + 8;
             n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
             if (w > kSortedMaxW) n_mblocks += (w + kMergePts - 1) / kMergePts;
             int n2 = 1;
@@ -300,14 +300,20 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             n_items += (w + kTileThreads * tr - 1) / (kTileThreads * tr);
         }
     }
-    for (int s = 0; s < 4; ++s) {
-        if (small[s].empty() || (int64_t)small[s].size() >= lat_windows_) continue;
-        for (int32_t q : small[s]) {
+    // latency mode: a class too sparse to fill the GPU runs a CTA per window (tile R = 1), where a warp
+    // walking 32R points (brute force) or sorting and scanning them (warp-sorted) would set the latency
+    // (all of a round's latency-mode windows go into one launch: per-class launches measured slower)
+    auto to_latency = [&](std::vector<int32_t>& v) {
+        for (int32_t q : v) {
             tile[2].push_back(q);
             n_items += (wins[q].w + kTileThreads - 1) / kTileThreads;
         }
-        small[s].clear();
-    }
+        v.clear();
+    };
+    for (int s = 0; s < 4; ++s)
+        if (!small[s].empty() && (int64_t)small[s].size() < lat_windows_) to_latency(small[s]);
+    for (int e = 0; e < 3; ++e)
+        if (!wsorted[e].empty() && (int64_t)wsorted[e].size() < lat_windows_) to_latency(wsorted[e]);
     // sorted scan: 1024 points per CTA when the batch fills the GPU (better lane balance in the per-warp
     // work queues), else 256 (more CTAs per window: latency-bound rounds)
     const int ppc = spts >= (int64_t)148 * 8 * 1024 ? 1024 : 256;
@@ -324,6 +330,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     int64_t n_wlist = 0;
     for (auto& v : wsorted) n_wlist += (int64_t)v.size();
     n_lists += n_wlist;
+
     {
         Status s = ensure_capacity(S, n + 1, n_items + n_sitems + n_segs + n_mblocks + n_fitems, n_pairs,
                                    n_lists + 2 * (int64_t)sorted.size() + 16);
@@ -341,7 +348,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const int64_t off_pairs = 0;
     const int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
     const int64_t off_lists = align64(off_wins + n * (int64_t)sizeof(KsgWin));
-    const int64_t off_wlist = align64(off_lists + (n_lists - n_wlist - (int64_t)sorted.size() - (int64_t)fused.size()) * 4);
+    const int64_t off_wlist = align64(off_lists + (n_lists - n_wlist - (int64_t)sorted.size() -
+                                                   (int64_t)fused.size()) * 4);
     const int64_t off_flist = align64(off_wlist + n_wlist * 4);
     const int64_t off_fitems = align64(off_flist + (int64_t)fused.size() * 4);
     const int64_t off_slist = align64(off_fitems + n_fitems * (int64_t)sizeof(KsgItem));
@@ -437,6 +445,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     int64_t brute_pairs = 0, probes = 0;
     for (int s = 0; s < 4; ++s)
         for (int32_t q : small[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
+
     for (int s = 0; s < 3; ++s)
         for (int32_t q : tile[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
     for (int32_t q : fused) {
@@ -549,7 +558,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         ISY_CK(cudaStreamWaitEvent(st, S.join_ev[a], 0));
     }
     if (!zc) ISY_CK(cudaMemcpyAsync(S.hrec, S.ddrec, n * sizeof(KsgRec), cudaMemcpyDeviceToHost, st));
-    for (int32_t q : fused) spts += wins[q].w;
+    int64_t spoints = 0;  // real points on the sorted path (spts includes the sentinel padding)
+    for (int32_t q : sorted) spoints += wins[q].w;
+    for (int32_t q : fused) spoints += wins[q].w;
     S.busy = true;
     S.st = st;
     S.n = n;
@@ -562,8 +573,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.probes = probes;
     S.sorted_windows = (int64_t)sorted.size() + (int64_t)fused.size() + n_wlist;
     for (auto& v : wsorted)
-        for (int32_t q : v) spts += wins[q].w;
-    S.spts = spts;
+        for (int32_t q : v) spoints += wins[q].w;
+    S.spts = spoints;
     return Status{};
 }
 

@@ -119,5 +119,30 @@ def launches(path, dst):
     open(dst, "w").write("\n".join(lines) + "\n")
 
 
+def traffic(path, key, dst="profiles/traffic.json"):
+    """Average dram__bytes_read.sum + dram__bytes_write.sum per captured launch of a --set full report;
+    stored under `key` (a bench.py path name) for bench.py's roofline "traffic" field."""
+    import json
+    import os
+
+    raw = ncu_csv(["-i", path, "--page", "raw"])
+    hdr, units = raw[0], raw[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot, n = 0.0, 0
+    for row in raw[2:]:
+        if len(row) != len(hdr):
+            continue
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            j = hdr.index(m)
+            b += float(row[j].replace(",", "")) * scale.get(units[j], 1.0)
+        tot += b
+        n += 1
+    d = json.load(open(dst)) if os.path.exists(dst) else {}
+    d[key] = {"bytes_per_launch": tot / max(n, 1), "launches": n, "source": os.path.basename(path)}
+    json.dump(d, open(dst, "w"), indent=1)
+    print(key, d[key])
+
+
 if __name__ == "__main__":
-    {"rep": rep, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"rep": rep, "launches": launches, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])

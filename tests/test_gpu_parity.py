@@ -284,3 +284,20 @@ def test_ksg2_cfg1_sweep_and_xl(isy, orc):
     wl2 = datagen.cfg2(n=60_000)
     x2, y2 = wl2.series
     check_windows(isy, orc, x2, y2, [(7, 7 + 16385)], 4, debug=True, label="ksg2 xl", variant=1)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_warp_sorted_dense_batches(isy, orc, variant):
+    """Batches dense enough (>= 592 windows per class) for the warp-per-window sorted kernel (64 < w <= 256;
+    sparser classes take the latency-mode tile kernel), per-point outputs included."""
+    wl = datagen.cfg2(n=40_000)
+    x, y = wl.series
+    rng = np.random.default_rng(7 + variant)
+    W = []
+    for w, cnt in ((65, 600), (100, 650), (128, 600), (129, 600), (200, 620), (256, 600)):
+        t0 = rng.integers(0, len(x) - w, cnt)
+        W += [(int(a), int(a) + w) for a in t0]
+    check_windows(isy, orc, x, y, W, 4, debug=True, label=f"wsorted v{variant}", variant=variant)
+    xi = np.floor(datagen.Stream(3, 1).uniform(len(x)) * 5).astype(np.float32)  # heavy ties
+    check_windows(isy, orc, xi, y, W[::2] + W[1::2][:700], 3, debug=True, label=f"wsorted ties v{variant}",
+                  variant=variant)
