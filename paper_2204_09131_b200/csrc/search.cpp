@@ -774,7 +774,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
-    double eval_ms = 0.0, adv_ms = 0.0, bu_ms = 0.0;
+    double eval_ms = 0.0, adv_ms = 0.0, bu_ms = 0.0, wait_ms = 0.0;
     int64_t round_no = 0;
     std::FILE* trace = nullptr;
     if (const char* tp = std::getenv("ISYCOS_TRACE")) trace = std::fopen(tp, "a");
@@ -807,7 +807,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         recs.resize(F.owners.size());
         const auto t_ev = clk::now();
         Status s = eng->collect(g, recs.data(), &bs);
-        eval_ms += std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
+        const double wms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
+        eval_ms += wms;
+        wait_ms += wms;
         if (!s.ok()) return s;
         for (size_t i = 0; i < F.owners.size(); ++i) {
             Entry& e = *F.owners[i];
@@ -1036,8 +1038,8 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         bs.host_ms = wall - eval_ms;
         bs.add_to(&stats->kernel);
         if (trace)
-            std::fprintf(trace, "# host: advance %.3f ms (BU %.3f), other %.3f ms, eval %.3f ms, rounds %lld\n", adv_ms,
-                         bu_ms, wall - eval_ms - adv_ms, eval_ms, (long long)round_no);
+            std::fprintf(trace, "# host: advance %.3f ms (BU %.3f), other %.3f ms, eval %.3f ms (collect wait %.3f), "
+                         "rounds %lld\n", adv_ms, bu_ms, wall - eval_ms - adv_ms, eval_ms, wait_ms, (long long)round_no);
     }
     return Status{};
 }
