@@ -254,13 +254,20 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // bin windows: small (warp per window) R = 1,2,4,8; sorted-marginal path; brute-force tile R = 2,4,
     // and tile R = 1 ("latency mode": a CTA per small window, one point per thread) for small classes too
     // sparse to fill the GPU, where a warp walking 32R points serially would set the round's latency.
-    std::vector<int32_t> small[4];
-    std::vector<int32_t> tile[3];
+    // per-batch class lists: engine members reused across rounds (no allocations on the round path)
+    auto& small = bins_.small;
+    auto& tile = bins_.tile;
+    for (auto& v : small) v.clear();
+    for (auto& v : tile) v.clear();
     static const int kTileRs[3] = {2, 4, 1};
-    std::vector<int32_t> sorted;
-    std::vector<int64_t> soff;
-    std::vector<int32_t> fused;  // sorted path, fused sort+scan kernel (w <= kFusedMaxW)
-    std::vector<int32_t> wsorted[3];  // sorted path, warp per window, E = 2, 4, 8
+    auto& sorted = bins_.sorted;
+    auto& soff = bins_.soff;
+    auto& fused = bins_.fused;      // sorted path, fused sort+scan kernel (w <= kFusedMaxW)
+    auto& wsorted = bins_.wsorted;  // sorted path, warp per window, E = 2, 4, 8
+    sorted.clear();
+    soff.clear();
+    fused.clear();
+    for (auto& v : wsorted) v.clear();
     int fused_n2 = 256;
     int64_t n_items = 0, n_sitems = 0, spts = 0, n_segs = 0, n_mblocks = 0;
     int W2 = 0;
@@ -440,7 +447,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
 
     // launches: biggest work first so the small classes fill the tail
     int n_launch = 0, n_ksg = 0;
-    std::vector<int> launch_cls;  // 0 sorted-marginal group, 1 brute-force launch
+    std::vector<int>& launch_cls = S.launch_cls;  // 0 sorted-marginal group, 1 brute-force launch
+    launch_cls.clear();
     // algorithmic work: brute-force ordered pairs; sorted path binary-search probes (5 searches per point)
     int64_t brute_pairs = 0, probes = 0;
     for (int s = 0; s < 4; ++s)
@@ -566,7 +574,6 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.n = n;
     S.profile = profile;
     S.n_ksg = n_ksg;
-    S.launch_cls = std::move(launch_cls);
     S.pp = pp;
     S.n_launch = n_launch;
     S.brute_pairs = brute_pairs;

@@ -207,6 +207,10 @@ private:
     int32_t knn_mode_ = 1;
     int* dflag_ = nullptr;
     Slot slots_[2];
+    struct Bins {                    // size-class lists of the batch being packed (reused)
+        std::vector<int32_t> small[4], tile[3], sorted, fused, wsorted[3];
+        std::vector<int64_t> soff;
+    } bins_;
     bool sorted_on_ = true;
     bool fused_on_ = true;           // sorted windows w <= kFusedMaxW: fused sort+scan kernel ...
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
@@ -230,6 +234,7 @@ struct SearchParams {
     int32_t anchor_lookahead = 64;  // BU: climbs started at the predicted re-anchor point
     int32_t bu_depth = 4;           // BU: iterations of delta-neighbourhood requested per round
     int32_t trend_depth = 32;       // BU: positions requested along a climb's current direction (head climbs)
+    int32_t ring_rank = 1 << 30;    // BU: climbs at most this many positions behind the head request rings
     bool pipeline = true;           // two batches in flight (host advance overlaps GPU evaluation)
     int32_t auto_M = 0, auto_m = 0;  // method 4 (AUTO): Alg. 3 sampling (0 => 20, 6)
     double auto_alpha = 0.0, auto_rho = 0.0;  // Eqs. 4-9 weights (0 => 0.5, 0.5)

@@ -416,7 +416,7 @@ struct Climb {
     // Advance as far as the cache allows.  Returns true when the climb is finished.  A speculative
     // climb whose window has grown beyond `cap` pauses (requests nothing) until it nears the chain head.
     bool advance(const SearchParams& P, PairCache* cache, int32_t pair_id, int64_t hi,
-                 int64_t cap = INT64_MAX) {
+                 int64_t cap = INT64_MAX, bool ring = true) {
         if (finished) return true;
         View v{cache, &touched};
         const int64_t smin = P.s_min, smax = P.s_max;
@@ -494,7 +494,7 @@ struct Climb {
                     if (missing) {
                         touched.resize(mark);
                         if (cap == INT64_MAX && !(ring_t0 == t0 && ring_t1 == t1)) want_trend(v, P, hi, d);
-                        want_ring(v, P, hi, d);
+                        if (ring) want_ring(v, P, hi, d);
                         return false;
                     }
                     // best neighbour: first maximum of MI in (t0, t1) order (R15)
@@ -580,13 +580,17 @@ struct BuJob {
             auto r = climbs.try_emplace(l);
             if (r.second) {
                 r.first->second.lo = l;
-                r.first->second.advance(*P, cache, pair_id, hi, cap_for(l));
+                r.first->second.advance(*P, cache, pair_id, hi, cap_for(l), ring_for(l));
             }
         }
     }
 
     // Speculation policy: the head and the next climb run unrestricted; climbs further ahead pause
     // once their window exceeds spec_cap_mult * s_min (they are likely skipped by an accept).
+    // Depth speculation (the radius-D ring) only for the climbs nearest the chain head: farther climbs
+    // are the likeliest to be discarded by an accept, and their rings dominated the host time.
+    bool ring_for(int64_t l) const { return (l - chain) / P->s_min <= P->ring_rank; }
+
     int64_t cap_for(int64_t l) const {
         const int64_t rank = (l - chain) / P->s_min;
         if (rank <= 1 || P->spec_cap_mult <= 0) return INT64_MAX;
@@ -620,7 +624,8 @@ struct BuJob {
     void advance(int g = -1) {
         if (done) return;
         for (auto& kv : climbs)
-            if (g < 0 || group_of(kv.first) == g) kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first));
+            if (g < 0 || group_of(kv.first) == g)
+                kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first), ring_for(kv.first));
         ensure_lookahead();
         for (;;) {
             if (chain + P->s_min > hi) {

@@ -137,7 +137,7 @@ void harness_use_cache(int on) {
 
 struct HarnessParams {
     int32_t k, method, noise, p, h, t_max_idle, n_chunks, lookahead, bu_depth, anchor, spec_cap, trend, pipeline,
-        _pad;
+        ring_rank;
     int64_t s_min, s_max, delta_td, delta_bu;
     double sigma, tau_ratio;
     uint64_t seed;
@@ -163,6 +163,7 @@ int harness_search(const float* const* series, int64_t n, const int32_t* pairs, 
     if (hp->bu_depth > 0) P.bu_depth = hp->bu_depth;
     if (hp->trend >= 0) P.trend_depth = hp->trend;
     if (hp->pipeline >= 0) P.pipeline = hp->pipeline != 0;
+    if (hp->ring_rank > 0) P.ring_rank = hp->ring_rank;
     if (hp->anchor >= 0) P.anchor_lookahead = hp->anchor;
     if (hp->spec_cap >= 0) P.spec_cap_mult = hp->spec_cap;
     P.s_min = hp->s_min;

@@ -31,7 +31,7 @@ def build():
 
 class HarnessParams(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("k", "method", "noise", "p", "h", "t_max_idle", "n_chunks", "lookahead",
-                                         "bu_depth", "anchor", "spec_cap", "trend", "pipeline", "_pad")] + \
+                                         "bu_depth", "anchor", "spec_cap", "trend", "pipeline", "ring_rank")] + \
                [("s_min", C.c_int64), ("s_max", C.c_int64), ("delta_td", C.c_int64), ("delta_bu", C.c_int64),
                 ("sigma", C.c_double), ("tau_ratio", C.c_double), ("seed", C.c_uint64),
                 ("sizes", C.POINTER(C.c_int64)), ("n_sizes", C.c_int64), ("auto_M", C.c_int32), ("auto_m", C.c_int32),
@@ -67,7 +67,7 @@ def search(series, pairs, sc, **kw):
     P3 = np.asarray(pr, np.int32)
     hp = HarnessParams()
     d = dict(k=sc.k, method=sc.method, noise=int(sc.noise), p=sc.p, h=sc.h, t_max_idle=sc.t_max_idle,
-             n_chunks=sc.n_chunks, lookahead=0, bu_depth=0, anchor=-1, spec_cap=-1, trend=-1, pipeline=-1, s_min=sc.s_min, s_max=sc.s_max,
+             n_chunks=sc.n_chunks, lookahead=0, bu_depth=0, anchor=-1, spec_cap=-1, trend=-1, pipeline=-1, ring_rank=0, s_min=sc.s_min, s_max=sc.s_max,
              delta_td=sc.delta_td, delta_bu=sc.delta_bu, sigma=sc.sigma, tau_ratio=sc.tau_ratio, seed=sc.seed,
              auto_M=sc.auto_M, auto_m=sc.auto_m, auto_alpha=sc.auto_alpha, auto_rho=sc.auto_rho)
     d.update(kw)

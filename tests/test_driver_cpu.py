@@ -45,7 +45,8 @@ def test_cfg1_driver_equals_oracle(hz, orc, method, noise):
 @pytest.mark.parametrize("spec", [dict(lookahead=1), dict(lookahead=3, bu_depth=1), dict(bu_depth=2),
                                   dict(bu_depth=6, anchor=0), dict(spec_cap=0, anchor=128),
                                   dict(lookahead=500, spec_cap=1), dict(trend=0), dict(trend=1),
-                                  dict(trend=200, bu_depth=1), dict(pipeline=0), dict(pipeline=0, lookahead=2)])
+                                  dict(trend=200, bu_depth=1), dict(pipeline=0), dict(pipeline=0, lookahead=2),
+                                  dict(ring_rank=1), dict(ring_rank=3, trend=4)])
 def test_speculation_settings_do_not_change_results(hz, orc, spec):
     check(hz, orc, datagen.cfg1(), spec=spec, label=str(spec))
 
