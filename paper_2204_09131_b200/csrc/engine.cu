@@ -123,6 +123,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
+    if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
@@ -484,9 +485,12 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // copy, so independent size classes overlap (a round's latency is the slowest class, not the sum).
     int n_aux_used = 0;
     bool forked = false;
+    // small batches (<= aux_min_windows_) keep every launch on the slot's stream: the fork/join API calls
+    // cost more host time than the kernels' overlap saves there
+    const bool use_aux = n > aux_min_windows_;
     auto launch = [&](int nk, auto&& fn) -> Status {
         cudaStream_t sg = st;
-        if (n_ksg > 0) {
+        if (n_ksg > 0 && use_aux) {
             if (!forked) {
                 ISY_CK(cudaEventRecord(S.fork_ev, st));
                 forked = true;

@@ -215,6 +215,7 @@ private:
     bool fused_on_ = true;           // sorted windows w <= kFusedMaxW: fused sort+scan kernel ...
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
     int32_t sorted_min_w_ = 257;
+    int64_t aux_min_windows_ = 256;  // batches with more windows fork size classes onto aux streams
     int32_t wsorted_min_w_ = 65;     // small windows w in [this, 256]: warp-per-window sorted kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
 };

@@ -301,3 +301,32 @@ def test_warp_sorted_dense_batches(isy, orc, variant):
     xi = np.floor(datagen.Stream(3, 1).uniform(len(x)) * 5).astype(np.float32)  # heavy ties
     check_windows(isy, orc, xi, y, W[::2] + W[1::2][:700], 3, debug=True, label=f"wsorted ties v{variant}",
                   variant=variant)
+
+
+def test_maximum_window_and_empty_batch(isy, orc):
+    """ISYCOS_MAX_W = 2^18 (the int64 fixed-point bound): sampled per-point outputs against the oracle's
+    one-point definition and the record against the oracle finish of the per-point terms; an empty batch
+    is a no-op; one point over the maximum is E_RANGE."""
+    n = 300_000
+    st = datagen.Stream(17, 1)
+    x = datagen.f32(st.normal(n))
+    y = datagen.f32(0.6 * x.astype(np.float64) + 0.8 * st.normal(n))
+    w = 1 << 18
+    t0 = 11
+    got = isy.isycos_mi_batch_ex(x, y, [(t0, t0 + w)], 4, debug=True)
+    xs, ys = x[t0:t0 + w], y[t0:t0 + w]
+    rng = np.random.default_rng(1)
+    for i in list(rng.integers(0, w, 12)) + [0, w - 1]:
+        e, nx, ny = orc.point(xs, ys, int(i), 4)
+        assert (got["eps"][i], got["nx"][i], got["ny"][i]) == (np.float32(e), nx, ny), i
+    sp = sl = 0
+    for i in range(w):
+        a, b = orc.point_terms(got["nx"][i], got["ny"][i], got["eps"][i])
+        sp += a
+        sl += b
+    assert sp == got["s_psi"][0] and sl == got["s_log"][0]
+    assert orc.finish(sp, sl, int((got["eps"] == 0).sum()), w, 4) == (got["mi"][0], got["h"][0], got["nmi"][0])
+    assert len(isy.isycos_mi_batch(x, y, np.zeros((0, 2), np.int64), 4)) == 0
+    with pytest.raises(isy.IsycosError) as e:
+        isy.isycos_mi_batch(x, y, [(0, w + 1)], 4)
+    assert e.value.code == -2
