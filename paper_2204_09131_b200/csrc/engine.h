@@ -236,6 +236,7 @@ struct SearchParams {
     int32_t bu_depth = 4;           // BU: iterations of delta-neighbourhood requested per round
     int32_t trend_depth = 32;       // BU: positions requested along a climb's current direction (head climbs)
     int32_t ring_rank = 1 << 30;    // BU: climbs at most this many positions behind the head request rings
+    int32_t host_threads = 0;       // advance-phase host threads over pairs (0 => min(16, hardware))
     bool pipeline = true;           // two batches in flight (host advance overlaps GPU evaluation)
     int32_t auto_M = 0, auto_m = 0;  // method 4 (AUTO): Alg. 3 sampling (0 => 20, 6)
     double auto_alpha = 0.0, auto_rho = 0.0;  // Eqs. 4-9 weights (0 => 0.5, 0.5)

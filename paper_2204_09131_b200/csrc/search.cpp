@@ -15,13 +15,18 @@
 // counters equal the sequential oracle's exactly (tests/test_gpu_search.py).
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "engine.h"
@@ -668,6 +673,76 @@ struct BuJob {
     }
 };
 
+// ------------------------------------------------------------------ host thread pool
+// Pairs are independent state machines (own window cache, own jobs), so a round's advance phase runs
+// them on several host threads (dynamic scheduling by an atomic counter; the caller participates).
+// Multi-pair searches (configs[3], configs[4]) are host-bound without it.
+class HostPool {
+public:
+    explicit HostPool(int n) {
+        for (int i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    int size() const { return (int)threads_.size() + 1; }
+    void run(int count, const std::function<void(int)>& f) {
+        if (threads_.empty() || count <= 1) {
+            for (int i = 0; i < count; ++i) f(i);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &f;
+            total_ = count;
+            next_.store(0);
+            pending_ = (int)threads_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+private:
+    void work() {
+        for (;;) {
+            const int i = next_.fetch_add(1);
+            if (i >= total_) break;
+            (*fn_)(i);
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            work();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> threads_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* fn_ = nullptr;
+    std::atomic<int> next_{0};
+    int total_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
 // ------------------------------------------------------------------ chunks + merge
 std::vector<std::pair<int64_t, int64_t>> chunks_of(int64_t n, int32_t n_p, int64_t s_max) {
     std::vector<std::pair<int64_t, int64_t>> c;
@@ -705,6 +780,11 @@ std::vector<isycos_result_window> merge_windows(std::vector<isycos_result_window
 
 struct PairWork {
     int32_t inflight = 0;  // batches in flight holding entries of this pair
+    // this round's requests, staged by the pair's own (parallel) advance task
+    std::vector<KsgWin> stage_w;
+    std::vector<Entry*> stage_o;
+    bool stage_bad = false;
+    int64_t bad_t0 = 0, bad_t1 = 0;
     int32_t method = 3;    // 1 TD, 2 BU, 3 both
     int32_t kind = 0;      // 0: a search whose windows are results; 1: an iSYCOS trial run (Alg. 3 l.3-4)
     int32_t auto_id = -1;  // trial runs: index of the pair's selection state
@@ -751,6 +831,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     };
     std::deque<Unit> queue;
     std::vector<AutoState> autos;
+    int n_threads = P.host_threads;
+    if (n_threads <= 0) n_threads = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+    if (n_pairs <= 1 && P.method != 4) n_threads = 1;  // one pair: nothing to spread
+    HostPool pool(n_threads);
     const int32_t aM = P.auto_M > 0 ? P.auto_M : 20, am = P.auto_m > 0 ? P.auto_m : 6;
     for (int32_t p = 0; p < n_pairs; ++p) {
         if (P.method != 4) {
@@ -779,7 +863,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
-    double eval_ms = 0.0, adv_ms = 0.0, bu_ms = 0.0, wait_ms = 0.0;
+    double eval_ms = 0.0, adv_ms = 0.0, wait_ms = 0.0;
     int64_t round_no = 0;
     std::FILE* trace = nullptr;
     if (const char* tp = std::getenv("ISYCOS_TRACE")) trace = std::fopen(tp, "a");
@@ -798,6 +882,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         bool busy = false;
         std::vector<Entry*> owners;
         std::vector<PairWork*> pws;
+        std::vector<int64_t> offs;  // batch offset of each pair in pws (+ end)
     };
     Flight fl[2];
     const int n_groups = P.pipeline ? 2 : 1;
@@ -816,15 +901,19 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         eval_ms += wms;
         wait_ms += wms;
         if (!s.ok()) return s;
-        for (size_t i = 0; i < F.owners.size(); ++i) {
-            Entry& e = *F.owners[i];
-            e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
-            e.ready = true;
-        }
+        // records -> entries, pairs in parallel (each pair's records are a contiguous slice)
+        pool.run((int)F.pws.size(), [&](int p) {
+            for (int64_t i = F.offs[p]; i < F.offs[p + 1]; ++i) {
+                Entry& e = *F.owners[i];
+                e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
+                e.ready = true;
+            }
+        });
         for (PairWork* pw : F.pws) pw->inflight -= 1;
         F.busy = false;
         F.owners.clear();
         F.pws.clear();
+        F.offs.clear();
         return Status{};
     };
 
@@ -877,15 +966,30 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 active.push_back(std::move(pw));
                 progress = true;
             }
-            // advance this group's jobs
+            // advance this group's jobs (pairs in parallel on the host pool)
             const auto t_adv = clk::now();
-            for (auto& pw : active) {
+            pool.run((int)active.size(), [&](int i) {
+                PairWork* pw = active[i].get();
                 if (g == 0)
                     for (auto& j : pw->td) j.advance();
-                const auto t_bu = clk::now();
                 for (auto& j : pw->bu) j.advance(n_groups == 1 ? -1 : g);
-                bu_ms += std::chrono::duration<double, std::milli>(clk::now() - t_bu).count();
-            }
+                // stage the pair's requests for the batch (finished pairs: leftovers dropped)
+                pw->stage_w.clear();
+                pw->stage_o.clear();
+                if (!pw->finished()) {
+                    for (uint64_t k : pw->cache.pending) {
+                        const int64_t t0 = key_t0(k), w = key_w(k);
+                        if (t0 < 0 || t0 + w > n || w <= P.k) {  // never hand the kernels an out-of-range window
+                            pw->stage_bad = true;
+                            pw->bad_t0 = t0;
+                            pw->bad_t1 = t0 + w;
+                        }
+                        pw->stage_w.push_back(KsgWin{t0, (int32_t)w, -1, -1});
+                        pw->stage_o.push_back(pw->cache.map.find(k));
+                    }
+                }
+                pw->cache.pending.clear();
+            });
             adv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_adv).count();
             // retire finished pairs (none of their entries may be in flight)
             for (size_t i = 0; i < active.size();) {
@@ -963,26 +1067,29 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             batch.clear();
             Flight& F = fl[g];
             for (auto& pw : active) {
-                if (pw->cache.pending.empty()) continue;
-                if (pw->finished()) {
-                    pw->cache.pending.clear();
-                    continue;
-                }
+                if (pw->stage_bad)
+                    return make_err(ISYCOS_E_RANGE, "internal: search requested window [" +
+                                                        std::to_string(pw->bad_t0) + ", " + std::to_string(pw->bad_t1) +
+                                                        ")");
+                if (pw->stage_w.empty()) continue;
                 pw->slot = (int32_t)table.size();
                 table.push_back(pw->ptrs);
-                for (uint64_t k : pw->cache.pending) {
-                    const int64_t t0 = key_t0(k), w = key_w(k);
-                    if (t0 < 0 || t0 + w > n || w <= P.k)  // never hand the kernels an out-of-range window
-                        return make_err(ISYCOS_E_RANGE, "internal: search requested window [" + std::to_string(t0) +
-                                                            ", " + std::to_string(t0 + w) + ")");
-                    batch.push_back(KsgWin{t0, (int32_t)w, pw->slot, -1});
-                    F.owners.push_back(pw->cache.map.find(k));
+                F.offs.push_back((int64_t)batch.size());
+                for (KsgWin kw : pw->stage_w) {
+                    kw.pair = pw->slot;
+                    batch.push_back(kw);
                 }
-                pw->cache.pending.clear();
+                F.owners.insert(F.owners.end(), pw->stage_o.begin(), pw->stage_o.end());
+                pw->stage_w.clear();
+                pw->stage_o.clear();
                 pw->inflight += 1;
                 F.pws.push_back(pw.get());
             }
-            if (batch.empty()) continue;
+            if (batch.empty()) {
+                F.offs.clear();
+                continue;
+            }
+            F.offs.push_back((int64_t)batch.size());
             const auto t_ev = clk::now();
             Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
                                    P.variant, DebugOut{}, sts[g], P.flags, &bs);
@@ -1043,8 +1150,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         bs.host_ms = wall - eval_ms;
         bs.add_to(&stats->kernel);
         if (trace)
-            std::fprintf(trace, "# host: advance %.3f ms (BU %.3f), other %.3f ms, eval %.3f ms (collect wait %.3f), "
-                         "rounds %lld\n", adv_ms, bu_ms, wall - eval_ms - adv_ms, eval_ms, wait_ms, (long long)round_no);
+            std::fprintf(trace, "# host: advance %.3f ms (%d threads), other %.3f ms, eval %.3f ms (collect wait %.3f), "
+                         "rounds %lld\n", adv_ms, pool.size(), wall - eval_ms - adv_ms, eval_ms, wait_ms,
+                         (long long)round_no);
     }
     return Status{};
 }
