@@ -685,62 +685,70 @@ public:
     ~HostPool() {
         {
             std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            ++gen_;
+            stop_.store(true);
+            gen_.fetch_add(1);
         }
         cv_.notify_all();
         for (auto& t : threads_) t.join();
     }
     int size() const { return (int)threads_.size() + 1; }
+    // Runs f(0..count-1) on the pool.  Workers spin briefly between tasks (a search round is ~50 us, a
+    // futex wake-up per worker per task cost more than the parallel work saved) and sleep when idle.
     void run(int count, const std::function<void(int)>& f) {
         if (threads_.empty() || count <= 1) {
             for (int i = 0; i < count; ++i) f(i);
             return;
         }
+        fn_ = &f;
+        total_ = count;
+        next_.store(0, std::memory_order_relaxed);
+        pending_.store((int)threads_.size(), std::memory_order_relaxed);
         {
             std::lock_guard<std::mutex> lk(mu_);
-            fn_ = &f;
-            total_ = count;
-            next_.store(0);
-            pending_ = (int)threads_.size();
-            ++gen_;
+            gen_.fetch_add(1, std::memory_order_release);
         }
-        cv_.notify_all();
+        if (sleepers_.load(std::memory_order_acquire) > 0) cv_.notify_all();
         work();
-        std::unique_lock<std::mutex> lk(mu_);
-        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        while (pending_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
     }
 
 private:
     void work() {
         for (;;) {
-            const int i = next_.fetch_add(1);
+            const int i = next_.fetch_add(1, std::memory_order_relaxed);
             if (i >= total_) break;
             (*fn_)(i);
         }
     }
     void loop() {
-        uint64_t seen = 0;
+        uint64_t seen = 0;  // gen_ starts at 0 (a thread may start after the first run() began)
         for (;;) {
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (stop_) return;
+            uint64_t g = gen_.load(std::memory_order_acquire);
+            for (int spin = 0; g == seen && spin < 20000; ++spin) {
+                std::this_thread::yield();
+                g = gen_.load(std::memory_order_acquire);
             }
+            if (g == seen) {
+                std::unique_lock<std::mutex> lk(mu_);
+                sleepers_.fetch_add(1);
+                cv_.wait(lk, [&] { return gen_.load() != seen; });
+                sleepers_.fetch_sub(1);
+                g = gen_.load();
+            }
+            seen = g;
+            if (stop_.load()) return;
             work();
-            std::lock_guard<std::mutex> lk(mu_);
-            if (--pending_ == 0) done_cv_.notify_one();
+            pending_.fetch_sub(1, std::memory_order_acq_rel);
         }
     }
     std::vector<std::thread> threads_;
     std::mutex mu_;
-    std::condition_variable cv_, done_cv_;
+    std::condition_variable cv_;
     const std::function<void(int)>* fn_ = nullptr;
-    std::atomic<int> next_{0};
-    int total_ = 0, pending_ = 0;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::atomic<int> next_{0}, pending_{0}, sleepers_{0};
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<bool> stop_{false};
+    int total_ = 0;
 };
 
 // ------------------------------------------------------------------ chunks + merge
@@ -901,9 +909,11 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         eval_ms += wms;
         wait_ms += wms;
         if (!s.ok()) return s;
-        // records -> entries, pairs in parallel (each pair's records are a contiguous slice)
-        pool.run((int)F.pws.size(), [&](int p) {
-            for (int64_t i = F.offs[p]; i < F.offs[p + 1]; ++i) {
+        // records -> entries, pairs in parallel for big batches (each pair's records are a contiguous slice)
+        pool.run(F.owners.size() >= 4096 ? (int)F.pws.size() : 1, [&](int p) {
+            if (F.owners.size() < 4096) p = -1;
+            const int64_t i0 = p < 0 ? 0 : F.offs[p], i1 = p < 0 ? (int64_t)F.owners.size() : F.offs[p + 1];
+            for (int64_t i = i0; i < i1; ++i) {
                 Entry& e = *F.owners[i];
                 e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
                 e.ready = true;
