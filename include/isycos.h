@@ -75,6 +75,8 @@ enum {
 #define ISYCOS_F_PROFILE 1u /* record CUDA events around every KSG kernel; fills *_kernel_ms */
 #define ISYCOS_F_BRUTE 2u   /* route every window to the brute-force kernels (no sorted-marginal path);
                                results are bit-identical either way — an A/B and test knob */
+#define ISYCOS_F_PROFILE_SORTED_ONLY 8u /* with ISYCOS_F_PROFILE: events around sorted-path launches only */
+#define ISYCOS_F_PROFILE_BRUTE_ONLY 16u  /* with ISYCOS_F_PROFILE: events around brute-force launches only */
 #define ISYCOS_F_UNFUSED 4u /* sorted-marginal windows always take the throughput form (sort kernel, then
                                scan kernel), never the fused latency kernel; results identical */
 

@@ -17,6 +17,8 @@ ISYCOS_OK, E_INVAL, E_RANGE, E_TOO_FEW, E_TRUNC, E_CUDA, E_NOMEM, E_NCCL = 0, -1
 F_PROFILE = 1
 F_BRUTE = 2   # force the brute-force kernels (A/B and test knob; results identical)
 F_UNFUSED = 4  # sorted path in its throughput form only (no fused latency kernel)
+F_PROFILE_SORTED_ONLY = 8
+F_PROFILE_BRUTE_ONLY = 16
 MAX_K = 16
 MAX_W = 262144
 ERROR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_RANGE", -3: "E_TOO_FEW", -4: "E_TRUNC", -5: "E_CUDA",
@@ -237,7 +239,7 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
                   delta_bu: int = 0, t_max_idle: int = 3, h: int = 5, n_chunks: int = 1, lookahead: int = 0,
                   seed: int = 0, variant: int = 0, profile: bool = False, brute: bool = False,
                   unfused: bool = False, stream=None, capacity: int = 1 << 16, auto_M: int = 0, auto_m: int = 0,
-                  auto_alpha: float = 0.0, auto_rho: float = 0.0):
+                  auto_alpha: float = 0.0, auto_rho: float = 0.0, profile_only: str | None = None):
     """SYCOS search over series pairs.  Returns (results, stats).
 
     series: list of float32 arrays / tensors (host or CUDA, all alike, same length)
@@ -266,6 +268,8 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
     o.n_chunks, o.lookahead, o.seed = int(n_chunks), int(lookahead), int(seed) & ((1 << 64) - 1)
     o.auto_M, o.auto_m, o.auto_alpha, o.auto_rho = int(auto_M), int(auto_m), float(auto_alpha), float(auto_rho)
     o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
+    if profile and profile_only:  # events around one path's launches only ("sorted" or "brute")
+        o.flags |= F_PROFILE_SORTED_ONLY if profile_only == "sorted" else F_PROFILE_BRUTE_ONLY
     o.stream = _stream_ptr(stream)
     while True:
         outw = (ResultWindow * max(1, capacity))()

@@ -488,7 +488,12 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // small batches (<= aux_min_windows_) keep every launch on the slot's stream: the fork/join API calls
     // cost more host time than the kernels' overlap saves there
     const bool use_aux = n > aux_min_windows_;
-    auto launch = [&](int nk, auto&& fn) -> Status {
+    // profiling: events around the launch groups of the selected path(s) only (event records cost host time
+    // on every round: bench.py times the dominant path alone)
+    const bool prof_sorted = profile && !(flags & ISYCOS_F_PROFILE_BRUTE_ONLY);
+    const bool prof_brute = profile && !(flags & ISYCOS_F_PROFILE_SORTED_ONLY);
+    int n_prof = 0;
+    auto launch = [&](int cls, int nk, auto&& fn) -> Status {
         cudaStream_t sg = st;
         if (n_ksg > 0 && use_aux) {
             if (!forked) {
@@ -502,12 +507,17 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             }
         }
         std::pair<cudaEvent_t, cudaEvent_t> ev{};
-        if (profile) {
-            ev = ev_pair(n_ksg);
+        const bool prof = cls == 0 ? prof_sorted : prof_brute;
+        if (prof) {
+            ev = ev_pair(n_prof);
             ISY_CK(cudaEventRecord(ev.first, sg));
         }
         ISY_CK(fn(sg));
-        if (profile) ISY_CK(cudaEventRecord(ev.second, sg));
+        if (prof) {
+            ISY_CK(cudaEventRecord(ev.second, sg));
+            launch_cls.push_back(cls);
+            ++n_prof;
+        }
         ++n_ksg;
         n_launch += nk;
         return Status{};
@@ -515,16 +525,14 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     if (!fused.empty()) {
         const int32_t* dfl = reinterpret_cast<const int32_t*>(S.dstage + off_flist);
         const KsgItem* dfi = reinterpret_cast<const KsgItem*>(S.dstage + off_fitems);
-        launch_cls.push_back(0);
-        Status r = launch(1, [&](cudaStream_t sg) { return launch_fused(L, dfl, dfi, (int32_t)n_fitems, gmax, sg); });
+        Status r = launch(0, 1, [&](cudaStream_t sg) { return launch_fused(L, dfl, dfi, (int32_t)n_fitems, gmax, sg); });
         if (!r.ok()) return r;
     }
     for (int e = 2; e >= 0; --e) {
         if (wsorted[e].empty()) continue;
         const int32_t* wlp = reinterpret_cast<const int32_t*>(S.dstage + off_wlist) + wlist_off[e];
         const int32_t cnt = (int32_t)wsorted[e].size();
-        launch_cls.push_back(0);
-        Status r = launch(1, [&](cudaStream_t sg) { return launch_wsorted(L, wlp, cnt, 2 << e, sg); });
+        Status r = launch(0, 1, [&](cudaStream_t sg) { return launch_wsorted(L, wlp, cnt, 2 << e, sg); });
         if (!r.ok()) return r;
     }
     if (!sorted.empty()) {
@@ -539,8 +547,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         float* TY = reinterpret_cast<float*>(S.sscratch + spts * 24);
         const KsgItem* dsg = reinterpret_cast<const KsgItem*>(S.dstage + off_segs);
         const KsgItem* dmb = reinterpret_cast<const KsgItem*>(S.dstage + off_mblk);
-        launch_cls.push_back(0);
-        Status r = launch(n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
+        Status r = launch(0, n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
                                  W2, dsi, (int32_t)n_sitems, sg);
         });
@@ -552,8 +559,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         int64_t cnt = 0;
         for (int32_t q : tile[s]) cnt += (wins[q].w + kTileThreads * R - 1) / (kTileThreads * R);
         const KsgItem* ip = ditems + item_off[s];
-        launch_cls.push_back(1);
-        Status r = launch(1, [&](cudaStream_t sg) { return launch_ksg_tile(L, ip, (int32_t)cnt, R, sg); });
+        Status r = launch(1, 1, [&](cudaStream_t sg) { return launch_ksg_tile(L, ip, (int32_t)cnt, R, sg); });
         if (!r.ok()) return r;
     }
     for (int s = 3; s >= 0; --s) {
@@ -561,8 +567,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         const int R = 1 << s;
         const int32_t* lp = dlists + list_off[s];
         const int32_t cnt = (int32_t)small[s].size();
-        launch_cls.push_back(1);
-        Status r = launch(1, [&](cudaStream_t sg) { return launch_ksg_small(L, lp, cnt, R, sg); });
+        Status r = launch(1, 1, [&](cudaStream_t sg) { return launch_ksg_small(L, lp, cnt, R, sg); });
         if (!r.ok()) return r;
     }
     for (int a = 0; a < std::min(n_aux_used, kAux); ++a) {  // join
@@ -577,7 +582,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.st = st;
     S.n = n;
     S.profile = profile;
-    S.n_ksg = n_ksg;
+    S.n_ksg = n_prof;  // profiled launch groups (events / launch_cls entries)
     S.pp = pp;
     S.n_launch = n_launch;
     S.brute_pairs = brute_pairs;

@@ -910,8 +910,8 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         wait_ms += wms;
         if (!s.ok()) return s;
         // records -> entries, pairs in parallel for big batches (each pair's records are a contiguous slice)
-        pool.run(F.owners.size() >= 4096 ? (int)F.pws.size() : 1, [&](int p) {
-            if (F.owners.size() < 4096) p = -1;
+        pool.run(F.owners.size() >= 512 ? (int)F.pws.size() : 1, [&](int p) {
+            if (F.owners.size() < 512) p = -1;
             const int64_t i0 = p < 0 ? 0 : F.offs[p], i1 = p < 0 ? (int64_t)F.owners.size() : F.offs[p + 1];
             for (int64_t i = i0; i < i1; ++i) {
                 Entry& e = *F.owners[i];
