@@ -45,7 +45,9 @@ class KernelStats(C.Structure):
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("host_ms", C.c_double),
                 ("wall_ms", C.c_double), ("scan_steps", C.c_int64), ("sorted_windows", C.c_int64),
                 ("sorted_points", C.c_int64), ("brute_point_pairs", C.c_int64), ("search_probes", C.c_int64),
-                ("sorted_kernel_ms", C.c_double), ("brute_kernel_ms", C.c_double)]
+                ("sorted_kernel_ms", C.c_double), ("brute_kernel_ms", C.c_double), ("profiled_rounds", C.c_int64),
+                ("prof_brute_point_pairs", C.c_int64), ("prof_scan_steps", C.c_int64),
+                ("prof_search_probes", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

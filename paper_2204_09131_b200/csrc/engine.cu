@@ -66,6 +66,10 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
     s->search_probes += search_probes;
     s->sorted_kernel_ms += sorted_ms;
     s->brute_kernel_ms += brute_ms;
+    s->profiled_rounds += prof_rounds;
+    s->prof_brute_point_pairs += prof_brute_pairs;
+    s->prof_scan_steps += prof_scan_steps;
+    s->prof_search_probes += prof_probes;
 }
 
 // ---------------------------------------------------------------- engine registry (one per device)
@@ -124,6 +128,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
+    if (const char* m = std::getenv("ISYCOS_PROFILE_EVERY")) profile_every_ = std::max<int64_t>(1, std::atoll(m));
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
@@ -242,7 +247,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     Slot& S = slots_[si];
     S.n = 0;
     S.busy = false;
-    const bool profile = (flags & ISYCOS_F_PROFILE) != 0;
+    const bool profile = (flags & ISYCOS_F_PROFILE) != 0 && (profile_ctr_++ % profile_every_) == 0;
     const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
     if (n > INT32_MAX / 2) return make_err(ISYCOS_E_INVAL, "batch too large");
@@ -619,6 +624,10 @@ Status Engine::collect(int si, KsgRec* recs_host, BatchStats* bs) {
         bs->brute_pairs += S.brute_pairs;
         bs->search_probes += S.probes;
         if (S.profile) {
+            bs->prof_rounds += 1;
+            bs->prof_brute_pairs += S.brute_pairs;
+            bs->prof_scan_steps += (int64_t)steps;
+            bs->prof_probes += S.probes;
             for (int i = 0; i < S.n_ksg; ++i) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, S.events[2 * i], S.events[2 * i + 1]);

@@ -122,6 +122,7 @@ struct BatchStats {
     int64_t scan_steps = 0, sorted_windows = 0, sorted_points = 0;
     int64_t brute_pairs = 0, search_probes = 0;
     double sorted_ms = 0.0, brute_ms = 0.0;
+    int64_t prof_rounds = 0, prof_brute_pairs = 0, prof_scan_steps = 0, prof_probes = 0;
     double kernel_ms = 0.0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     double host_ms = 0.0, wall_ms = 0.0;
@@ -216,6 +217,8 @@ private:
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
     int32_t sorted_min_w_ = 257;
     int64_t aux_min_windows_ = 256;  // batches with more windows fork size classes onto aux streams
+    int64_t profile_every_ = 1;      // ISYCOS_F_PROFILE: time every N-th round (event records cost host time)
+    int64_t profile_ctr_ = 0;
     int32_t wsorted_min_w_ = 65;     // small windows w in [this, 256]: warp-per-window sorted kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
 };

@@ -119,18 +119,21 @@ def launches(path, dst):
     open(dst, "w").write("\n".join(lines) + "\n")
 
 
-def traffic(path, key, dst="profiles/traffic.json"):
+def traffic(path, key, name_re=".*", dst="profiles/traffic.json"):
     """Average dram__bytes_read.sum + dram__bytes_write.sum per captured launch of a --set full report;
     stored under `key` (a bench.py path name) for bench.py's roofline "traffic" field."""
     import json
     import os
 
+    import re
+
     raw = ncu_csv(["-i", path, "--page", "raw"])
     hdr, units = raw[0], raw[1]
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    kn = hdr.index("Kernel Name")
     tot, n = 0.0, 0
     for row in raw[2:]:
-        if len(row) != len(hdr):
+        if len(row) != len(hdr) or not re.search(name_re, row[kn]):
             continue
         b = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
@@ -139,7 +142,8 @@ def traffic(path, key, dst="profiles/traffic.json"):
         tot += b
         n += 1
     d = json.load(open(dst)) if os.path.exists(dst) else {}
-    d[key] = {"bytes_per_launch": tot / max(n, 1), "launches": n, "source": os.path.basename(path)}
+    d[key] = {"bytes_per_launch": tot / max(n, 1), "launches": n, "source": os.path.basename(path),
+              "kernels": name_re}
     json.dump(d, open(dst, "w"), indent=1)
     print(key, d[key])
 
