@@ -138,3 +138,49 @@ def test_multi_pair_auto_selection(isy, orc):
     ores, ost, gres, gst = run_both(isy, orc, wl, pairs=pairs, s_max=1024, method=4, auto_M=5, auto_m=2)
     assert_same(ores, ost, gres, gst, "cfg4 auto")
     assert gst["auto_td"] + gst["auto_bu"] == len(pairs)
+
+
+# ---------------------------------------------------------------- BASELINE.json full sizes (sampled outputs)
+def _check_result_windows(orc, series, pairs, res, sc, n_check=6):
+    """Properties every result set must have at any size: per (pair, method) pairwise
+    disjoint, s_min <= |w| <= s_max, nmi >= sigma, sorted by (pair, method, t0); and a sample of the
+    windows re-evaluated one by one by the oracle, bitwise (mi, h, nmi)."""
+    assert res == sorted(res, key=lambda r: (r[0], r[1], r[2]))
+    by = {}
+    for r in res:
+        by.setdefault((r[0], r[1]), []).append(r)
+        assert sc.s_min <= r[3] - r[2] <= sc.s_max and r[6] >= sc.sigma
+    for lst in by.values():
+        for a, b in zip(lst, lst[1:]):
+            assert a[3] <= b[2], (a, b)
+    pid = {p[2] if len(p) > 2 else i: p for i, p in enumerate(pairs)}
+    for r in sorted(res, key=lambda r: r[3] - r[2])[:n_check]:  # the cheapest ones for the O(w^2) oracle
+        xs, ys = pid[r[0]][0], pid[r[0]][1]
+        ref = orc.mi_batch(series[xs], series[ys], np.asarray([[r[2], r[3]]], np.int64), sc.k)
+        assert (r[4], r[5], r[6]) == (ref["mi"][0], ref["h"][0], ref["nmi"][0]), r
+
+
+def test_full_size_cfg4_pairs(isy, orc):
+    """configs[3] at full size (n = 1,000,000, scales 64..16,384, TD+BU, noise on) on three of its pairs
+    (two planted, one background); sampled result windows against the oracle, properties on all."""
+    wl = datagen.cfg4()
+    planted = sorted(wl.planted)[:2]
+    pairs = [tuple(wl.pairs[i]) + (i,) for i in planted] + [tuple(wl.pairs[5]) + (5,)]
+    res, st = isy.search_workload(wl, pairs=pairs)
+    _check_result_windows(orc, wl.series, pairs, res, wl.search)
+    for i in planted:  # each planted relation is found (union coverage >= 0.5 by either method)
+        (a, b, _), = wl.planted[i]
+        cov = set()
+        for r in res:
+            if r[0] == i:
+                cov.update(range(max(a, r[2]), min(b, r[3])))
+        assert len(cov) >= 0.5 * (b - a), (i, a, b, len(cov))
+
+
+def test_full_size_cfg5_pair(isy, orc):
+    """configs[4] at full size for one pair (n = 10,000,000, scales 128..65,536, 16 chunks, TD + noise
+    pruning): XL windows, the chunk plan and the merge; sampled windows against the oracle."""
+    wl = datagen.cfg5(n_series=2)
+    res, st = isy.search_workload(wl, pairs=[(0, 1, 0)])
+    _check_result_windows(orc, wl.series, [(0, 1, 0)], res, wl.search, n_check=4)
+    assert st["td_windows"] > 0
