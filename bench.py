@@ -131,6 +131,17 @@ def traffic_for(path):
         return None
 
 
+def issue_for(key):
+    """Issue efficiency of the path's kernels from the committed ncu --set full capture
+    (profiles/issue.json, written by `scripts/ncu_summary.py issue`): warp-issue utilisation and the
+    fraction of the FP32/INT32 lane-issue peak used (the north star's "% of issue peak"); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
 def compares_of(stats):
     # 2 * sum w(w-1) over the distinct windows the search consumed (brute-force-equivalent compares)
     return 2.0 * stats["distinct_pairs"]
@@ -233,6 +244,7 @@ def sweep_cfg3(isy, stream, reps: int):
                          "achieved": alg / (kms / 1e3) / 1e12 if kms else None, "peak": peak / 1e12,
                          "unit": "Tcompare/s", "frac": alg / (kms / 1e3) / peak if kms else None,
                          "kernel_share_of_step": kms / ms if ms else None,
+                         "ncu_issue": issue_for("sorted_throughput"),
                          "algorithmic_compares_per_step": alg,
                          "scan_steps_per_point": st["scan_steps"] / max(1, st["sorted_points"])}}
 
@@ -448,6 +460,7 @@ def main():
                          "kernel_share_of_step": (paths[dom]["kernel_ms"] * rounds / max(1, kk.get("profiled_rounds", 0))
                                                   / ms_total) if ms_total else None,
                          "paths": paths,
+                         "ncu_issue": issue_for(dom),
                          "bruteforce_equivalent_compares_per_step": 2.0 * kpairs / args.steps},
             "e2e": {"value": e2e_all / (e2e_max / 1e3), "unit": "compares/s",
                     "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},

@@ -148,5 +148,47 @@ def traffic(path, key, name_re=".*", dst="profiles/traffic.json"):
     print(key, d[key])
 
 
+def issue(path, key, name_re=".*", dst="profiles/issue.json"):
+    """Issue efficiency of the matching launches of a --set full report (launch-duration weighted):
+    warp-issue utilisation (smsp__issue_active / cycles) x lane utilisation (avg active threads / 32) =
+    the fraction of the SMs' FP32/INT32 lane-issue peak actually used (the north star's "% of issue
+    peak").  Stored under `key` for bench.py's roofline object."""
+    import json
+    import os
+    import re
+
+    rows = ncu_csv(["-i", path, "--page", "details"])
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+    per = {}
+    for r in rows[1:]:
+        if len(r) <= ix["Metric Value"] or not re.search(name_re, r[ix["Kernel Name"]]):
+            continue
+        d = per.setdefault(r[ix["ID"]], {})
+        d[r[ix["Metric Name"]]] = r[ix["Metric Value"]].replace(",", "")
+    tw = busy = lanes = 0.0
+    n = 0
+    for d in per.values():
+        try:
+            dur = float(d["Duration"])
+            b = float(d["Issue Slots Busy"]) / 100.0
+            a = float(d["Avg. Active Threads Per Warp"]) / 32.0
+        except (KeyError, ValueError):
+            continue
+        tw += dur
+        busy += dur * b
+        lanes += dur * b * a
+        n += 1
+    if not n:
+        print(key, "no launches matched")
+        return
+    out = {"issue_slots_busy": busy / tw, "lane_issue_frac": lanes / tw, "launches": n,
+           "source": os.path.basename(path), "kernels": name_re}
+    dd = json.load(open(dst)) if os.path.exists(dst) else {}
+    dd[key] = out
+    json.dump(dd, open(dst, "w"), indent=1)
+    print(key, out)
+
+
 if __name__ == "__main__":
-    {"rep": rep, "launches": launches, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
+    {"rep": rep, "launches": launches, "traffic": traffic, "issue": issue}[sys.argv[1]](*sys.argv[2:])
