@@ -235,7 +235,7 @@ def sweep_cfg3(isy, stream, reps: int):
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / reps
     peak = peak_compares(1965.0)
-    alg = (st["scan_steps"] + st["search_probes"]) / reps
+    alg = (st["prof_scan_steps"] + st["prof_search_probes"]) / reps
     kms = st["sorted_kernel_ms"] / reps
     return {"workload": "cfg3 sweep (configs[2]): 17,460 windows x k in {3,4,8} per step",
             "ms_per_step": ms, "windows_per_s": len(W) * len(ks) / (ms / 1e3),

@@ -101,8 +101,8 @@ typedef struct {
     int64_t brute_point_pairs; /* ordered point pairs of windows evaluated by the brute-force kernels */
     int64_t search_probes; /* sorted path: binary-search probes (5 searches x ceil(log2 w) per point) */
     double sorted_kernel_ms, brute_kernel_ms; /* ISYCOS_F_PROFILE: per-path share of kernel_ms */
-    /* ISYCOS_F_PROFILE samples every ISYCOS_PROFILE_EVERY-th round (env, default 1): the work of the
-     * profiled rounds, to divide by the *_kernel_ms above */
+    /* isycos_search with ISYCOS_F_PROFILE times every ISYCOS_PROFILE_EVERY-th round (env, default 1):
+     * the work of the profiled rounds, to divide by the *_kernel_ms above */
     int64_t profiled_rounds, prof_brute_point_pairs, prof_scan_steps, prof_search_probes;
 } isycos_kernel_stats;
 

@@ -267,6 +267,7 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     if (const char* e = std::getenv("ISYCOS_PIPELINE")) P.pipeline = std::atoi(e) != 0;
     if (const char* e = std::getenv("ISYCOS_RING_RANK")) P.ring_rank = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_HOST_THREADS")) P.host_threads = std::atoi(e);
+    if (const char* e = std::getenv("ISYCOS_PROFILE_EVERY")) P.profile_every = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("ISYCOS_ANCHOR")) P.anchor_lookahead = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_SPEC_CAP")) P.spec_cap_mult = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_LOOKAHEAD")) P.lookahead = std::atoi(e);

@@ -128,7 +128,6 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
-    if (const char* m = std::getenv("ISYCOS_PROFILE_EVERY")) profile_every_ = std::max<int64_t>(1, std::atoll(m));
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
@@ -247,7 +246,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     Slot& S = slots_[si];
     S.n = 0;
     S.busy = false;
-    const bool profile = (flags & ISYCOS_F_PROFILE) != 0 && (profile_ctr_++ % profile_every_) == 0;
+    const bool profile = (flags & ISYCOS_F_PROFILE) != 0;
     const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
     if (n > INT32_MAX / 2) return make_err(ISYCOS_E_INVAL, "batch too large");

@@ -217,8 +217,6 @@ private:
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
     int32_t sorted_min_w_ = 257;
     int64_t aux_min_windows_ = 256;  // batches with more windows fork size classes onto aux streams
-    int64_t profile_every_ = 1;      // ISYCOS_F_PROFILE: time every N-th round (event records cost host time)
-    int64_t profile_ctr_ = 0;
     int32_t wsorted_min_w_ = 65;     // small windows w in [this, 256]: warp-per-window sorted kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
 };
@@ -240,6 +238,7 @@ struct SearchParams {
     int32_t trend_depth = 32;       // BU: positions requested along a climb's current direction (head climbs)
     int32_t ring_rank = 1 << 30;    // BU: climbs at most this many positions behind the head request rings
     int32_t host_threads = 0;       // advance-phase host threads over pairs (0 => min(16, hardware))
+    int32_t profile_every = 1;      // ISYCOS_F_PROFILE in a search: time every N-th round (env ISYCOS_PROFILE_EVERY)
     bool pipeline = true;           // two batches in flight (host advance overlaps GPU evaluation)
     int32_t auto_M = 0, auto_m = 0;  // method 4 (AUTO): Alg. 3 sampling (0 => 20, 6)
     double auto_alpha = 0.0, auto_rho = 0.0;  // Eqs. 4-9 weights (0 => 0.5, 0.5)

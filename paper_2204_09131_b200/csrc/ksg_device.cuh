@@ -554,7 +554,7 @@ __device__ __forceinline__ void warp_sort(T (&v)[E], int lane) {
 // not idle on their slowest lane (per-point scan lengths vary several-fold with the local density ratio).
 template <int K1>
 __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0, int wb, int we, float* eps_s,
-                                               unsigned long long& steps) {
+                                               unsigned long long& steps, int2* stop_s = nullptr) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     constexpr int B = 4;
@@ -622,6 +622,7 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
             if (!lact && !ract) {
                 fin = true;
                 eps_s[mloc] = rk[K1 - 1];
+                if (stop_s) stop_s[mloc] = make_int2(lj, rj);  // next unvisited index on each side
             }
         }
         const unsigned fm = __ballot_sync(0xffffffffu, fin);
@@ -642,10 +643,11 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
 
 // Phase B for one point at sorted position m (a4, a5): interval counts by binary search with the
 // identical predicates, digamma / log terms, debug outputs.
+// [xlo, xhi] brackets the x-interval's ends (KSG-1: from phase A's stopping points; else [0, w]).
 template <bool V2>
 __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_t dbg, const float2* P2,
                                                const int32_t* OX, const float* YS, int m, float eps, long long& sp,
-                                               long long& sl, int& z) {
+                                               long long& sl, int& z, int xlo = 0, int xhi = INT_MAX) {
     const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
     const float2 me = P2[m];
     const float xv = me.x, yv = me.y;
@@ -654,14 +656,14 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
     if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
     if (V2 || eps > 0.0f) {
         // x: left part [0, m] uses fl(x_i - x_j) < ex, right part [m, w) uses fl(x_j - x_i) < ex
-        int lo = 0, hi = m;
+        int lo = V2 ? 0 : xlo, hi = m;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (xv - XS[2 * mid] < ex) hi = mid; else lo = mid + 1;
         }
         const int Lx = lo;
         lo = m;
-        hi = w;
+        hi = V2 ? w : min(w, xhi);
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
@@ -688,22 +690,35 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
 // Scan of one CTA's slice [cta0, cta0 + cta_n) of a window's x-sorted points (arrays in global or shared
 // memory, generic pointers): P2[m] = (x, y) of the m-th point in x order, OX[m] its window index, YS the
 // sorted y.  Each warp owns a contiguous part of the slice.  Ends with the CTA reduction.
+//
+// KSG-1 narrowing: phase A stops a side at a block whose farthest candidate has |dx| >= r(t) >= eps, so
+// with lj / rj the next unvisited indices, positions <= lj + 1 and >= rj - 1 are outside the strict
+// interval {|dx| < eps}: the x binary searches run on [lj + 2, m] and [m, rj - 1] (stop_s, optional).
+// (KSG-2's closed |dx| <= d_x, d_x <= eps, may include |dx| = eps: full ranges there.)
 template <int K1, bool V2>
 __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, int ntiles, const float2* P2,
-                                            const int32_t* OX, const float* YS, int cta0, int cta_n, float* eps_s) {
+                                            const int32_t* OX, const float* YS, int cta0, int cta_n, float* eps_s,
+                                            int2* stop_s = nullptr) {
     const int nwarps = blockDim.x >> 5;
     const int kPerWarp = (cta_n + nwarps - 1) / nwarps;
     const int warp = threadIdx.x >> 5;
     const int wb = min(warp * kPerWarp, cta_n);
     const int we = min(wb + kPerWarp, cta_n);
     unsigned long long steps = 0;
-    sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps);
+    sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s);
     __syncthreads();
     long long sp = 0, sl = 0;
     int z = 0;
     const int64_t dbg = L.wins[q].dbg_off;
-    for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x)
-        sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z);
+    for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x) {
+        int xlo = 0, xhi = w;
+        if (stop_s) {
+            const int2 st = stop_s[ml];
+            xlo = max(0, st.x + 2);
+            xhi = min(w, st.y - 1);
+        }
+        sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z, xlo, xhi);
+    }
     cta_finish(L, q, w, ntiles, sp, sl, z, steps);
 }
 

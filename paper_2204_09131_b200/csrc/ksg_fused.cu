@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(kFusedThreads)
     }
     __syncthreads();
     const int ppc = fused_ppc_of(w, gmax);
-    sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2, OX, YS, it.i0, min(ppc, w - it.i0), eps_s);
+    // the final sorted x keys (xs) are dead after the layout build: phase A's stop indices go there
+    sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2, OX, YS, it.i0, min(ppc, w - it.i0), eps_s,
+                        reinterpret_cast<int2*>(xs));
 }
 
 template <int K1>

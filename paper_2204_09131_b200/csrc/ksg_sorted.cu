@@ -97,12 +97,14 @@ __global__ void __launch_bounds__(kSortedThreads)
                       const KsgItem* __restrict__ items) {
     const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
     __shared__ float eps_s[kSortedPts];
+    __shared__ int2 stop_s[kSortedPts];
     const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list, it.i0 = first point
     const int b = it.win;
     const int q = list[b];
     const int w = L.wins[q].w;
     const int64_t o = soff[b];
-    sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2g + o, OXg + o, YSg + o, it.i0, min(ppc, w - it.i0), eps_s);
+    sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2g + o, OXg + o, YSg + o, it.i0, min(ppc, w - it.i0), eps_s,
+                        stop_s);
 }
 
 template <int K1>

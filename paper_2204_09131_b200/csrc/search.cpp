@@ -1101,8 +1101,12 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             }
             F.offs.push_back((int64_t)batch.size());
             const auto t_ev = clk::now();
+            // kernel timing samples every profile_every-th round (event records are host time per round)
+            uint32_t fl_round = P.flags;
+            if ((fl_round & ISYCOS_F_PROFILE) && P.profile_every > 1 && (round_no % P.profile_every) != 0)
+                fl_round &= ~ISYCOS_F_PROFILE;
             Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
-                                   P.variant, DebugOut{}, sts[g], P.flags, &bs);
+                                   P.variant, DebugOut{}, sts[g], fl_round, &bs);
             const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
             eval_ms += ev_ms;
             if (!s.ok()) return s;
