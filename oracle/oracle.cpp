@@ -21,6 +21,7 @@
 //   SYCOS_BU                             Alg. 2 (Defs 5.2-5.3)
 //   noise predicate + pruning            Def 6.2, §6.2, §6.3
 //   chunks + merge                       Alg. 4 line 14
+//   iSYCOS selection (method 4, AUTO)    Alg. 3, Eqs. 4-9; readings R24-R26
 //
 // Parity status: every function is pinned by tests/test_oracle_*.py except the
 // search readings the paper leaves open (RNG, delta, h, p, T_maxIdle, tie

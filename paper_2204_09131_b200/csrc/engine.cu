@@ -299,8 +299,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             while (fused_n2 < w) fused_n2 <<= 1;
         } else if (use_sorted && w >= sorted_min_w_) {
             sorted.push_back((int32_t)i);
-            soff.push_back(spts + 4);  // 4 sentinel entries on either side of the window's region
-            spts += w + 8;
+            soff.push_back(spts + kScanB);  // kScanB sentinel entries on either side of the window's region
+            spts += w + 2 * kScanB;
             n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
             if (w > kSortedMaxW) n_mblocks += (w + kMergePts - 1) / kMergePts;
             int n2 = 1;

@@ -78,6 +78,7 @@ int tile_R(int w);                       // points per thread of the tile kernel
 constexpr int kSortedPts = 1024;         // max points per CTA of the sorted-path scan kernel (4 warps)
 constexpr int kSortedMaxW = 16384;       // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
 constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
+constexpr int kScanB = 8;                // sorted-path scan: candidates per block and side (= sentinels per end)
 constexpr int kFusedMaxW = 4096;         // fused sort+scan path (latency mode): windows up to this size
 constexpr int kFusedThreads = 512;       // threads per fused CTA (16 warps: one 256-key sort chunk each)
 

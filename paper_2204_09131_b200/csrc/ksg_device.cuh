@@ -363,11 +363,11 @@ __device__ __forceinline__ unsigned sortable(float f) {
     const unsigned u = __float_as_uint(f);
     return u ^ ((u >> 31) ? 0xffffffffu : 0x80000000u);
 }
-__device__ __forceinline__ void put_sentinels(float2* P2, int w, int t) {  // t < 8: one entry each
-    if (t < 4)
+__device__ __forceinline__ void put_sentinels(float2* P2, int w, int t) {  // t < 2 kScanB: one entry each
+    if (t < kScanB)
         P2[-1 - t] = make_float2(-kInf, 0.0f);
-    else if (t < 8)
-        P2[w + t - 4] = make_float2(kInf, 0.0f);
+    else if (t < 2 * kScanB)
+        P2[w + t - kScanB] = make_float2(kInf, 0.0f);
 }
 __device__ __forceinline__ float unsortable(unsigned s) {
     return __uint_as_float(s ^ ((s >> 31) ? 0x80000000u : 0xffffffffu));
@@ -549,7 +549,7 @@ __device__ __forceinline__ void warp_sort(T (&v)[E], int lane) {
 
 // Phase A of the sorted path for the points [wb, we) (positions relative to cta0) of one warp: exact
 // k-NN radius by outward scan in x order (a3).  Writes eps_s[ml]; adds the candidate visits to `steps`.
-// P2 must carry sentinels: P2[-4..-1] = (-inf, 0) and P2[w..w+3] = (+inf, 0) (no bounds checks).
+// P2 must carry sentinels: P2[-kScanB..-1] = (-inf, 0), P2[w..w+kScanB-1] = (+inf, 0) (no bounds checks).
 // Warp-local work queue: a lane that finishes its point takes the next one (ballot + popc), so warps do
 // not idle on their slowest lane (per-point scan lengths vary several-fold with the local density ratio).
 template <int K1>
@@ -557,7 +557,7 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                                                unsigned long long& steps, int2* stop_s = nullptr) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    constexpr int B = 4;
+    constexpr int B = kScanB;
     int mloc = wb + lane;
     bool act = mloc < we;
     int next = wb + 32;
@@ -581,7 +581,9 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
     // a block with any candidate below r_{k+1}: all four through the min/max network (exact: inserting
     // d >= r_{k+1} leaves the list unchanged), no per-candidate branches
     auto visit = [&](const float (&d)[B]) {
-        const float mn = fminf(fminf(d[0], d[1]), fminf(d[2], d[3]));
+        float mn = d[0];
+#pragma unroll
+        for (int u = 1; u < B; ++u) mn = fminf(mn, d[u]);
         if (mn < rk[K1 - 1]) {
 #pragma unroll
             for (int u = 0; u < B; ++u) topk_insert<K1>(rk, d[u]);
@@ -595,7 +597,7 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                 float d[B], far = 0.f;
 #pragma unroll
                 for (int u = 0; u < B; ++u) {
-                    const float2 c = P2[lj - u];  // P2[-4..-1] = (-inf, 0) sentinels: d = far = +inf
+                    const float2 c = P2[lj - u];  // P2[-B..-1] = (-inf, 0) sentinels: d = far = +inf
                     const float dx = xi - c.x;    // >= 0: ascending order
                     d[u] = fmaxf(dx, fabsf(yi - c.y));
                     far = dx;
@@ -609,7 +611,7 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                 float d[B], far = 0.f;
 #pragma unroll
                 for (int u = 0; u < B; ++u) {
-                    const float2 c = P2[rj + u];  // P2[w..w+3] = (+inf, 0) sentinels
+                    const float2 c = P2[rj + u];  // P2[w..w+B-1] = (+inf, 0) sentinels
                     const float dx = c.x - xi;
                     d[u] = fmaxf(dx, fabsf(yi - c.y));
                     far = dx;

@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(kFusedThreads)
     int n2 = 256;
     while (n2 < w) n2 <<= 1;
     const int maxn2 = L.fused_n2;  // shared-memory layout stride (batch maximum)
-    unsigned long long* X0 = fsm;                // maxn2 + 8 entries each: the scan layout P2 reuses one
-    unsigned long long* X1 = fsm + (maxn2 + 8);  // of them with 4 sentinels on either side
-    unsigned* Y0 = reinterpret_cast<unsigned*>(fsm + 2 * (maxn2 + 8));
+    unsigned long long* X0 = fsm;                         // maxn2 + 2 kScanB entries each: the scan layout P2
+    unsigned long long* X1 = fsm + (maxn2 + 2 * kScanB);  // reuses one, with kScanB sentinels on either side
+    unsigned* Y0 = reinterpret_cast<unsigned*>(fsm + 2 * (maxn2 + 2 * kScanB));
     unsigned* Y1 = Y0 + maxn2;
     float* eps_s = reinterpret_cast<float*>(Y1 + maxn2);  // maxn2 floats (a slice can be the whole window)
     const float* gx = L.pairs[W.pair].x + W.t0;
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(kFusedThreads)
         yd = ty;
     }
     // step 3: scan layout: P2 (x, y) in x order -> the free x buffer, OX -> the free y buffer, YS in place
-    float2* P2 = reinterpret_cast<float2*>(xd) + 4;
-    if (threadIdx.x < 8) put_sentinels(P2, w, threadIdx.x);
+    float2* P2 = reinterpret_cast<float2*>(xd) + kScanB;
+    if (threadIdx.x < 2 * kScanB) put_sentinels(P2, w, threadIdx.x);
     int32_t* OX = reinterpret_cast<int32_t*>(yd);
     float* YS = reinterpret_cast<float*>(ys);
     for (int m = threadIdx.x; m < w; m += kFusedThreads) {
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kFusedThreads)
 template <int K1>
 cudaError_t fused_k(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
                     cudaStream_t st) {
-    const size_t smem = (size_t)L.fused_n2 * 28 + 128;
+    const size_t smem = (size_t)L.fused_n2 * 28 + 32 * kScanB;
     if (L.variant == 1)
         fused_sorted_kernel<K1, true><<<n_items, kFusedThreads, smem, st>>>(L, list, items, gmax);
     else
@@ -140,7 +140,7 @@ cudaError_t fused_k(const KsgLaunch& L, const int32_t* list, const KsgItem* item
 template <int K1, bool V2>
 cudaError_t fused_attr() {
     return cudaFuncSetAttribute(fused_sorted_kernel<K1, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kFusedMaxW * 28 + 128);
+                                kFusedMaxW * 28 + 32 * kScanB);
 }
 template <int K1>
 cudaError_t fused_attr_k(const KsgLaunch&) {

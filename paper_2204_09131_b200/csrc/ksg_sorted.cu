@@ -24,7 +24,7 @@ __global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict_
     const float* gx = L.pairs[W.pair].x + W.t0;
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int64_t o = soff[b];  // the window's region has 4 spare entries on either side (scan sentinels)
-    if (s0 == 0 && threadIdx.x < 8) put_sentinels(P2 + o, w, threadIdx.x);
+    if (s0 == 0 && threadIdx.x < 2 * kScanB) put_sentinels(P2 + o, w, threadIdx.x);
     // pass 0: x with the index packed into one 64-bit word (sortable float bits << 32 | index): one
     // compare/swap per exchange, ties broken by index.  pass 1: y keys alone (32-bit).
     unsigned long long* k64 = reinterpret_cast<unsigned long long*>(sm);

@@ -12,7 +12,7 @@ template <int K1, int E, bool V2>
 __global__ void __launch_bounds__(kSmallWarps * 32)
     warp_sorted_kernel(const KsgLaunch L, const int32_t* __restrict__ list, int32_t n) {
     constexpr int N = 32 * E;
-    __shared__ __align__(16) float2 sP2[kSmallWarps][N + 8];  // 4 sentinels on either side
+    __shared__ __align__(16) float2 sP2[kSmallWarps][N + 2 * kScanB];  // kScanB sentinels on either side
     __shared__ float sYS[kSmallWarps][N];
     __shared__ int32_t sOX[kSmallWarps][N];
     __shared__ float seps[kSmallWarps][N];
@@ -34,8 +34,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     }
     warp_sort<unsigned long long, E>(vx, lane);
     warp_sort<unsigned, E>(vy, lane);
-    float2* P2 = sP2[warp] + 4;
-    if (lane < 8) put_sentinels(P2, w, lane);
+    float2* P2 = sP2[warp] + kScanB;
+    if (lane < 2 * kScanB) put_sentinels(P2, w, lane);
     int32_t* OX = sOX[warp];
     float* YS = sYS[warp];
 #pragma unroll
