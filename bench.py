@@ -249,6 +249,27 @@ def sweep_cfg3(isy, stream, reps: int):
                          "scan_steps_per_point": st["scan_steps"] / max(1, st["sorted_points"])}}
 
 
+def multi_pair(isy, stream):
+    """Third line: a multi-pair search (the cfg4s reduction of configs[3]: 8 series x 200,000, 28 pairs,
+    scales 64..4,096, TD+BU, noise on) — the regime where batches fill the GPU and the host thread pool
+    carries the per-pair state machines.  One timed step after one warm-up."""
+    import torch
+
+    wl, desc = make_workload("cfg4s")
+    dev = [torch.from_numpy(s).cuda() for s in wl.series]
+    isy.search_workload(wl, series=dev, stream=stream)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    res, st = isy.search_workload(wl, series=dev, stream=stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    return {"workload": desc, "ms_per_step": ms, "compares_per_s": compares_of(st) / (ms / 1e3),
+            "windows_per_s": st["distinct_windows"] / (ms / 1e3), "results": len(res),
+            "rounds": st["kernel"]["rounds"], "host_ms": st["kernel"]["host_ms"]}
+
+
 def noise_ablation(isy, wl, series, stream, reps: int):
     """The paper's Origin-vs-Noise protocol (Figs. 6-7) on the bench workload: the same search
     with MI-based noise pruning on and off — device time, MI evaluations consumed (TD windows / BU
@@ -476,6 +497,7 @@ def main():
         if not args.no_sweep:
             line["throughput_sweep"] = sweep_cfg3(isy, stream, max(1, args.steps // 2))
             line["noise_ablation"] = noise_ablation(isy, wl, dev_series, stream, max(1, args.steps // 2))
+            line["multi_pair_search"] = multi_pair(isy, stream)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
