@@ -126,6 +126,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_FUSED_SMALL_MIN_W")) fused_small_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -315,10 +316,17 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // latency mode: a class too sparse to fill the GPU runs a CTA per window (tile R = 1), where a warp
     // walking 32R points (brute force) or sorting and scanning them (warp-sorted) would set the latency
     // (all of a round's latency-mode windows go into one launch: per-class launches measured slower)
+    // (windows >= fused_small_min_w_ take the fused sort+scan kernel when the round is in latency mode)
     auto to_latency = [&](std::vector<int32_t>& v) {
         for (int32_t q : v) {
+            const int w = wins[q].w;
+            if (fuse && w >= fused_small_min_w_) {
+                fused.push_back(q);
+                while (fused_n2 < w) fused_n2 <<= 1;
+                continue;
+            }
             tile[2].push_back(q);
-            n_items += (wins[q].w + kTileThreads - 1) / kTileThreads;
+            n_items += (w + kTileThreads - 1) / kTileThreads;
         }
         v.clear();
     };
