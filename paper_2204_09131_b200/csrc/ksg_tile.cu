@@ -56,23 +56,7 @@ __global__ void __launch_bounds__(kTileThreads)
         ng = wpad >> 2;
         const float4* sx4 = reinterpret_cast<const float4*>(sx);
         const float4* sy4 = reinterpret_cast<const float4*>(sy);
-        if (R == 1) {
-            // latency mode (one point per thread, few warps per SM): two independent top-(k+1) lists over
-            // the even and odd candidate groups, merged at the end — two dependency chains interleave
-            float rk2[R][K1];
-#pragma unroll
-            for (int m = 0; m < K1; ++m) rk2[0][m] = kInf;
-            int g = 0;
-            for (; g + 1 < ng; g += 2) {
-                knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
-                knn_step<K1, R, false>(xi, yi, rk2, sx4[g + 1], sy4[g + 1]);
-            }
-            if (g < ng) knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
-#pragma unroll
-            for (int m = 0; m < K1; ++m) topk_insert<K1>(rk[0], rk2[0][m]);  // union of disjoint sets
-        } else {
-            for (int g = 0; g < ng; ++g) knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
-        }
+        for (int g = 0; g < ng; ++g) knn_step<K1, R, false>(xi, yi, rk, sx4[g], sy4[g]);
     } else {
         for (int jt = 0; jt < nj; ++jt) {
             const int j0 = jt * kTileJ;
