@@ -1076,6 +1076,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             std::vector<PairPtrs> table;
             batch.clear();
             Flight& F = fl[g];
+            int64_t tot = 0;
             for (auto& pw : active) {
                 if (pw->stage_bad)
                     return make_err(ISYCOS_E_RANGE, "internal: search requested window [" +
@@ -1084,17 +1085,28 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 if (pw->stage_w.empty()) continue;
                 pw->slot = (int32_t)table.size();
                 table.push_back(pw->ptrs);
-                F.offs.push_back((int64_t)batch.size());
-                for (KsgWin kw : pw->stage_w) {
-                    kw.pair = pw->slot;
-                    batch.push_back(kw);
-                }
-                F.owners.insert(F.owners.end(), pw->stage_o.begin(), pw->stage_o.end());
-                pw->stage_w.clear();
-                pw->stage_o.clear();
+                F.offs.push_back(tot);
+                tot += (int64_t)pw->stage_w.size();
                 pw->inflight += 1;
                 F.pws.push_back(pw.get());
             }
+            // each pair copies its staged requests to its slice of the batch (in parallel when large)
+            batch.resize(tot);
+            F.owners.resize(tot);
+            pool.run(tot >= 512 ? (int)F.pws.size() : 1, [&](int p) {
+                const int p0 = tot >= 512 ? p : 0, p1 = tot >= 512 ? p + 1 : (int)F.pws.size();
+                for (int q = p0; q < p1; ++q) {
+                    PairWork* pw = F.pws[q];
+                    int64_t o = F.offs[q];
+                    for (size_t i = 0; i < pw->stage_w.size(); ++i, ++o) {
+                        batch[o] = pw->stage_w[i];
+                        batch[o].pair = pw->slot;
+                        F.owners[o] = pw->stage_o[i];
+                    }
+                    pw->stage_w.clear();
+                    pw->stage_o.clear();
+                }
+            });
             if (batch.empty()) {
                 F.offs.clear();
                 continue;
