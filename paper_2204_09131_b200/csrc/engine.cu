@@ -129,6 +129,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_FUSED_SMALL_MIN_W")) fused_small_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
+    if (const char* m = std::getenv("ISYCOS_ZC_DESC")) zc_desc_ = std::atoi(m) != 0;
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
@@ -226,7 +227,9 @@ Status Engine::ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t
         int64_t c = std::max<int64_t>(bytes, S.hstage_cap * 2);
         cudaFreeHost(S.hstage);
         S.hstage = nullptr;
-        ISY_CK(cudaMallocHost(&S.hstage, c));
+        S.hstage_dev = nullptr;
+        ISY_CK(cudaHostAlloc(&S.hstage, c, cudaHostAllocMapped));  // mapped: zero-copy descriptors
+        ISY_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.hstage_dev), S.hstage, 0));
         S.hstage_cap = c;
     }
     return Status{};
@@ -433,12 +436,16 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
                 for (int i0 = 0; i0 < w; i0 += kMergePts) mb[cm++] = KsgItem{(int32_t)b, i0};
         }
     }
-    ISY_CK(cudaMemcpyAsync(S.dstage, S.hstage, total, cudaMemcpyHostToDevice, st));
+    // descriptors: small batches are read by the kernels straight from the mapped pinned staging buffer
+    // (no copy, no extra API call on the round path); big ones are copied once
+    const bool zc_desc = zc_desc_ && n <= kZeroCopyMaxRecs;
+    char* dbase = zc_desc ? S.hstage_dev : S.dstage;
+    if (!zc_desc) ISY_CK(cudaMemcpyAsync(S.dstage, S.hstage, total, cudaMemcpyHostToDevice, st));
     if (bs) bs->h2d_bytes += total;
 
     KsgLaunch L;
-    L.pairs = reinterpret_cast<const PairPtrs*>(S.dstage + off_pairs);
-    L.wins = reinterpret_cast<const KsgWin*>(S.dstage + off_wins);
+    L.pairs = reinterpret_cast<const PairPtrs*>(dbase + off_pairs);
+    L.wins = reinterpret_cast<const KsgWin*>(dbase + off_wins);
     L.psi = psi_;
     L.psiq = psiq_;
     L.lnc = lnc_;
@@ -455,8 +462,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     L.sorted_ppc = ppc;
     L.fused_n2 = fused_n2;
     L.pad3_ = 0;
-    const int32_t* dlists = reinterpret_cast<const int32_t*>(S.dstage + off_lists);
-    const KsgItem* ditems = reinterpret_cast<const KsgItem*>(S.dstage + off_items);
+    const int32_t* dlists = reinterpret_cast<const int32_t*>(dbase + off_lists);
+    const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dbase + off_items);
 
     // launches: biggest work first so the small classes fill the tail
     int n_launch = 0, n_ksg = 0;
@@ -535,30 +542,30 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         return Status{};
     };
     if (!fused.empty()) {
-        const int32_t* dfl = reinterpret_cast<const int32_t*>(S.dstage + off_flist);
-        const KsgItem* dfi = reinterpret_cast<const KsgItem*>(S.dstage + off_fitems);
+        const int32_t* dfl = reinterpret_cast<const int32_t*>(dbase + off_flist);
+        const KsgItem* dfi = reinterpret_cast<const KsgItem*>(dbase + off_fitems);
         Status r = launch(0, 1, [&](cudaStream_t sg) { return launch_fused(L, dfl, dfi, (int32_t)n_fitems, gmax, sg); });
         if (!r.ok()) return r;
     }
     for (int e = 2; e >= 0; --e) {
         if (wsorted[e].empty()) continue;
-        const int32_t* wlp = reinterpret_cast<const int32_t*>(S.dstage + off_wlist) + wlist_off[e];
+        const int32_t* wlp = reinterpret_cast<const int32_t*>(dbase + off_wlist) + wlist_off[e];
         const int32_t cnt = (int32_t)wsorted[e].size();
         Status r = launch(0, 1, [&](cudaStream_t sg) { return launch_wsorted(L, wlp, cnt, 2 << e, sg); });
         if (!r.ok()) return r;
     }
     if (!sorted.empty()) {
-        const int32_t* dsl = reinterpret_cast<const int32_t*>(S.dstage + off_slist);
-        const int64_t* dso = reinterpret_cast<const int64_t*>(S.dstage + off_soff);
-        const KsgItem* dsi = reinterpret_cast<const KsgItem*>(S.dstage + off_sitems);
+        const int32_t* dsl = reinterpret_cast<const int32_t*>(dbase + off_slist);
+        const int64_t* dso = reinterpret_cast<const int64_t*>(dbase + off_soff);
+        const KsgItem* dsi = reinterpret_cast<const KsgItem*>(dbase + off_sitems);
         float2* P2 = reinterpret_cast<float2*>(S.sscratch);
         int32_t* OX = reinterpret_cast<int32_t*>(S.sscratch + spts * 8);
         float* YS = reinterpret_cast<float*>(S.sscratch + spts * 12);
         float* TX = reinterpret_cast<float*>(S.sscratch + spts * 16);
         int32_t* TI = reinterpret_cast<int32_t*>(S.sscratch + spts * 20);
         float* TY = reinterpret_cast<float*>(S.sscratch + spts * 24);
-        const KsgItem* dsg = reinterpret_cast<const KsgItem*>(S.dstage + off_segs);
-        const KsgItem* dmb = reinterpret_cast<const KsgItem*>(S.dstage + off_mblk);
+        const KsgItem* dsg = reinterpret_cast<const KsgItem*>(dbase + off_segs);
+        const KsgItem* dmb = reinterpret_cast<const KsgItem*>(dbase + off_mblk);
         Status r = launch(0, n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
                                  W2, dsi, (int32_t)n_sitems, sg);
