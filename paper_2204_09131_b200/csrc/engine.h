@@ -173,8 +173,7 @@ private:
         int64_t acc_cap = 0;
         char* dstage = nullptr;      // packed [pairs | wins | lists | items]
         int64_t dstage_cap = 0;
-        char* hstage = nullptr;      // pinned (mapped) mirror of dstage
-        char* hstage_dev = nullptr;  // device alias of hstage (zero-copy descriptors)
+        char* hstage = nullptr;      // pinned mirror of dstage
         int64_t hstage_cap = 0;
         KsgRec* drec = nullptr;      // device alias of hrec
         KsgRec* hrec = nullptr;      // mapped pinned (kernels write records here)
@@ -219,7 +218,6 @@ private:
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points
     int32_t sorted_min_w_ = 257;
     int64_t aux_min_windows_ = 256;  // batches with more windows fork size classes onto aux streams
-    bool zc_desc_ = false;           // small batches: kernels read descriptors from mapped host memory
     int32_t wsorted_min_w_ = 65;     // small windows w in [this, 256]: warp-per-window sorted kernel
     int32_t fused_small_min_w_ = 1 << 30;  // latency mode: small windows >= this go to the fused kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
