@@ -49,6 +49,32 @@ __device__ __host__ __forceinline__ int fused_ppc_of(int w, int gmax) {
     return (ppc + 31) & ~31;
 }
 
+// Step 1 of the fused sort: warp c sorts keys [32E c, 32E (c+1)) (blocked, E per lane) of x (with the
+// window index) and of y; the raw y also goes to `rawy` for the layout build.
+template <int E>
+__device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const float* __restrict__ gy, int w, int n2,
+                                           unsigned long long* X0, unsigned* Y0, float* rawy, int warp, int lane) {
+    for (int c = warp; c * 32 * E < n2; c += kFusedThreads / 32) {
+        unsigned long long vx[E];
+        unsigned vy[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = c * 32 * E + lane * E + e;
+            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
+            const float yv = i < w ? gy[i] : 0.0f;
+            vy[e] = i < w ? sortable(yv) : ~0u;
+            if (i < w) rawy[i] = yv;  // raw y kept in the (not yet used) eps buffer for the layout build
+        }
+        warp_sort<unsigned long long, E>(vx, lane);
+        warp_sort<unsigned, E>(vy, lane);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            X0[c * 32 * E + lane * E + e] = vx[e];
+            Y0[c * 32 * E + lane * E + e] = vy[e];
+        }
+    }
+}
+
 template <int K1, bool V2>
 __global__ void __launch_bounds__(kFusedThreads)
     fused_sorted_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const KsgItem* __restrict__ items,
@@ -70,24 +96,9 @@ __global__ void __launch_bounds__(kFusedThreads)
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // a2 + sort, step 1: each warp sorts 256-key chunks in registers (8 consecutive keys per lane)
-    for (int c = warp; c * 256 < n2; c += kFusedThreads / 32) {
-        unsigned long long vx[8];
-        unsigned vy[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int i = c * 256 + lane * 8 + e;
-            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
-            vy[e] = i < w ? sortable(gy[i]) : ~0u;
-        }
-        warp_sort<unsigned long long, 8>(vx, lane);
-        warp_sort<unsigned, 8>(vy, lane);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            X0[c * 256 + lane * 8 + e] = vx[e];
-            Y0[c * 256 + lane * 8 + e] = vy[e];
-        }
-    }
+    // a2 + sort, step 1: each warp sorts 256-key chunks in registers (8 consecutive keys per lane;
+    // smaller chunks with more merge levels measured slower)
+    chunk_sort<8>(gx, gy, w, n2, X0, Y0, eps_s, warp, lane);
     __syncthreads();
     // step 2: merge-path levels 256 -> n2 (ping-pong)
     unsigned long long* xs = X0;
@@ -113,7 +124,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     for (int m = threadIdx.x; m < w; m += kFusedThreads) {
         const unsigned long long v = xs[m];
         const int32_t idx = (int32_t)(v & 0xffffffffu);
-        P2[m] = make_float2(unsortable((unsigned)(v >> 32)), gy[idx]);
+        P2[m] = make_float2(unsortable((unsigned)(v >> 32)), eps_s[idx]);
         OX[m] = idx;
         YS[m] = unsortable(ys[m]);
     }
