@@ -547,6 +547,60 @@ __device__ __forceinline__ void warp_sort(T (&v)[E], int lane) {
 }
 
 
+// merge adjacent sorted runs of length r (src) into runs of 2r (dst); thread t < n2/8 writes outputs
+// [8t, 8t+8).  Merge path: the co-rank i (outputs taken from run A) is found by binary search, A first
+// on ties.
+template <typename T>
+__device__ __forceinline__ void merge_level(const T* __restrict__ src, T* __restrict__ dst, int n2, int r) {
+    const int t = threadIdx.x;
+    if (t * 8 < n2) {
+        const int g = t * 8;
+        const int base = (g / (2 * r)) * (2 * r);
+        const T* A = src + base;
+        const T* Bv = src + base + r;
+        const int o = g - base;
+        int lo = max(0, o - r), hi = min(o, r);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (A[mid] <= Bv[o - mid - 1]) lo = mid + 1; else hi = mid;
+        }
+        int ia = lo, ib = o - lo;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const bool takeA = ib >= r || (ia < r && A[ia] <= Bv[ib]);
+            dst[base + o + e] = takeA ? A[ia] : Bv[ib];
+            ia += takeA ? 1 : 0;
+            ib += takeA ? 0 : 1;
+        }
+    }
+}
+
+// Step 1 of the fused sort: warp c sorts keys [32E c, 32E (c+1)) (blocked, E per lane) of x (with the
+// window index) and of y; the raw y also goes to `rawy` for the layout build.
+template <int E>
+__device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const float* __restrict__ gy, int w, int n2,
+                                           unsigned long long* X0, unsigned* Y0, float* rawy, int warp, int lane) {
+    for (int c = warp; c * 32 * E < n2; c += (int)(blockDim.x >> 5)) {
+        unsigned long long vx[E];
+        unsigned vy[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = c * 32 * E + lane * E + e;
+            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
+            const float yv = i < w ? gy[i] : 0.0f;
+            vy[e] = i < w ? sortable(yv) : ~0u;
+            if (rawy && i < w) rawy[i] = yv;  // raw y for the layout build (optional)
+        }
+        warp_sort<unsigned long long, E>(vx, lane);
+        warp_sort<unsigned, E>(vy, lane);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            X0[c * 32 * E + lane * E + e] = vx[e];
+            Y0[c * 32 * E + lane * E + e] = vy[e];
+        }
+    }
+}
+
 // Phase A of the sorted path for the points [wb, we) (positions relative to cta0) of one warp: exact
 // k-NN radius by outward scan in x order (a3).  Writes eps_s[ml]; adds the candidate visits to `steps`.
 // P2 must carry sentinels: P2[-kScanB..-1] = (-inf, 0), P2[w..w+kScanB-1] = (+inf, 0) (no bounds checks).

@@ -12,34 +12,6 @@ namespace {
 // memory double the run length up to n2 (next power of two >= w).  x keys carry the window index in
 // the low 32 bits (sortable x bits << 32 | index: unique keys, ties of x broken by index); y keys are
 // the sortable y bits alone.
-// merge adjacent sorted runs of length r (src) into runs of 2r (dst); thread t < n2/8 writes outputs
-// [8t, 8t+8).  Merge path: the co-rank i (outputs taken from run A) is found by binary search, A first
-// on ties.
-template <typename T>
-__device__ __forceinline__ void merge_level(const T* __restrict__ src, T* __restrict__ dst, int n2, int r) {
-    const int t = threadIdx.x;
-    if (t * 8 < n2) {
-        const int g = t * 8;
-        const int base = (g / (2 * r)) * (2 * r);
-        const T* A = src + base;
-        const T* Bv = src + base + r;
-        const int o = g - base;
-        int lo = max(0, o - r), hi = min(o, r);
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (A[mid] <= Bv[o - mid - 1]) lo = mid + 1; else hi = mid;
-        }
-        int ia = lo, ib = o - lo;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const bool takeA = ib >= r || (ia < r && A[ia] <= Bv[ib]);
-            dst[base + o + e] = takeA ? A[ia] : Bv[ib];
-            ia += takeA ? 1 : 0;
-            ib += takeA ? 0 : 1;
-        }
-    }
-}
-
 // fused items: {list position, slice start}; a window of w points has slices of fused_ppc(w, gmax) points
 __device__ __host__ __forceinline__ int fused_ppc_of(int w, int gmax) {
     int g = (w + kFusedThreads - 1) / kFusedThreads;  // at most one point per thread per slice ...
@@ -47,32 +19,6 @@ __device__ __host__ __forceinline__ int fused_ppc_of(int w, int gmax) {
     g = g < 1 ? 1 : g;
     const int ppc = (w + g - 1) / g;
     return (ppc + 31) & ~31;
-}
-
-// Step 1 of the fused sort: warp c sorts keys [32E c, 32E (c+1)) (blocked, E per lane) of x (with the
-// window index) and of y; the raw y also goes to `rawy` for the layout build.
-template <int E>
-__device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const float* __restrict__ gy, int w, int n2,
-                                           unsigned long long* X0, unsigned* Y0, float* rawy, int warp, int lane) {
-    for (int c = warp; c * 32 * E < n2; c += kFusedThreads / 32) {
-        unsigned long long vx[E];
-        unsigned vy[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const int i = c * 32 * E + lane * E + e;
-            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
-            const float yv = i < w ? gy[i] : 0.0f;
-            vy[e] = i < w ? sortable(yv) : ~0u;
-            if (i < w) rawy[i] = yv;  // raw y kept in the (not yet used) eps buffer for the layout build
-        }
-        warp_sort<unsigned long long, E>(vx, lane);
-        warp_sort<unsigned, E>(vy, lane);
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            X0[c * 32 * E + lane * E + e] = vx[e];
-            Y0[c * 32 * E + lane * E + e] = vy[e];
-        }
-    }
 }
 
 template <int K1, bool V2>

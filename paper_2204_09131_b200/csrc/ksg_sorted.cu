@@ -5,7 +5,7 @@
 namespace isy {
 namespace {
 
-__global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
                                    const int64_t* __restrict__ soff, const KsgItem* __restrict__ segs,
                                    float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
                                    float* __restrict__ TX, int32_t* __restrict__ TI, float* __restrict__ TY,
@@ -25,6 +25,39 @@ __global__ void sort_window_kernel(const KsgLaunch L, const int32_t* __restrict_
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int64_t o = soff[b];  // the window's region has 4 spare entries on either side (scan sentinels)
     if (s0 == 0 && threadIdx.x < 2 * kScanB) put_sentinels(P2 + o, w, threadIdx.x);
+    if (whole && n2 >= 256 && n2 <= kFusedMaxW) {
+        // windows up to 4,096: register chunk sorts (256 keys per warp) + merge-path levels in SMEM, x and
+        // y side by side (the fused kernel's sort) instead of the SMEM-bandwidth-bound bitonic below
+        unsigned long long* X0 = reinterpret_cast<unsigned long long*>(sm);
+        unsigned long long* X1 = X0 + n2;
+        unsigned* Y0 = reinterpret_cast<unsigned*>(X1 + n2);
+        unsigned* Y1 = Y0 + n2;
+        chunk_sort<8>(gx, gy, w, n2, X0, Y0, nullptr, threadIdx.x >> 5, threadIdx.x & 31);
+        __syncthreads();
+        unsigned long long* xs = X0;
+        unsigned long long* xd = X1;
+        unsigned* ys = Y0;
+        unsigned* yd = Y1;
+        for (int r = 256; r < n2; r <<= 1) {
+            merge_level(xs, xd, n2, r);
+            merge_level(ys, yd, n2, r);
+            __syncthreads();
+            unsigned long long* tx = xs;
+            xs = xd;
+            xd = tx;
+            unsigned* ty = ys;
+            ys = yd;
+            yd = ty;
+        }
+        for (int m = threadIdx.x; m < w; m += blockDim.x) {
+            const unsigned long long v = xs[m];
+            const int32_t idx = (int32_t)(v & 0xffffffffu);
+            P2[o + m] = make_float2(unsortable((unsigned)(v >> 32)), gy[idx]);
+            OX[o + m] = idx;
+            YS[o + m] = unsortable(ys[m]);
+        }
+        return;
+    }
     // pass 0: x with the index packed into one 64-bit word (sortable float bits << 32 | index): one
     // compare/swap per exchange, ties broken by index.  pass 1: y keys alone (32-bit).
     unsigned long long* k64 = reinterpret_cast<unsigned long long*>(sm);
@@ -127,12 +160,13 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSortedMaxW * 8);
+                                             std::max(kSortedMaxW * 8, kFusedMaxW * 24));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int threads = std::min(1024, std::max(64, W2 / 2));
-    sort_window_kernel<<<n_segs, threads, (size_t)W2 * 8, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
+    const int threads = std::min(1024, std::max(64, W2 / 2));  // >= n2 / 8 for every segment (merge levels)
+    const size_t smem = std::max<size_t>((size_t)W2 * 8, (size_t)std::min(W2, kFusedMaxW) * 24);
+    sort_window_kernel<<<n_segs, threads, smem, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (n_mblocks > 0) {
