@@ -76,7 +76,7 @@ constexpr int kTileJ = 4096;             // j-tile (points) staged per cp.async.
 int small_class_R(int w);                // 1,2,4,8 for w <= 256; 0 => tile kernel
 int tile_R(int w);                       // points per thread of the tile kernel
 constexpr int kSortedPts = 1024;         // max points per CTA of the sorted-path scan kernel (4 warps)
-constexpr int kSortedMaxW = 16384;       // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
+constexpr int kSortedMaxW = 8192;        // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
 constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
 constexpr int kScanB = 8;                // sorted-path scan: candidates per block and side (= sentinels per end)
 constexpr int kFusedMaxW = 4096;         // fused sort+scan path (latency mode): windows up to this size

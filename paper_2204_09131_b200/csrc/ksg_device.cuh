@@ -579,14 +579,15 @@ __device__ __forceinline__ void merge_level(const T* __restrict__ src, T* __rest
 // window index) and of y; the raw y also goes to `rawy` for the layout build.
 template <int E>
 __device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const float* __restrict__ gy, int w, int n2,
-                                           unsigned long long* X0, unsigned* Y0, float* rawy, int warp, int lane) {
+                                           unsigned long long* X0, unsigned* Y0, float* rawy, int warp, int lane,
+                                           int ioff = 0) {
     for (int c = warp; c * 32 * E < n2; c += (int)(blockDim.x >> 5)) {
         unsigned long long vx[E];
         unsigned vy[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const int i = c * 32 * E + lane * E + e;
-            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)i : ~0ull;
+            vx[e] = i < w ? ((unsigned long long)sortable(gx[i]) << 32) | (unsigned)(i + ioff) : ~0ull;
             const float yv = i < w ? gy[i] : 0.0f;
             vy[e] = i < w ? sortable(yv) : ~0u;
             if (rawy && i < w) rawy[i] = yv;  // raw y for the layout build (optional)

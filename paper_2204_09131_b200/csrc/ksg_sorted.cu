@@ -25,36 +25,52 @@ __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, co
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int64_t o = soff[b];  // the window's region has 4 spare entries on either side (scan sentinels)
     if (s0 == 0 && threadIdx.x < 2 * kScanB) put_sentinels(P2 + o, w, threadIdx.x);
-    if (whole && n2 >= 256 && n2 <= kFusedMaxW) {
-        // windows up to 4,096: register chunk sorts (256 keys per warp) + merge-path levels in SMEM, x and
-        // y side by side (the fused kernel's sort) instead of the SMEM-bandwidth-bound bitonic below
+    if (n2 >= 256) {
+        // register chunk sorts (256 keys per warp) + merge-path levels in SMEM (the fused kernel's sort, ~2x
+        // the SMEM-bandwidth-bound bitonic below).  x (with the window index) is merged and written out
+        // first, then y is merged through the freed x buffers: 20 n2 bytes of SMEM.
         unsigned long long* X0 = reinterpret_cast<unsigned long long*>(sm);
         unsigned long long* X1 = X0 + n2;
         unsigned* Y0 = reinterpret_cast<unsigned*>(X1 + n2);
-        unsigned* Y1 = Y0 + n2;
-        chunk_sort<8>(gx, gy, w, n2, X0, Y0, nullptr, threadIdx.x >> 5, threadIdx.x & 31);
+        chunk_sort<8>(gx + s0, gy + s0, len, n2, X0, Y0, nullptr, threadIdx.x >> 5, threadIdx.x & 31, s0);
         __syncthreads();
         unsigned long long* xs = X0;
         unsigned long long* xd = X1;
-        unsigned* ys = Y0;
-        unsigned* yd = Y1;
         for (int r = 256; r < n2; r <<= 1) {
             merge_level(xs, xd, n2, r);
-            merge_level(ys, yd, n2, r);
             __syncthreads();
             unsigned long long* tx = xs;
             xs = xd;
             xd = tx;
+        }
+        for (int m = threadIdx.x; m < len; m += blockDim.x) {
+            const unsigned long long v = xs[m];
+            const float xv = unsortable((unsigned)(v >> 32));
+            const int32_t idx = (int32_t)(v & 0xffffffffu);
+            if (whole) {
+                P2[o + m] = make_float2(xv, gy[idx]);
+                OX[o + m] = idx;
+            } else {
+                TX[o + s0 + m] = xv;
+                TI[o + s0 + m] = idx;
+            }
+        }
+        __syncthreads();
+        unsigned* ys = Y0;
+        unsigned* yd = reinterpret_cast<unsigned*>(X0);  // x buffers are free now
+        for (int r = 256; r < n2; r <<= 1) {
+            merge_level(ys, yd, n2, r);
+            __syncthreads();
             unsigned* ty = ys;
             ys = yd;
             yd = ty;
         }
-        for (int m = threadIdx.x; m < w; m += blockDim.x) {
-            const unsigned long long v = xs[m];
-            const int32_t idx = (int32_t)(v & 0xffffffffu);
-            P2[o + m] = make_float2(unsortable((unsigned)(v >> 32)), gy[idx]);
-            OX[o + m] = idx;
-            YS[o + m] = unsortable(ys[m]);
+        for (int m = threadIdx.x; m < len; m += blockDim.x) {
+            const float yv = unsortable(ys[m]);
+            if (whole)
+                YS[o + m] = yv;
+            else
+                TY[o + s0 + m] = yv;
         }
         return;
     }
@@ -160,12 +176,12 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             std::max(kSortedMaxW * 8, kFusedMaxW * 24));
+                                             kSortedMaxW * 20);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const int threads = std::min(1024, std::max(64, W2 / 2));  // >= n2 / 8 for every segment (merge levels)
-    const size_t smem = std::max<size_t>((size_t)W2 * 8, (size_t)std::min(W2, kFusedMaxW) * 24);
+    const size_t smem = (size_t)W2 * 20;  // chunk + merge sort (bitonic for n2 < 256 needs 8 n2)
     sort_window_kernel<<<n_segs, threads, smem, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

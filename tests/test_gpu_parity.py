@@ -178,12 +178,12 @@ def test_errors(isy):
 
 
 def test_sorted_path_segment_boundaries(isy, orc):
-    """Windows at the sorted path's segment boundary (16384 = one SMEM sort; 16385+ = runs + rank merge),
+    """Windows at the sorted path's segment boundary (8,192 = one SMEM sort; 8,193+ = runs + rank merge),
     with heavy x ties (integer-rounded x) so the run merge must order equal keys consistently."""
     wl = datagen.cfg2(n=60_000)
     x, y = wl.series
     xr = np.round(x * 2).astype(np.float32)
-    W = [(100, 100 + 16384), (7, 7 + 16385), (30_001, 30_001 + 20_001)]
+    W = [(100, 100 + 16384), (7, 7 + 16385), (30_001, 30_001 + 20_001), (50, 50 + 8192), (3, 3 + 8193)]
     check_windows(isy, orc, x, y, W, 4, debug=True, label="segments")
     check_windows(isy, orc, xr, y, W[1:], 3, debug=True, label="segments ties")
 
