@@ -165,7 +165,11 @@ def issue(path, key, name_re=".*", dst="profiles/issue.json"):
         if len(r) <= ix["Metric Value"] or not re.search(name_re, r[ix["Kernel Name"]]):
             continue
         d = per.setdefault(r[ix["ID"]], {})
-        d[r[ix["Metric Name"]]] = r[ix["Metric Value"]].replace(",", "")
+        val = r[ix["Metric Value"]].replace(",", "")
+        if r[ix["Metric Name"]] == "Duration":  # normalise to us
+            sc = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+            val = str(float(val) * sc.get(r[ix["Metric Unit"]], 1.0))
+        d[r[ix["Metric Name"]]] = val
     tw = busy = lanes = 0.0
     n = 0
     for d in per.values():
