@@ -126,6 +126,8 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_SORTED_PPC"))
+        sorted_ppc_ = std::max(128, std::min(kSortedPts, std::atoi(m)));
     if (const char* m = std::getenv("ISYCOS_FUSED_SMALL_MIN_W")) fused_small_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
@@ -336,7 +338,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         if (!wsorted[e].empty() && (int64_t)wsorted[e].size() < lat_windows_) to_latency(wsorted[e]);
     // sorted scan: 1024 points per CTA when the batch fills the GPU (better lane balance in the per-warp
     // work queues), else 256 (more CTAs per window: latency-bound rounds)
-    const int ppc = spts >= (int64_t)148 * 8 * 1024 ? 1024 : 256;
+    const int ppc = spts >= (int64_t)148 * 8 * 1024 ? sorted_ppc_ : 256;
     for (int32_t q : sorted) n_sitems += (wins[q].w + ppc - 1) / ppc;
     // fused: split windows into up to ceil(w / 512) slices while the batch has fewer than 2 CTAs per SM
     const int gmax = std::max<int>(1, (int)(2 * 148 / std::max<size_t>(1, fused.size())));

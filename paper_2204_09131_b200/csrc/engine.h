@@ -219,6 +219,7 @@ private:
     int32_t sorted_min_w_ = 257;
     int64_t aux_min_windows_ = 256;  // batches with more windows fork size classes onto aux streams
     int32_t wsorted_min_w_ = 65;     // small windows w in [this, 256]: warp-per-window sorted kernel
+    int32_t sorted_ppc_ = kSortedPts;  // throughput scan: points per CTA
     int32_t fused_small_min_w_ = 1 << 30;  // latency mode: small windows >= this go to the fused kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
 };
