@@ -180,7 +180,9 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int threads = std::min(1024, std::max(64, W2 / 2));  // >= n2 / 8 for every segment (merge levels)
+    // one thread per 8 keys (= one merge-path output run; chunk sorts are 256 keys per warp): smaller CTAs
+    // for small segments keep every warp busy and let more CTAs share an SM
+    const int threads = std::min(1024, std::max(64, W2 / 8));
     const size_t smem = (size_t)W2 * 20;  // chunk + merge sort (bitonic for n2 < 256 needs 8 n2)
     sort_window_kernel<<<n_segs, threads, smem, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
     cudaError_t e = cudaGetLastError();
