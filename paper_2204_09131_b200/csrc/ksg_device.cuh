@@ -565,12 +565,20 @@ __device__ __forceinline__ void merge_level(const T* __restrict__ src, T* __rest
             if (A[mid] <= Bv[o - mid - 1]) lo = mid + 1; else hi = mid;
         }
         int ia = lo, ib = o - lo;
+        // the heads of both runs stay in registers: one SMEM load per output instead of two
+        T a = ia < r ? A[ia] : T(0);
+        T bv = ib < r ? Bv[ib] : T(0);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const bool takeA = ib >= r || (ia < r && A[ia] <= Bv[ib]);
-            dst[base + o + e] = takeA ? A[ia] : Bv[ib];
-            ia += takeA ? 1 : 0;
-            ib += takeA ? 0 : 1;
+            const bool takeA = ib >= r || (ia < r && a <= bv);
+            dst[base + o + e] = takeA ? a : bv;
+            if (takeA) {
+                ++ia;
+                if (ia < r) a = A[ia];
+            } else {
+                ++ib;
+                if (ib < r) bv = Bv[ib];
+            }
         }
     }
 }
