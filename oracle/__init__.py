@@ -55,6 +55,7 @@ class OStats(C.Structure):
 
 MIFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_double),
                    C.POINTER(C.c_double), C.POINTER(C.c_double))
+DRAWFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64)
 
 _lib = None
 
@@ -78,6 +79,8 @@ def lib():
                                     C.POINTER(OStats)]
         L.oracle_search_mock.argtypes = [MIFN, C.c_void_p, C.c_int64, C.POINTER(OParams), C.c_void_p,
                                          C.c_int64, C.POINTER(C.c_int64), C.POINTER(OStats)]
+        L.oracle_search_mock_draws.argtypes = [MIFN, DRAWFN, C.c_void_p, C.c_int64, C.POINTER(OParams),
+                                               C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(OStats)]
         L.oracle_point.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                    C.c_void_p, C.c_void_p]
         L.oracle_point_psi_q.restype = C.c_int64
@@ -218,6 +221,35 @@ def search_mock(fn, n: int, params: OParams, cap: int = 1 << 14):
                                   C.byref(count), C.byref(st))
     if rc != 0:
         raise ValueError(f"oracle_search_mock rc={rc}")
+    return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS + STAT_FIELDS_F}, calls
+
+
+def search_mock_draws(fn, draws, n: int, params: OParams, cap: int = 1 << 14):
+    """search_mock with the LAHC history-index draws (Alg. 2 line 11) passed in as inputs: draws is a
+    dict {climb start lo: [r_0, r_1, ...]} (one entry per iteration with a non-empty neighbourhood) or a
+    list used for every climb.  Asking for a draw beyond the list aborts the search (ValueError)."""
+    calls = []
+    asked = []
+
+    def cb(ctx, t0, t1, mi, h, nmi):
+        calls.append((t0, t1))
+        a, b, c = fn(t0, t1)
+        mi[0], h[0], nmi[0] = a, b, c
+        return 0
+
+    def dcb(ctx, lo, it):
+        asked.append((lo, it))
+        seq = draws.get(lo, []) if isinstance(draws, dict) else draws
+        return seq[it] if it < len(seq) else -1
+
+    cfn, dfn = MIFN(cb), DRAWFN(dcb)
+    out = (OResult * cap)()
+    count = C.c_int64(0)
+    st = OStats()
+    rc = lib().oracle_search_mock_draws(cfn, dfn, None, n, C.byref(params), C.cast(out, C.c_void_p), cap,
+                                        C.byref(count), C.byref(st))
+    if rc != 0:
+        raise ValueError(f"oracle_search_mock_draws rc={rc} (draws asked: {asked[-3:]})")
     return _results(out, count.value), {f: getattr(st, f) for f in STAT_FIELDS + STAT_FIELDS_F}, calls
 
 

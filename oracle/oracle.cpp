@@ -261,6 +261,10 @@ struct OStats {
 
 namespace {
 
+// LAHC history index draw (Alg. 2 line 11 "random.get(L_h)"): tests may pass the draws in as inputs
+// (called with the climb start lo and the iteration number; a value outside [0, h) aborts the search).
+using Draw = std::function<int(int64_t lo, int64_t it)>;
+
 struct Searcher {
     const OParams& P;
     Provider provider;
@@ -268,6 +272,7 @@ struct Searcher {
     OStats* st;
     std::map<std::pair<int64_t, int64_t>, Eval> memo;   // distinct windows consumed
     int err = 0;
+    Draw draw;                                           // null: the SplitMix64 stream (reading R14)
 
     Searcher(const OParams& p, Provider prov, int32_t id, OStats* s)
         : P(p), provider(std::move(prov)), pair_id(id), st(s) {}
@@ -379,6 +384,7 @@ struct Searcher {
             double Iw = I(t0, t1).mi;                                       // l.3
             std::vector<double> L(P.h, Iw);                                 // l.4
             int idle = 0;                                                   // l.5
+            int64_t it = 0;
             int streak[2] = {0, 0};
             bool pruned[2] = {false, false};                                // 0 LEFT, 1 RIGHT
             Rng rng{P.seed ^ ((uint64_t)(uint32_t)pair_id * 0x9E3779B97F4A7C15ull) ^
@@ -420,6 +426,11 @@ struct Searcher {
                     }
                 }
                 int r = (int)((rng.next() >> 32) % (uint64_t)P.h);          // l.11 random get
+                if (draw) {
+                    r = draw(lo, it);
+                    if (r < 0 || r >= P.h) { if (err == 0) err = -1; return; }
+                }
+                it += 1;
                 double Ih = L[r];
                 if (bI > Ih || bI > Iw) {                                   // l.12 (strict, G4)
                     t0 = bt0; t1 = bt1; Iw = bI; idle = 0;                  // l.13-14
@@ -472,7 +483,7 @@ std::vector<OResult> merge(std::vector<OResult> all) {
 }
 
 int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats* st,
-             std::vector<OResult>& out);
+             std::vector<OResult>& out, Draw draw = nullptr);
 
 void add_stats(OStats* a, const OStats& b) {
     a->td_windows += b.td_windows; a->td_noise_checks += b.td_noise_checks; a->td_skips += b.td_skips;
@@ -553,9 +564,10 @@ int run_auto(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats
 }
 
 int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats* st,
-             std::vector<OResult>& out) {
+             std::vector<OResult>& out, Draw draw) {
     if (P.method == 4) return run_auto(P, prov, pair_id, n, st, out);
     Searcher S(P, std::move(prov), pair_id, st);
+    S.draw = std::move(draw);
     auto chunks = chunk_plan(n, P.n_chunks < 1 ? 1 : P.n_chunks, P.s_max);
     for (int m = 1; m <= 2; ++m) {
         if (!(P.method & m)) continue;
@@ -563,6 +575,7 @@ int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats
         for (auto [lo, hi] : chunks) {
             std::vector<OResult> R;
             if (m == 1) S.td(lo, hi, R); else S.bu(lo, hi, R);
+            if (S.err) return S.err;
             all.insert(all.end(), R.begin(), R.end());
         }
         auto merged = merge(all);
@@ -685,6 +698,26 @@ int oracle_search_mock(oracle_mi_fn fn, void* ctx, int64_t n, const OParams* P, 
     Provider prov = [&](int64_t t0, int64_t t1, Eval* e) { return fn(ctx, t0, t1, &e->mi, &e->h, &e->nmi); };
     std::vector<OResult> res;
     int rc = run_pair(*P, prov, 0, n, st, res);
+    *count = (int64_t)res.size();
+    int64_t m = std::min<int64_t>(cap, (int64_t)res.size());
+    for (int64_t i = 0; i < m; ++i) out[i] = res[i];
+    if (rc) return rc;
+    return (int64_t)res.size() > cap ? -4 : 0;
+}
+
+// The mock search with the LAHC history draws passed in as inputs (tests: hand-traced Alg. 2 runs).
+typedef int (*oracle_draw_fn)(void* ctx, int64_t lo, int64_t it);
+
+int oracle_search_mock_draws(oracle_mi_fn fn, oracle_draw_fn dfn, void* ctx, int64_t n, const OParams* P,
+                             OResult* out, int64_t cap, int64_t* count, OStats* stats) {
+    if (!fn || !dfn || !P || !count) return -1;
+    OStats local{};
+    OStats* st = stats ? stats : &local;
+    std::memset(st, 0, sizeof(OStats));
+    Provider prov = [&](int64_t t0, int64_t t1, Eval* e) { return fn(ctx, t0, t1, &e->mi, &e->h, &e->nmi); };
+    Draw draw = [&](int64_t lo, int64_t it) { return dfn(ctx, lo, it); };
+    std::vector<OResult> res;
+    int rc = run_pair(*P, prov, 0, n, st, res, draw);
     *count = (int64_t)res.size();
     int64_t m = std::min<int64_t>(cap, (int64_t)res.size());
     for (int64_t i = 0; i < m; ++i) out[i] = res[i];

@@ -10,6 +10,8 @@ import pytest
 
 import datagen
 
+pytestmark = pytest.mark.timeout(300)  # a broken LAHC history can climb forever
+
 
 def P(orc, **kw):
     base = dict(k=2, method=1, noise=0, s_min=16, s_max=16, sigma=0.2, tau_ratio=0.25, p=3, h=5,
@@ -160,6 +162,97 @@ def test_bu_noise_prunes_right_p1(orc):
     assert st1["bu_neighbors"] < st0["bu_neighbors"]
 
 
+# ------------------------------------------------------------------ LAHC acceptance + history (Alg. 2 l.11-21)
+# Hand traces of Alg. 2 with the history draws r of line 11 passed in as inputs (the paper's
+# "random policy"; tests may fix random numbers).  Landscapes live on the line t0 = lo: windows
+# starting elsewhere score -1, so the best neighbour of (0, t1) is the better of (0, t1 - d), (0, t1 + d).
+def _line(f, good):
+    def fn(t0, t1):
+        if t0 != 0:
+            return (-1.0, 1.0, 0.0)
+        return (f[t1], 1.0, 1.0 if t1 == good else 0.0)
+    return fn
+
+
+def _bu(orc, **kw):
+    base = dict(method=2, s_min=32, s_max=200, delta_bu=10, k=4, t_max_idle=0, h=2)
+    base.update(kw)
+    return P(orc, **base)
+
+
+def test_lahc_late_acceptance_crosses_a_dip(orc):
+    """l.12 "I_best > I_h or I_best > I_w": the history lets the climb accept a worse window and cross a dip.
+    f(t1) = 0.1, 0.3, 0.5, 0.4, 0.9, 0.2, 0.2 at t1 = 32..92; L = [0.1, 0.1]; draws r = 0, 0, 1, 0, 1.
+      it1 r=0: best (0,42) 0.3 > L0 0.1: accept; I_w 0.3 > I_h -> L0 = 0.3
+      it2 r=0: best (0,52) 0.5 > 0.3: accept; L0 = 0.5
+      it3 r=1: best (0,62) 0.4 (the dip) > L1 0.1: accept although 0.4 < I_w 0.5; L1 = 0.4
+      it4 r=0: best (0,72) 0.9 > 0.5: accept; L0 = 0.9
+      it5 r=1: best (0,62) 0.4, not > L1 0.4, not > 0.9: reject; idle 1 > T_maxIdle 0: stop at (0,72).
+    With "and" (or plain hill climbing, I_best > I_w only) it3 rejects and the climb stops on the 0.5 peak
+    (0,52), whose normalized MI is below sigma: no result."""
+    f = {32: 0.1, 42: 0.3, 52: 0.5, 62: 0.4, 72: 0.9, 82: 0.2, 92: 0.2}
+    res, st, _ = orc.search_mock_draws(_line(f, 72), {0: [0, 0, 1, 0, 1]}, 100, _bu(orc))
+    assert [(r[2], r[3]) for r in res] == [(0, 72)]
+    assert st["bu_iterations"] == 5 and st["bu_climbs"] == 1   # lo = 72 next: 72 + 32 > 100 (S:407)
+
+
+def test_lahc_accepts_above_current_below_history(orc):
+    """The "or I_best > I_w" half: after the dip, the way back up is better than the current window but not
+    than the history entry drawn.  Same trace to it3 (L = [0.5, 0.4], w = (0,62) 0.4), then
+      it4 r=0: best (0,52) 0.5: not > L0 0.5, but > I_w 0.4: accept; I_w 0.5 not > I_h 0.5: no update
+      it5 r=1: best (0,62) 0.4: reject; stop at (0,52).
+    Dropping the I_w test rejects at it4 and stops at (0,62) (normalized MI below sigma): no result."""
+    f = {32: 0.1, 42: 0.3, 52: 0.5, 62: 0.4, 72: 0.2, 82: 0.2, 92: 0.2}
+    res, st, _ = orc.search_mock_draws(_line(f, 52), {0: [0, 0, 1, 0, 1]}, 80, _bu(orc))
+    assert [(r[2], r[3]) for r in res] == [(0, 52)]
+    assert st["bu_iterations"] == 5 and st["bu_climbs"] == 1   # lo = 52 next: 52 + 32 > 80
+
+
+def test_lahc_history_update_writes_current_value(orc):
+    """l.19-20 "if I_w > I_wh then I_wh := I_w" (the current solution's value, not the rejected candidate's).
+    2-D landscape, d = 10, s_min 30, s_max 60, [lo, hi) = [0, 70), h = 3, T_maxIdle = 2,
+    draws r = 1, 2, 0, 1, 2, 2, 2, 0, 1:
+      start (0,30) 0.2, L = [.2 .2 .2]
+      it1 r=1: N = (0,40) .5, (10,40) .2 -> (0,40) .5 > .2 accept;  L = [.2 .5 .2]
+      it2 r=2: best (0,50) .3 > L2 .2: accept (late, downhill);       L = [.2 .5 .3]
+      it3 r=0: best (0,60) .7: accept;                                 L = [.7 .5 .3]
+      it4 r=1: best (10,60) .5 = L1, < .7: reject, idle 1; .7 > .5 -> L1 = .7 (the rejected .5 would stay)
+      it5 r=2: (10,60) .5 > L2 .3: accept, idle 0;                     L = [.7 .7 .5]
+      it6 r=2: best (20,70) .8: accept;                                L = [.7 .7 .8]
+      it7 r=2: best (30,60) .6 < .8: reject, idle 1
+      it8 r=0: .6 < L0 .7: reject, idle 2; L0 = .8
+      it9 r=1: .6 < L1 .7: reject, idle 3 > 2: stop at (20,70) after 9 iterations.
+    Writing I_best instead leaves L1 = .5 at it4, so it9 accepts (30,60) and the climb runs 13 iterations."""
+    vals = {(0, 30): .2, (0, 40): .5, (0, 50): .3, (0, 60): .7, (10, 40): .2, (10, 50): .1, (10, 60): .5,
+            (10, 70): .1, (20, 50): .2, (20, 60): .3, (20, 70): .8, (30, 60): .6, (30, 70): .5, (40, 70): .3}
+
+    def fn(t0, t1):
+        return (vals.get((t0, t1), -1.0), 1.0, 1.0 if (t0, t1) == (20, 70) else 0.0)
+
+    res, st, _ = orc.search_mock_draws(fn, {0: [1, 2, 0, 1, 2, 2, 2, 0, 1]}, 70,
+                                       _bu(orc, s_min=30, s_max=60, h=3, t_max_idle=2))
+    assert [(r[2], r[3]) for r in res] == [(20, 70)]
+    assert st["bu_iterations"] == 9 and st["bu_climbs"] == 1
+
+
+def test_bu_restart_after_accept(orc):
+    """Line 25 / S:407: after an accepted window the next climb starts at its end (max(t1, lo + s_min));
+    after a rejected climb at lo + s_min.  The unimodal climb of test_bu_climbs_to_unimodal_peak accepts
+    (50, 112) from lo = 0, so the climbs start at 0, 112, 144, ..., 368 (368 + 32 <= 400): 10 climbs
+    (restarting at lo + s_min instead would give 12, starting at 0, 32, ..., 352)."""
+    d = 10
+    a, b = 50, 50 + 32 + 3 * d
+
+    def fn(t0, t1):
+        v = 1.0 - (abs(t0 - a) + abs(t1 - b)) / 1000.0
+        return (v, 1.0, 0.5 if (t0, t1) == (a, b) else 0.05)
+
+    res, st, calls = orc.search_mock(fn, 400, P(orc, method=2, s_min=32, s_max=200, delta_bu=d, k=4))
+    assert [(r[2], r[3]) for r in res] == [(a, b)]
+    assert st["bu_climbs"] == 10
+    assert (112, 144) in calls and (368, 400) in calls
+
+
 def test_bu_seed_determinism(orc):
     wl = datagen.cfg1()
     p = orc.make_params(wl.search, method=2)
@@ -179,6 +272,35 @@ def test_chunks_np1_equals_plain(orc):
     a = orc.search(wl.series, wl.pairs, orc.make_params(wl.search))
     b = orc.search(wl.series, wl.pairs, orc.make_params(wl.search, n_chunks=1))
     assert a == b
+
+
+def _chunk_mock(a, b):
+    """n = 200, n_p = 2, s_max = s_min = 64 (TD, one layer, delta 16): chunks [0,100) and [36,200) (Alg. 4
+    line 14).  Chunk 0 scans t = 0, 16, 32 and accepts (32,96); chunk 1 scans t = 36 and accepts
+    (36,100), then 100, 116, 132.  The two results overlap: the merge keeps one (reading R20)."""
+    def fn(t0, t1):
+        if (t0, t1) == (32, 96):
+            return a
+        if (t0, t1) == (36, 100):
+            return b
+        return (0.0, 1.0, 0.0)
+    return fn
+
+
+@pytest.mark.parametrize("a,b,keep", [
+    ((1.0, 2.0, 0.9), (5.0, 9.0, 0.5), (32, 96)),     # higher normalized MI first, whatever the raw MI
+    ((2.0, 2.0, 1.0), (3.0, 3.0, 1.0), (36, 100)),    # normalized tie (saturated at 1): higher raw MI
+    ((2.0, 2.0, 1.0), (2.0, 2.0, 1.0), (32, 96)),     # full tie: smaller (t0, t1)
+    ((3.0, 3.0, 1.0), (2.0, 2.0, 1.0), (32, 96)),
+])
+def test_chunk_merge_priority(orc, a, b, keep):
+    """R20: greedy by (normalized MI desc, raw MI desc, t0 asc, t1 asc), keep if disjoint, sort by t0."""
+    p = P(orc, method=1, s_min=64, s_max=64, n_chunks=2)
+    res, st, calls = orc.search_mock(_chunk_mock(a, b), 200, p)
+    assert (32, 96) in calls and (36, 100) in calls and st["td_accepted"] == 2
+    assert [(r[2], r[3]) for r in res] == [keep]
+    got = res[0]
+    assert (got[4], got[5], got[6]) == (a if keep == (32, 96) else b)
 
 
 def test_chunks_interior_windows_preserved(orc):
