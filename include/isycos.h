@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define ISYCOS_ABI_VERSION 2
+#define ISYCOS_ABI_VERSION 3
 #define ISYCOS_MAX_K 16
 #define ISYCOS_MAX_W 262144 /* 2^18: int64 fixed-point bound of the digamma sums */
 
@@ -180,6 +180,13 @@ typedef struct {
      * with it).  Zero => defaults M = 20, m = 6, alpha = 0.5, rho = 0.5.  Needs m <= M, n / M >= s_min. */
     int32_t auto_M, auto_m;
     double auto_alpha, auto_rho;
+    /* (pair, chunk) work units for multi-GPU sharding (Alg. 4 line 14): 0, 0 => every
+     * chunk of the n_chunks plan, merged per (pair, method).  Otherwise only chunks [chunk_begin,
+     * chunk_end) of the plan run and their windows are returned UNMERGED (per chunk, each chunk's windows
+     * disjoint); isycos_merge_windows applies the merge once all chunks of a pair are gathered.  The
+     * per-chunk searches are independent, so the merged result equals the all-chunks call.  Not with
+     * method 4. */
+    int32_t chunk_begin, chunk_end;
 } isycos_search_opts;
 
 /* One accepted window (Def 3.5).  Records are sorted by (pair, method, t0); per (pair,
@@ -220,6 +227,16 @@ int isycos_search(const float* const* series, int32_t n_series, int64_t n, const
                   int32_t n_pairs, const isycos_scales* scales, int32_t k, const isycos_noise* noise,
                   const isycos_search_opts* opts, isycos_result_window* out_windows,
                   int64_t out_capacity, int64_t* out_count, isycos_search_stats* out_stats);
+
+/*
+ * isycos_merge_windows — the chunk merge of Alg. 4 (the paper is silent on the rule, reading R20):
+ * per (pair, method), greedy by (nmi desc, mi desc, t0 asc, t1 asc), a window is kept iff it is disjoint
+ * from every window kept before it; output sorted by (pair, method, t0).
+ *   in       n records (host memory, any order); out  out_capacity records (host memory, may not alias in)
+ * Errors: E_INVAL (null pointers, n < 0), E_TRUNC (first out_capacity written, *out_count = required).
+ */
+int isycos_merge_windows(const isycos_result_window* in, int64_t n, isycos_result_window* out,
+                         int64_t out_capacity, int64_t* out_count);
 
 /* Message for the last non-OK return on this thread ("" if none).  Valid until the next call. */
 const char* isycos_last_error(void);

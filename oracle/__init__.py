@@ -16,7 +16,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
-CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC", "-pthread"]
 
 
 def build(force: bool = False) -> str:
@@ -35,6 +35,7 @@ class OParams(C.Structure):
         ("sigma", C.c_double), ("tau_ratio", C.c_double), ("seed", C.c_uint64),
         ("sizes", C.POINTER(C.c_int64)), ("n_sizes", C.c_int32), ("_pad", C.c_int32),
         ("auto_M", C.c_int32), ("auto_m", C.c_int32), ("auto_alpha", C.c_double), ("auto_rho", C.c_double),
+        ("chunk_begin", C.c_int32), ("chunk_end", C.c_int32),
     ]
 
 
@@ -160,7 +161,7 @@ def mi_batch(x, y, windows, k: int = 4, variant: int = 0):
 def make_params(sc=None, **kw) -> OParams:
     d = dict(k=4, variant=0, method=3, noise=1, p=3, h=5, t_max_idle=3, n_chunks=1, s_min=64,
              s_max=512, delta_td=0, delta_bu=0, sigma=0.2, tau_ratio=0.25, seed=0, sizes=None,
-             auto_M=0, auto_m=0, auto_alpha=0.0, auto_rho=0.0)
+             auto_M=0, auto_m=0, auto_alpha=0.0, auto_rho=0.0, chunk_begin=0, chunk_end=0)
     if sc is not None:
         d.update(k=sc.k, method=sc.method, noise=int(sc.noise), p=sc.p, h=sc.h, t_max_idle=sc.t_max_idle,
                  n_chunks=sc.n_chunks, s_min=sc.s_min, s_max=sc.s_max, delta_td=sc.delta_td,

@@ -31,10 +31,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
 #include <set>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -130,51 +132,90 @@ double normalized(double mi, double h, int32_t zero_eps) {
     return r;
 }
 
+// Point i of a window: eps_i (KSG-1 radius, both variants) and the variant's marginal counts.
+void point_eval(const float* x, const float* y, int64_t w, int64_t i, int k, int variant, int eps_method,
+                std::vector<float>& buf, std::vector<std::pair<float, int64_t>>& dj, float* eps_o,
+                int64_t* nx_o, int64_t* ny_o) {
+    float eps = kth_distance(x, y, w, i, k, eps_method, buf);
+    int64_t nx = 0, ny = 0;
+    if (variant == 0) {
+        // KSG-1: n_x(i) = #{j != i : |x_i - x_j| < eps_i}  (strict; north star)
+        for (int64_t j = 0; j < w; ++j) {
+            if (j == i) continue;
+            if (std::fabs(x[i] - x[j]) < eps) ++nx;
+            if (std::fabs(y[i] - y[j]) < eps) ++ny;
+        }
+    } else {
+        // KSG-2 (Eq. 2): the k nearest in ascending (d_ij, j) order; per-dimension
+        // d_x, d_y = max over them; n_x = #{j != i : |x_i - x_j| <= d_x}.
+        dj.clear();
+        for (int64_t j = 0; j < w; ++j)
+            if (j != i) dj.push_back({dist(x[i], y[i], x[j], y[j]), j});
+        std::sort(dj.begin(), dj.end());
+        float dxk = 0.0f, dyk = 0.0f;
+        for (int m = 0; m < k; ++m) {
+            int64_t j = dj[m].second;
+            float ax = std::fabs(x[i] - x[j]);
+            float ay = std::fabs(y[i] - y[j]);
+            if (ax > dxk) dxk = ax;
+            if (ay > dyk) dyk = ay;
+        }
+        for (int64_t j = 0; j < w; ++j) {
+            if (j == i) continue;
+            if (std::fabs(x[i] - x[j]) <= dxk) ++nx;
+            if (std::fabs(y[i] - y[j]) <= dyk) ++ny;
+        }
+    }
+    *eps_o = eps;
+    *nx_o = nx;
+    *ny_o = ny;
+}
+
+// Optional worker threads for the per-point loop of large windows (env ORACLE_THREADS, default 1; used
+// only to precompute the full-size golden files).  The points are independent and every sum below runs
+// sequentially in point order, so the results do not depend on the thread count.
+int oracle_threads() {
+    static int t = [] {
+        const char* e = std::getenv("ORACLE_THREADS");
+        int v = e ? std::atoi(e) : 1;
+        return v < 1 ? 1 : v;
+    }();
+    return t;
+}
+
 // KSG-1 (north star) or KSG-2 (Eq. 2 literal) MI of one window of w points, plus the
 // Kozachenko-Leonenko joint entropy H from the same eps_i (Eq. 13 reading).
 int window_estimate(const float* x, const float* y, int64_t w, int k, int variant, int eps_method,
                     WinResult* out, float* eps_out, int32_t* nx_out, int32_t* ny_out) {
     if (w <= k || k < 1) return -3;
     ensure_psi(w + 1);
-    std::vector<float> buf;
-    buf.reserve(w);
+    std::vector<float> E(w);
+    std::vector<int64_t> NX(w), NY(w);
+    auto run = [&](int64_t i0, int64_t i1) {
+        std::vector<float> buf;
+        buf.reserve(w);
+        std::vector<std::pair<float, int64_t>> dj;
+        for (int64_t i = i0; i < i1; ++i) point_eval(x, y, w, i, k, variant, eps_method, buf, dj, &E[i], &NX[i], &NY[i]);
+    };
+    const int T = w >= 2048 ? oracle_threads() : 1;
+    if (T > 1) {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t) th.emplace_back(run, w * t / T, w * (t + 1) / T);
+        for (auto& h : th) h.join();
+    } else {
+        run(0, w);
+    }
     int64_t s_psi = 0, s_log = 0;
     int32_t zeros = 0;
     double plain_psi = 0.0, plain_log = 0.0;
-    std::vector<std::pair<float, int64_t>> dj;
     for (int64_t i = 0; i < w; ++i) {
-        float eps = kth_distance(x, y, w, i, k, eps_method, buf);
-        int64_t nx = 0, ny = 0;
+        const float eps = E[i];
+        const int64_t nx = NX[i], ny = NY[i];
         if (variant == 0) {
-            // KSG-1: n_x(i) = #{j != i : |x_i - x_j| < eps_i}  (strict; north star)
-            for (int64_t j = 0; j < w; ++j) {
-                if (j == i) continue;
-                if (std::fabs(x[i] - x[j]) < eps) ++nx;
-                if (std::fabs(y[i] - y[j]) < eps) ++ny;
-            }
             int64_t a = nx + 1, b = ny + 1;
             s_psi += q32(psi(a)) + q32(psi(b));
             plain_psi += psi(a) + psi(b);
         } else {
-            // KSG-2 (Eq. 2): the k nearest in ascending (d_ij, j) order; per-dimension
-            // d_x, d_y = max over them; n_x = #{j != i : |x_i - x_j| <= d_x}.
-            dj.clear();
-            for (int64_t j = 0; j < w; ++j)
-                if (j != i) dj.push_back({dist(x[i], y[i], x[j], y[j]), j});
-            std::sort(dj.begin(), dj.end());
-            float dxk = 0.0f, dyk = 0.0f;
-            for (int m = 0; m < k; ++m) {
-                int64_t j = dj[m].second;
-                float ax = std::fabs(x[i] - x[j]);
-                float ay = std::fabs(y[i] - y[j]);
-                if (ax > dxk) dxk = ax;
-                if (ay > dyk) dyk = ay;
-            }
-            for (int64_t j = 0; j < w; ++j) {
-                if (j == i) continue;
-                if (std::fabs(x[i] - x[j]) <= dxk) ++nx;
-                if (std::fabs(y[i] - y[j]) <= dyk) ++ny;
-            }
             s_psi += q32(psi(nx)) + q32(psi(ny));
             plain_psi += psi(nx) + psi(ny);
         }
@@ -240,6 +281,7 @@ struct OParams {
     int32_t n_sizes, _pad;
     int32_t auto_M, auto_m;                // Alg. 3: M partitions, m sampled (0 => 20, 6)
     double auto_alpha, auto_rho;           // Eqs. 4-9 weight alpha, small/large cut rho (0 => 0.5, 0.5)
+    int32_t chunk_begin, chunk_end;        // 0,0: every chunk, merged; else chunks [begin,end) only, unmerged
 };
 
 struct OResult {
@@ -569,6 +611,11 @@ int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats
     Searcher S(P, std::move(prov), pair_id, st);
     S.draw = std::move(draw);
     auto chunks = chunk_plan(n, P.n_chunks < 1 ? 1 : P.n_chunks, P.s_max);
+    const bool sel = P.chunk_end > P.chunk_begin;   // one shard's (pair, chunk) units: merged by the caller
+    if (sel) {
+        if (P.chunk_begin < 0 || P.chunk_end > (int32_t)chunks.size()) return -1;
+        chunks = std::vector<std::pair<int64_t, int64_t>>(chunks.begin() + P.chunk_begin, chunks.begin() + P.chunk_end);
+    }
     for (int m = 1; m <= 2; ++m) {
         if (!(P.method & m)) continue;
         std::vector<OResult> all;
@@ -577,6 +624,10 @@ int run_pair(const OParams& P, Provider prov, int32_t pair_id, int64_t n, OStats
             if (m == 1) S.td(lo, hi, R); else S.bu(lo, hi, R);
             if (S.err) return S.err;
             all.insert(all.end(), R.begin(), R.end());
+        }
+        if (sel) {
+            out.insert(out.end(), all.begin(), all.end());
+            continue;
         }
         auto merged = merge(all);
         out.insert(out.end(), merged.begin(), merged.end());

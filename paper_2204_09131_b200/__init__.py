@@ -12,6 +12,7 @@ from ._capi import (  # noqa: F401
     isycos_last_error,
     isycos_mi_batch,
     isycos_mi_batch_ex,
+    isycos_merge_windows,
     isycos_release_cache,
     isycos_search,
     lib,
@@ -19,4 +20,4 @@ from ._capi import (  # noqa: F401
 )
 
 __all__ = ["isycos_mi_batch", "isycos_mi_batch_ex", "isycos_search", "isycos_last_error",
-           "isycos_abi_version", "isycos_release_cache", "IsycosError", "search_workload"]
+           "isycos_abi_version", "isycos_release_cache", "isycos_merge_windows", "IsycosError", "search_workload"]

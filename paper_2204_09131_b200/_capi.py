@@ -25,8 +25,8 @@ ERROR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_RANGE", -3: "E_TOO_FEW", -4: "E_TR
                -6: "E_NOMEM", -7: "E_NCCL"}
 
 # symbols declared in include/isycos.h (checked by tests/test_abi.py)
-EXPORTS = ["isycos_mi_batch", "isycos_mi_batch_ex", "isycos_search", "isycos_last_error",
-           "isycos_abi_version", "isycos_release_cache"]
+EXPORTS = ["isycos_mi_batch", "isycos_mi_batch_ex", "isycos_search", "isycos_merge_windows",
+           "isycos_last_error", "isycos_abi_version", "isycos_release_cache"]
 
 
 class IsycosError(RuntimeError):
@@ -78,12 +78,18 @@ class SearchOpts(C.Structure):
                 ("delta_td", C.c_int64), ("delta_bu", C.c_int64), ("t_max_idle", C.c_int32),
                 ("h", C.c_int32), ("n_chunks", C.c_int32), ("lookahead", C.c_int32), ("seed", C.c_uint64),
                 ("flags", C.c_uint32), ("stream", C.c_void_p), ("auto_M", C.c_int32), ("auto_m", C.c_int32),
-                ("auto_alpha", C.c_double), ("auto_rho", C.c_double)]
+                ("auto_alpha", C.c_double), ("auto_rho", C.c_double), ("chunk_begin", C.c_int32),
+                ("chunk_end", C.c_int32)]
 
 
 class ResultWindow(C.Structure):
     _fields_ = [("pair", C.c_int32), ("method", C.c_int32), ("t0", C.c_int64), ("t1", C.c_int64),
                 ("mi", C.c_double), ("h", C.c_double), ("nmi", C.c_double)]
+
+
+RESULT_DTYPE = np.dtype([("pair", np.int32), ("method", np.int32), ("t0", np.int64), ("t1", np.int64),
+                         ("mi", np.float64), ("h", np.float64), ("nmi", np.float64)])
+assert RESULT_DTYPE.itemsize == C.sizeof(ResultWindow)
 
 
 SEARCH_STAT_FIELDS = ["td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs",
@@ -122,6 +128,7 @@ def lib():
         L.isycos_search.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.POINTER(Pair), C.c_int32,
                                     C.POINTER(Scales), C.c_int32, C.POINTER(Noise), C.POINTER(SearchOpts),
                                     C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(SearchStats)]
+        L.isycos_merge_windows.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -145,25 +152,45 @@ def _check(rc: int):
 
 # ------------------------------------------------------------------ buffer marshalling
 class _Buf:
-    """A pointer to host (numpy) or device (torch CUDA tensor) memory, kept alive."""
+    """A pointer to host (numpy) or device (torch CUDA tensor) memory, kept alive.
 
-    def __init__(self, obj, dtype):
+    CUDA tensors are passed through as they are, so they must already have the dtype the C ABI expects and
+    live on the current device (no silent reinterpretation, no cross-device pointers); host inputs are
+    converted.  Output buffers (output=True) are written in place, so they must match exactly."""
+
+    def __init__(self, obj, dtype, output: bool = False, name: str = "buffer"):
         self.obj = obj
         self.device = False
         try:
             import torch
 
             if isinstance(obj, torch.Tensor):
+                want = {np.float32: torch.float32, np.float64: torch.float64, np.int64: torch.int64,
+                        np.int32: torch.int32}[np.dtype(dtype).type]
                 if obj.is_cuda:
-                    assert obj.is_contiguous(), "device tensors must be contiguous"
+                    if obj.dtype != want:
+                        raise TypeError(f"{name}: CUDA tensor of dtype {obj.dtype}, expected {want}")
+                    if obj.device.index != torch.cuda.current_device():
+                        raise ValueError(f"{name}: tensor on {obj.device}, but the current device is "
+                                         f"cuda:{torch.cuda.current_device()} (torch.cuda.set_device)")
+                    if not obj.is_contiguous():
+                        raise ValueError(f"{name}: device tensors must be contiguous")
                     self.device = True
                     self.ptr = obj.data_ptr()
                     self.n = obj.numel()
                     return
+                if output and (obj.dtype != want or not obj.is_contiguous()):
+                    raise TypeError(f"{name}: output tensor must be contiguous {want}")
                 obj = obj.detach().numpy()
         except ImportError:  # pragma: no cover
             pass
-        self.obj = np.ascontiguousarray(obj, dtype=dtype)
+        if output:
+            if not (isinstance(obj, np.ndarray) and obj.dtype == np.dtype(dtype) and obj.flags.c_contiguous
+                    and obj.flags.writeable):
+                raise TypeError(f"{name}: output buffer must be a writeable C-contiguous {np.dtype(dtype)} array")
+            self.obj = obj
+        else:
+            self.obj = np.ascontiguousarray(obj, dtype=dtype)
         self.ptr = self.obj.ctypes.data
         self.n = self.obj.size
 
@@ -190,9 +217,10 @@ def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", 
     x, y: float32 numpy arrays or torch tensors (CPU or CUDA); windows: (n, 2) int64 array/tensor.
     out: optional dict of caller-provided output buffers (e.g. CUDA tensors) keyed like `outputs`.
     """
-    bx, by = _Buf(x, np.float32), _Buf(y, np.float32)
-    assert bx.n == by.n, "x and y must have the same length"
-    bw = _Buf(windows, np.int64)
+    bx, by = _Buf(x, np.float32, name="x"), _Buf(y, np.float32, name="y")
+    if bx.n != by.n:
+        raise ValueError("x and y must have the same length")
+    bw = _Buf(windows, np.int64, name="windows")
     nw = bw.n // 2
     res = {}
     o = MiOpts()
@@ -203,7 +231,9 @@ def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", 
 
     def target(name, dtype, count):
         if out is not None and name in out:
-            b = _Buf(out[name], dtype)
+            b = _Buf(out[name], dtype, output=True, name=f"out[{name!r}]")
+            if b.n < count:
+                raise ValueError(f"out[{name!r}] holds {b.n} elements, needs {count}")
             keep.append(b)
             res[name] = out[name]
             return b.ptr
@@ -240,17 +270,19 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
                   tau_ratio: float = 0.25, p: int = 3, sigma: float = 0.2, method: int = 3, delta_td: int = 0,
                   delta_bu: int = 0, t_max_idle: int = 3, h: int = 5, n_chunks: int = 1, lookahead: int = 0,
                   seed: int = 0, variant: int = 0, profile: bool = False, brute: bool = False,
-                  unfused: bool = False, stream=None, capacity: int = 1 << 16, auto_M: int = 0, auto_m: int = 0,
-                  auto_alpha: float = 0.0, auto_rho: float = 0.0, profile_only: str | None = None):
+                  unfused: bool = False, stream=None, capacity: int | None = None, auto_M: int = 0, auto_m: int = 0,
+                  auto_alpha: float = 0.0, auto_rho: float = 0.0, profile_only: str | None = None,
+                  chunks: tuple | None = None):
     """SYCOS search over series pairs.  Returns (results, stats).
 
     series: list of float32 arrays / tensors (host or CUDA, all alike, same length)
     pairs:  list of (xs, ys) or (xs, ys, id)
     results: list of tuples (pair, method, t0, t1, mi, h, nmi) sorted by (pair, method, t0)
     """
-    bufs = [_Buf(s, np.float32) for s in series]
+    bufs = [_Buf(s, np.float32, name=f"series[{i}]") for i, s in enumerate(series)]
     n = bufs[0].n
-    assert all(b.n == n for b in bufs), "all series must have the same length"
+    if not all(b.n == n for b in bufs):
+        raise ValueError("all series must have the same length")
     ptrs = (C.c_void_p * len(bufs))(*[b.ptr for b in bufs])
     pr = (Pair * max(1, len(pairs)))()
     for i, q in enumerate(pairs):
@@ -269,24 +301,41 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
     o.delta_td, o.delta_bu, o.t_max_idle, o.h = int(delta_td), int(delta_bu), int(t_max_idle), int(h)
     o.n_chunks, o.lookahead, o.seed = int(n_chunks), int(lookahead), int(seed) & ((1 << 64) - 1)
     o.auto_M, o.auto_m, o.auto_alpha, o.auto_rho = int(auto_M), int(auto_m), float(auto_alpha), float(auto_rho)
+    if chunks is not None:  # (pair, chunk) units: chunks [begin, end) of the plan, windows unmerged
+        o.chunk_begin, o.chunk_end = int(chunks[0]), int(chunks[1])
     o.flags = (F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
     if profile and profile_only:  # events around one path's launches only ("sorted" or "brute")
         o.flags |= F_PROFILE_SORTED_ONLY if profile_only == "sorted" else F_PROFILE_BRUTE_ONLY
     o.stream = _stream_ptr(stream)
+    # results per pair and method are disjoint windows of >= s_min samples: at most n // s_min each.  The
+    # buffer is np.empty (untouched pages cost nothing), so the bound never forces a second search.
+    n_methods = 2 if int(method) in (3, 4) else 1
+    if capacity is None:
+        capacity = min(max(1, n_methods * len(pairs) * (n // max(1, int(s_min)))), 1 << 24)
     while True:
-        outw = (ResultWindow * max(1, capacity))()
+        outw = np.empty(max(1, capacity), dtype=RESULT_DTYPE)
         cnt = C.c_int64(0)
         st = SearchStats()
         rc = lib().isycos_search(C.cast(ptrs, C.c_void_p), len(bufs), n, pr, len(pairs), C.byref(sc), int(k),
-                                 C.byref(nz), C.byref(o), C.cast(outw, C.c_void_p), capacity, C.byref(cnt),
+                                 C.byref(nz), C.byref(o), outw.ctypes.data, capacity, C.byref(cnt),
                                  C.byref(st))
-        if rc == E_TRUNC:
+        if rc == E_TRUNC:  # only when the caller passed a smaller capacity
             capacity = int(cnt.value)
             continue
         _check(rc)
         break
-    res = [(r.pair, r.method, r.t0, r.t1, r.mi, r.h, r.nmi) for r in outw[:cnt.value]]
+    res = [tuple(r) for r in outw[:cnt.value].tolist()]
     return res, st.as_dict()
+
+
+def isycos_merge_windows(results):
+    """Alg. 4 chunk merge (reading R20) of gathered per-chunk result tuples; sorted by (pair, method, t0)."""
+    arr = np.array([tuple(r) for r in results], dtype=RESULT_DTYPE) if len(results) else np.empty(0, RESULT_DTYPE)
+    out = np.empty(max(1, len(arr)), dtype=RESULT_DTYPE)
+    cnt = C.c_int64(0)
+    _check(lib().isycos_merge_windows(arr.ctypes.data if len(arr) else None, len(arr), out.ctypes.data, len(arr),
+                                      C.byref(cnt)))
+    return [tuple(r) for r in out[:cnt.value].tolist()]
 
 
 def search_workload(wl, *, series=None, pairs=None, **kw):

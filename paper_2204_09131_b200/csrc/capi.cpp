@@ -1,5 +1,5 @@
 // C ABI of libisycos.so (include/isycos.h): validation, host/device pointer handling, error codes.
-// All arithmetic of the path runs in ksg_kernels.cu; this file only marshals.
+// All arithmetic of the path runs in the ksg_*.cu kernels; this file only marshals.
 
 #include <algorithm>
 #include <cmath>
@@ -13,7 +13,11 @@ using namespace isy;
 
 namespace {
 
-bool is_device_ptr(const void* p) {
+// Device memory (or managed memory) the kernels can read directly?  Device memory of ANOTHER device is an
+// argument error (kernels would fault with a sticky illegal-address error): *other_dev is set and the
+// callers return ISYCOS_E_INVAL.  Host memory (pageable, pinned or mapped) is staged by the library.
+bool is_device_ptr(const void* p, bool* other_dev = nullptr) {
+    if (other_dev) *other_dev = false;
     if (!p) return false;
     cudaPointerAttributes a;
     cudaError_t e = cudaPointerGetAttributes(&a, p);
@@ -21,7 +25,20 @@ bool is_device_ptr(const void* p) {
         cudaGetLastError();  // clear: unregistered host memory on some drivers
         return false;
     }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    if (a.type == cudaMemoryTypeManaged) return true;
+    if (a.type != cudaMemoryTypeDevice) return false;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && a.device != cur && other_dev) *other_dev = true;
+    return true;
+}
+
+Status check_ptr(const void* p, const char* what) {
+    bool other = false;
+    is_device_ptr(p, &other);
+    if (other)
+        return make_err(ISYCOS_E_INVAL, std::string(what) + " is device memory of another GPU than the current "
+                                                              "device (call cudaSetDevice / torch.cuda.set_device)");
+    return Status{};
 }
 
 int fail(const Status& s) {
@@ -94,6 +111,12 @@ extern "C" int isycos_mi_batch_ex(const float* x, const float* y, int64_t n, con
     if (n_windows == 0) return ok();
 
     Status s;
+    for (auto [p, what] : {std::pair<const void*, const char*>{x, "x"}, {y, "y"}, {windows, "windows"},
+                           {out_mi, "out_mi"}, {o.out_h, "out_h"}, {o.out_nmi, "out_nmi"},
+                           {o.out_sum_psi_q, "out_sum_psi_q"}, {o.out_sum_log_q, "out_sum_log_q"},
+                           {o.out_zero_eps, "out_zero_eps"}, {o.dbg_eps, "dbg_eps"}, {o.dbg_nx, "dbg_nx"},
+                           {o.dbg_ny, "dbg_ny"}})
+        if (!(s = check_ptr(p, what)).ok()) return fail(s);
     Engine* eng = engine_for_current_device(&s);
     if (!eng) return fail(s);
     cudaStream_t st = o.stream ? static_cast<cudaStream_t>(o.stream) : eng->own_stream();
@@ -261,6 +284,8 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     P.lookahead = opts->lookahead > 0 ? opts->lookahead : 32;
     P.seed = opts->seed;
     P.flags = opts->flags;
+    P.chunk_begin = opts->chunk_begin;
+    P.chunk_end = opts->chunk_end;
     // speculation tuning knobs (do not change results)
     if (const char* e = std::getenv("ISYCOS_BU_DEPTH")) P.bu_depth = std::atoi(e);
     if (const char* e = std::getenv("ISYCOS_TREND_DEPTH")) P.trend_depth = std::atoi(e);
@@ -289,6 +314,12 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
             return bad("AUTO: auto_alpha and auto_rho must be in [0, 1]");
     }
     if (P.n_chunks < 1) return bad("n_chunks must be >= 1");
+    if (P.chunk_begin != 0 || P.chunk_end != 0) {
+        if (P.method == 4) return bad("chunk selection is not available with method 4 (AUTO)");
+        const int32_t n_plan = (int32_t)chunks_of(n, P.n_chunks, P.s_max).size();
+        if (P.chunk_begin < 0 || P.chunk_end <= P.chunk_begin || P.chunk_end > n_plan)
+            return bad("need 0 <= chunk_begin < chunk_end <= number of chunks");
+    }
     if (P.delta_td < 0 || P.delta_bu < 0) return bad("delta must be >= 0");
     for (size_t i = 0; i < P.sizes.size(); ++i) {
         if (P.sizes[i] <= k || P.sizes[i] > P.s_max || P.sizes[i] < P.s_min || (i && P.sizes[i] >= P.sizes[i - 1]))
@@ -300,6 +331,8 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     }
 
     Status s;
+    for (int32_t i = 0; i < n_series; ++i)
+        if (!(s = check_ptr(series[i], "a series pointer")).ok()) return fail(s);
     Engine* eng = engine_for_current_device(&s);
     if (!eng) return fail(s);
     cudaStream_t st = opts->stream ? static_cast<cudaStream_t>(opts->stream) : eng->own_stream();
@@ -333,6 +366,30 @@ extern "C" int isycos_search(const float* const* series, int32_t n_series, int64
     *out_count = (int64_t)res.size();
     const int64_t m = std::min<int64_t>(out_capacity, (int64_t)res.size());
     if (m > 0) std::memcpy(out_windows, res.data(), m * sizeof(isycos_result_window));
+    if ((int64_t)res.size() > out_capacity)
+        return fail(make_err(ISYCOS_E_TRUNC, "out_capacity too small: need " + std::to_string(res.size())));
+    return ok();
+}
+
+extern "C" int isycos_merge_windows(const isycos_result_window* in, int64_t n, isycos_result_window* out,
+                                    int64_t out_capacity, int64_t* out_count) {
+    if ((!in && n > 0) || !out_count || (!out && out_capacity > 0) || n < 0 || out_capacity < 0)
+        return fail(make_err(ISYCOS_E_INVAL, "null pointer or negative count"));
+    std::vector<isycos_result_window> all(in, in + n);
+    std::stable_sort(all.begin(), all.end(), [](const isycos_result_window& a, const isycos_result_window& b) {
+        return a.pair != b.pair ? a.pair < b.pair : a.method < b.method;
+    });
+    std::vector<isycos_result_window> res;
+    for (size_t i = 0; i < all.size();) {
+        size_t j = i;
+        while (j < all.size() && all[j].pair == all[i].pair && all[j].method == all[i].method) ++j;
+        auto m = merge_windows(std::vector<isycos_result_window>(all.begin() + i, all.begin() + j));
+        res.insert(res.end(), m.begin(), m.end());
+        i = j;
+    }
+    *out_count = (int64_t)res.size();
+    const int64_t m = std::min<int64_t>(out_capacity, (int64_t)res.size());
+    if (m > 0) std::memcpy(out, res.data(), m * sizeof(isycos_result_window));
     if ((int64_t)res.size() > out_capacity)
         return fail(make_err(ISYCOS_E_TRUNC, "out_capacity too small: need " + std::to_string(res.size())));
     return ok();

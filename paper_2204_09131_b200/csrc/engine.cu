@@ -247,8 +247,11 @@ Status Engine::evaluate(const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wi
 Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
                       int32_t variant, const DebugOut& dbg, cudaStream_t st, uint32_t flags, BatchStats* bs) {
     Slot& S = slots_[si];
+    if (S.busy) {  // never reuse a slot's staging/record buffers while an earlier batch may still read them
+        cudaStreamSynchronize(S.st);
+        S.busy = false;
+    }
     S.n = 0;
-    S.busy = false;
     const bool profile = (flags & ISYCOS_F_PROFILE) != 0;
     const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
@@ -440,6 +443,10 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     char* dbase = S.dstage;
     ISY_CK(cudaMemcpyAsync(S.dstage, S.hstage, total, cudaMemcpyHostToDevice, st));
     if (bs) bs->h2d_bytes += total;
+    S.busy = true;  // from here on the slot's buffers are in use (an error return below leaves it to be synced)
+    S.st = st;
+    S.profile = false;
+    S.n_ksg = 0;
 
     KsgLaunch L;
     L.pairs = reinterpret_cast<const PairPtrs*>(dbase + off_pairs);

@@ -4,7 +4,7 @@
 //   capi.cpp     validation, pointer classification, error codes  (C ABI)
 //   search.cpp   batched SYCOS_TD / SYCOS_BU / noise / chunk driver (host state machines)
 //   engine.cu    per-device context: digamma tables, buffers, batch evaluation, profiling
-//   ksg_kernels.cu  the sm_100a KSG window kernels (a2-a6 of SURVEY §8(a))
+//   ksg_*.cu     the sm_100a KSG window kernels (a2-a6 of SURVEY §8(a)), ksg_device.cuh their helpers
 #pragma once
 
 #include <cuda_runtime.h>
@@ -82,7 +82,7 @@ constexpr int kScanB = 8;                // sorted-path scan: candidates per blo
 constexpr int kFusedMaxW = 4096;         // fused sort+scan path (latency mode): windows up to this size
 constexpr int kFusedThreads = 512;       // threads per fused CTA (16 warps: one 256-key sort chunk each)
 
-// Launchers (ksg_kernels.cu).  Return cudaGetLastError().
+// Launchers (ksg_*.cu).  Return cudaGetLastError().
 cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
 cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st);
 // sorted path: sort kernel over segments {list pos, start}, XL rank merge over blocks {list pos, start},
@@ -100,6 +100,9 @@ int fused_ppc(int w, int gmax);
 cudaError_t launch_psi_tables(double* psi, long long* psiq, double* inv, int64_t m_max, double* lnc,
                               cudaStream_t st);
 cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStream_t st);
+// Opt a kernel into > 48 KB of dynamic shared memory on the current device.  The attribute is per device,
+// so this is done once per (device, kernel) under a lock (several devices / threads per process).
+cudaError_t smem_optin(const void* kernel, int bytes);
 
 // ---------------------------------------------------------------- errors
 struct Status {
@@ -247,7 +250,13 @@ struct SearchParams {
     double auto_alpha = 0.0, auto_rho = 0.0;  // Eqs. 4-9 weights (0 => 0.5, 0.5)
     uint64_t seed = 0;
     uint32_t flags = 0;          // ISYCOS_F_PROFILE | ISYCOS_F_BRUTE
+    int32_t chunk_begin = 0, chunk_end = 0;  // (pair, chunk) units: chunks [begin, end) only, unmerged
 };
+
+// Alg. 4 chunk plan (clipped) and the chunk merge (reading R20), shared by the search driver and
+// isycos_merge_windows.
+std::vector<std::pair<int64_t, int64_t>> chunks_of(int64_t n, int32_t n_p, int64_t s_max);
+std::vector<isycos_result_window> merge_windows(std::vector<isycos_result_window> all);
 
 Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std::vector<int32_t>& pair_ids,
                   int64_t n, const SearchParams& P, cudaStream_t st, std::vector<isycos_result_window>* out,

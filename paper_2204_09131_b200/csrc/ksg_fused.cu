@@ -96,8 +96,7 @@ cudaError_t fused_k(const KsgLaunch& L, const int32_t* list, const KsgItem* item
 
 template <int K1, bool V2>
 cudaError_t fused_attr() {
-    return cudaFuncSetAttribute(fused_sorted_kernel<K1, V2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kFusedMaxW * 28 + 32 * kScanB);
+    return smem_optin(reinterpret_cast<const void*>(fused_sorted_kernel<K1, V2>), kFusedMaxW * 28 + 32 * kScanB);
 }
 template <int K1>
 cudaError_t fused_attr_k(const KsgLaunch&) {
@@ -108,12 +107,10 @@ cudaError_t fused_attr_k(const KsgLaunch&) {
 cudaError_t launch_fused(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
                          cudaStream_t st) {
     if (n_items <= 0) return cudaSuccess;
-    static bool attr[17] = {};
     if (L.k < 1 || L.k > 16) return cudaErrorInvalidValue;
-    if (!attr[L.k]) {
+    {
         cudaError_t e = [&]() -> cudaError_t { ISY_K_CASES(fused_attr_k, L) }();
         if (e != cudaSuccess) return e;
-        attr[L.k] = true;
     }
     ISY_K_CASES(fused_k, L, list, items, n_items, gmax, st)
 }

@@ -1,4 +1,8 @@
-// Digamma tables, input validation, size-class helpers.
+// Digamma tables, input validation, size-class helpers, shared-memory opt-in.
+#include <mutex>
+#include <set>
+#include <tuple>
+
 #include "ksg_device.cuh"
 
 namespace isy {
@@ -66,5 +70,19 @@ cudaError_t launch_nonfinite_scan(const float* p, int64_t n, int* flag, cudaStre
     return cudaGetLastError();
 }
 
+
+cudaError_t smem_optin(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<int, const void*, int>> done;
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, kernel, bytes);
+    if (done.count(key)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
+}
 
 }  // namespace isy

@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, co
     while (n2 < len) n2 <<= 1;
     const float* gx = L.pairs[W.pair].x + W.t0;
     const float* gy = L.pairs[W.pair].y + W.t0;
-    const int64_t o = soff[b];  // the window's region has 4 spare entries on either side (scan sentinels)
+    const int64_t o = soff[b];  // the window's region has kScanB spare entries on either side (scan sentinels)
     if (s0 == 0 && threadIdx.x < 2 * kScanB) put_sentinels(P2 + o, w, threadIdx.x);
     if (n2 >= 256) {
         // register chunk sorts (256 keys per warp) + merge-path levels in SMEM (the fused kernel's sort, ~2x
@@ -173,12 +173,9 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_items, cudaStream_t st) {
     static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
     if (n_segs <= 0) return cudaSuccess;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(sort_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kSortedMaxW * 20);
+    {
+        cudaError_t e = smem_optin(reinterpret_cast<const void*>(sort_window_kernel), kSortedMaxW * 20);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     // one thread per 8 keys (= one merge-path output run; chunk sorts are 256 keys per warp): smaller CTAs
     // for small segments keep every warp busy and let more CTAs share an SM

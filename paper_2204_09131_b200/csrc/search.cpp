@@ -215,21 +215,25 @@ struct TdJob {
     }
     int64_t delta(int64_t s) const { return P->delta_td > 0 ? P->delta_td : std::max<int64_t>(1, s / 4); }
 
+    // The delta-grid of [t, b) anchored at t: every window the layer can visit there while no accept or
+    // noise skip moves it off this grid (plus the two noise sub-windows of every shifted position).
+    void request_grid(View& v, int64_t t, int64_t b, int64_t s, bool first_unshifted) {
+        const int64_t d = delta(s);
+        const bool nz = P->noise && d > P->k && s - d > P->k;
+        for (int64_t u = t; u + s <= b; u += d) {
+            v.want(u, u + s);
+            if (nz && (u > t || !first_unshifted)) {
+                v.want(u, u + s - d);
+                v.want(u + s - d, u + s);
+            }
+        }
+    }
+
     void request_layer(int64_t s) {
         std::vector<uint64_t> dummy;
         View v{cache, &dummy};
-        const int64_t d = delta(s);
-        const bool nz = P->noise && d > P->k && s - d > P->k;
-        for (auto [a, b] : parts) {
-            if (b - a < s) continue;
-            for (int64_t t = a; t + s <= b; t += d) {
-                v.want(t, t + s);
-                if (nz && t > a) {
-                    v.want(t, t + s - d);
-                    v.want(t + s - d, t + s);
-                }
-            }
-        }
+        for (auto [a, b] : parts)
+            if (b - a >= s) request_grid(v, a, b, s, true);
     }
 
     // One exact replay of the layer (Alg. 1 lines 3-15 over every partition).  Returns false if a
@@ -253,7 +257,14 @@ struct TdJob {
             while (t + s <= b) {
                 ls.td_windows += 1;
                 const Eval* e = v.get(t, t + s);
-                if (!e) return false;
+                if (!e) {
+                    // off the layer-start grid (an accept or a noise skip moved t by s, s % delta != 0):
+                    // queue the rest of this partition anchored at t, so it costs one round, not one per window
+                    std::vector<uint64_t> dummy;
+                    View w{cache, &dummy};
+                    request_grid(w, t, b, s, !shifted);
+                    return false;
+                }
                 if (e->nmi >= P->sigma) {
                     lr.push_back({pair_id, 1, t, t + s, e->mi, e->h, e->nmi});
                     ls.td_accepted += 1;
@@ -751,6 +762,8 @@ private:
     int total_ = 0;
 };
 
+}  // namespace
+
 // ------------------------------------------------------------------ chunks + merge
 std::vector<std::pair<int64_t, int64_t>> chunks_of(int64_t n, int32_t n_p, int64_t s_max) {
     std::vector<std::pair<int64_t, int64_t>> c;
@@ -786,6 +799,8 @@ std::vector<isycos_result_window> merge_windows(std::vector<isycos_result_window
     return kept;
 }
 
+namespace {
+
 struct PairWork {
     int32_t inflight = 0;  // batches in flight holding entries of this pair
     // this round's requests, staged by the pair's own (parallel) advance task
@@ -817,7 +832,13 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                   int64_t n, const SearchParams& P, cudaStream_t st, std::vector<isycos_result_window>* out,
                   isycos_search_stats* stats) {
     const int32_t n_pairs = (int32_t)pair_ptrs.size();
-    const auto plan = chunks_of(n, std::max(1, P.n_chunks), P.s_max);
+    auto plan = chunks_of(n, std::max(1, P.n_chunks), P.s_max);
+    const bool chunk_sel = P.chunk_end > P.chunk_begin;  // (pair, chunk) units: these chunks only, unmerged
+    if (chunk_sel) {
+        if (P.chunk_begin < 0 || P.chunk_end > (int32_t)plan.size())
+            return make_err(ISYCOS_E_INVAL, "chunk range outside the plan");
+        plan = std::vector<std::pair<int64_t, int64_t>>(plan.begin() + P.chunk_begin, plan.begin() + P.chunk_end);
+    }
     const int max_active = 64;
     AlgStats total;
     BatchStats bs;
@@ -893,6 +914,16 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         std::vector<int64_t> offs;  // batch offset of each pair in pws (+ end)
     };
     Flight fl[2];
+    // error exits leave no batch in flight: the slot's staging buffer and mapped records would otherwise be
+    // reused by the next call while the old copies and kernels still run
+    struct Drain {
+        Engine* eng;
+        Flight* fl;
+        ~Drain() {
+            for (int g = 0; g < 2; ++g)
+                if (fl[g].busy) eng->collect(g, nullptr, nullptr);
+        }
+    } drain{eng, fl};
     const int n_groups = P.pipeline ? 2 : 1;
     cudaStream_t sts[2] = {st, eng->second_stream()};
     if (n_groups == 2) {  // the second slot's stream starts after everything already queued on st
@@ -1028,6 +1059,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                                 if (m == 1 && !small) A.nL_td += 1;
                                 if (m == 2 && small) A.nS_bu += 1;
                             }
+                            continue;
+                        }
+                        if (chunk_sel) {  // merged by isycos_merge_windows once every chunk is gathered
+                            all.insert(all.end(), per.begin(), per.end());
                             continue;
                         }
                         auto merged = merge_windows(per);

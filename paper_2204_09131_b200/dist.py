@@ -109,19 +109,77 @@ def _gpu_search(series, pairs, **kw):
     return isycos_search(series, pairs, **kw)
 
 
-def search_sharded(series, pairs, *, search=None, device=None, **kw):
-    """SYCOS search over `pairs` sharded by pair (LPT on a w^2 cost proxy); every rank returns the
-    merged result list sorted by (pair, method, t0) and the summed algorithm counters."""
+def _gpu_merge(results):
+    from . import isycos_merge_windows
+
+    return isycos_merge_windows(results)
+
+
+def chunk_plan(n: int, n_p: int, s_max: int):
+    """Alg. 4 line 14, clipped: chunk c = [max(0, cL - s_max), min(n, (c+1)L)), L = ceil(n / n_p)."""
+    L = -(-n // n_p)
+    return [(max(0, c * L - s_max), min(n, (c + 1) * L)) for c in range(n_p) if c * L < n]
+
+
+STAT_NAMES = ["td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs", "bu_iterations",
+              "bu_neighbors", "bu_noise_checks", "bu_prunes", "bu_accepted", "distinct_windows",
+              "distinct_pairs", "eval_cost", "auto_td", "auto_bu"]
+FSTAT_NAMES = ["auto_nscore_td", "auto_nscore_bu"]  # sums over pairs (rank order: not bitwise)
+
+
+def shard_units(n: int, pairs, units: str, world: int, *, n_chunks: int = 1, s_min: int = 64,
+                s_max: int = 512):
+    """Work units and their LPT assignment.  units = "pair": one unit per pair, cost = the w^2-weighted
+    first-layer proxy (equal for equal-length pairs -> round robin); "pair_chunk": one unit per (pair,
+    chunk) of the Alg. 4 plan, cost proportional to the chunk length.  Returns per rank a list of calls
+    (pair indices, chunk range or None)."""
+    if units == "pair":
+        cost = [pair_cost(n, s_max, s_min)] * len(pairs)
+        return [[(idx, None)] if idx else [] for idx in lpt_assign(cost, world)]
+    plan = chunk_plan(n, max(1, n_chunks), s_max)
+    us = [(p, c) for p in range(len(pairs)) for c in range(len(plan))]
+    cost = [pair_cost(plan[c][1] - plan[c][0], s_max, s_min) for (_, c) in us]
+    out = []
+    for idx in lpt_assign(cost, world):
+        by_chunk = {}
+        for i in idx:
+            p, c = us[i]
+            by_chunk.setdefault(c, []).append(p)
+        out.append([(ps, (c, c + 1)) for c, ps in sorted(by_chunk.items())])  # one call per chunk index
+    return out
+
+
+def search_sharded(series, pairs, *, search=None, merge=None, device=None, units: str = "pair", **kw):
+    """SYCOS search over `pairs` sharded over the process group by work unit (shard_units); one NCCL
+    all_gather of the result windows (plus one of the counters); every rank returns the merged result list
+    sorted by (pair, method, t0) and the summed algorithm counters (+ this rank's kernel stats under
+    "kernel" when the compute reports them).  Results never depend on the number of ranks: pair ids key the
+    LAHC streams and (pair, chunk) units are independent searches merged by isycos_merge_windows (Alg. 4).
+    With (pair, chunk) units distinct_windows / distinct_pairs / eval_cost count per unit (a window in the
+    overlap of two chunks counts once per chunk)."""
     import torch
     import torch.distributed as dist
 
     search = search or _gpu_search
+    merge = merge or _gpu_merge
     world, rank = dist.get_world_size(), dist.get_rank()
     n = len(series[0])
     pairs = [tuple(p) if len(p) > 2 else (p[0], p[1], i) for i, p in enumerate(pairs)]
-    cost = [pair_cost(n, kw.get("s_max", 512), kw.get("s_min", 64))] * len(pairs)
-    mine = lpt_assign(cost, world)[rank]
-    res, st = search(series, [pairs[i] for i in mine], **kw) if mine else ([], {})
+    calls = shard_units(n, pairs, units, world, n_chunks=kw.get("n_chunks", 1), s_min=kw.get("s_min", 64),
+                        s_max=kw.get("s_max", 512))[rank]
+    res, st, kern = [], {}, {}
+    for idx, chunks in calls:
+        ckw = dict(kw)
+        if chunks is not None:
+            ckw["chunks"] = chunks
+        r, s = search(series, [pairs[i] for i in idx], **ckw)
+        res += r
+        for k_, v in s.items():
+            if k_ == "kernel":
+                for f, x in v.items():
+                    kern[f] = kern.get(f, 0) + x
+            else:
+                st[k_] = st.get(k_, 0) + v
     dev = device or ("cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu")
     payload = np.array([[r[0], r[1], r[2], r[3], r[4], r[5], r[6]] for r in res], np.float64).reshape(-1, 7)
     parts = _all_gather_variable(torch.from_numpy(payload).to(dev))
@@ -130,15 +188,15 @@ def search_sharded(series, pairs, *, search=None, device=None, **kw):
         for row in p.cpu().numpy():
             merged.append((int(row[0]), int(row[1]), int(row[2]), int(row[3]), float(row[4]), float(row[5]),
                            float(row[6])))
+    if units == "pair_chunk":
+        merged = merge(merged)
     merged.sort(key=lambda r: (r[0], r[1], r[2]))
-    stat_names = ["td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs", "bu_iterations",
-                  "bu_neighbors", "bu_noise_checks", "bu_prunes", "bu_accepted", "distinct_windows",
-                  "distinct_pairs", "eval_cost", "auto_td", "auto_bu"]
-    fstat_names = ["auto_nscore_td", "auto_nscore_bu"]  # sums over pairs (rank order: not bitwise)
-    vec = torch.tensor([int(st.get(k, 0)) for k in stat_names], dtype=torch.int64, device=dev)
-    fvec = torch.tensor([float(st.get(k, 0.0)) for k in fstat_names], dtype=torch.float64, device=dev)
+    vec = torch.tensor([int(st.get(k, 0)) for k in STAT_NAMES], dtype=torch.int64, device=dev)
+    fvec = torch.tensor([float(st.get(k, 0.0)) for k in FSTAT_NAMES], dtype=torch.float64, device=dev)
     dist.all_reduce(vec)
     dist.all_reduce(fvec)
-    out = {k: int(v) for k, v in zip(stat_names, vec.cpu().tolist())}
-    out.update({k: float(v) for k, v in zip(fstat_names, fvec.cpu().tolist())})
+    out = {k: int(v) for k, v in zip(STAT_NAMES, vec.cpu().tolist())}
+    out.update({k: float(v) for k, v in zip(FSTAT_NAMES, fvec.cpu().tolist())})
+    if kern:
+        out["kernel"] = kern
     return merged, out

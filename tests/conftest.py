@@ -6,6 +6,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# the oracle may spread the points of one large window over host threads (results do not depend on it)
+os.environ.setdefault("ORACLE_THREADS", str(min(16, os.cpu_count() or 1)))
 
 
 def pytest_configure(config):

@@ -55,7 +55,7 @@ def test_kernels_use_bulk_copy(capi):
 
 
 def test_abi_version(capi):
-    assert capi.isycos_abi_version() == 2
+    assert capi.isycos_abi_version() == 3
 
 
 def test_validation_before_gpu(capi):
@@ -96,3 +96,35 @@ def test_product_path_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"\boracle\b\s*(import|\.)|import\s+oracle|from\s+oracle", src), f
                 assert "oracle.cpp" not in src and "liboracle" not in src, f
+
+
+def test_merge_windows_rule(capi):
+    """isycos_merge_windows (Alg. 4 chunk merge, reading R20): per (pair, method), greedy by (nmi desc,
+    mi desc, t0 asc, t1 asc), keep if disjoint; host logic, no GPU needed."""
+    R = [(0, 1, 32, 96, 1.0, 2.0, 0.9), (0, 1, 36, 100, 5.0, 9.0, 0.5),   # higher nmi wins
+         (0, 2, 32, 96, 2.0, 2.0, 1.0), (0, 2, 36, 100, 3.0, 3.0, 1.0),   # nmi tie: higher mi
+         (1, 1, 36, 100, 2.0, 2.0, 1.0), (1, 1, 32, 96, 2.0, 2.0, 1.0),   # full tie: smaller t0
+         (1, 1, 100, 164, 0.5, 1.0, 0.3), (1, 1, 10, 20, 0.1, 1.0, 0.2)]  # disjoint ones kept
+    got = capi.isycos_merge_windows(R)
+    assert [(r[0], r[1], r[2], r[3]) for r in got] == [(0, 1, 32, 96), (0, 2, 36, 100), (1, 1, 10, 20),
+                                                        (1, 1, 32, 96), (1, 1, 100, 164)]
+    assert capi.isycos_merge_windows([]) == []
+
+
+def test_chunk_selection_validation(capi):
+    x = np.zeros(256, np.float32)
+    for kw in (dict(chunks=(0, 3)), dict(chunks=(1, 1)), dict(chunks=(-1, 1)), dict(chunks=(0, 1), method=4)):
+        with pytest.raises(capi.IsycosError) as ei:
+            capi.isycos_search([x, x], [(0, 1)], s_min=16, s_max=64, n_chunks=2, **kw)
+        assert ei.value.code == capi.E_INVAL, kw
+
+
+def test_binding_rejects_mismatched_buffers(capi):
+    x = np.zeros(64, np.float32)
+    w = np.array([[0, 32]], np.int64)
+    with pytest.raises(TypeError):   # an output buffer of the wrong dtype would be written past its end
+        capi.isycos_mi_batch_ex(x, x, w, 4, out={"mi": np.zeros(1, np.float32)})
+    with pytest.raises(ValueError):
+        capi.isycos_mi_batch_ex(x, x, w, 4, out={"mi": np.zeros(0)})
+    with pytest.raises(ValueError):
+        capi.isycos_mi_batch_ex(x, np.zeros(63, np.float32), w, 4)

@@ -34,10 +34,20 @@ def _oracle_mi_batch(x, y, W, k):
 def _oracle_search(series, pairs, **kw):
     import oracle
 
+    ch = kw.pop("chunks", None)
+    if ch is not None:
+        kw["chunk_begin"], kw["chunk_end"] = ch
     P = oracle.make_params(None, **{k: v for k, v in kw.items() if k in (
         "k", "method", "noise", "p", "h", "t_max_idle", "n_chunks", "s_min", "s_max", "sigma", "tau_ratio",
-        "seed")})
+        "seed", "chunk_begin", "chunk_end")})
     return oracle.search(series, pairs, P)
+
+
+def _cpu_merge(results):
+    # the product's host-side chunk merge (isycos_merge_windows: no GPU involved)
+    from paper_2204_09131_b200 import isycos_merge_windows
+
+    return isycos_merge_windows(results)
 
 
 def _worker(rank, world, port, task, q):
@@ -58,6 +68,12 @@ def _worker(rank, world, port, task, q):
             W = datagen.sweep_windows(len(x), [64, 128, 256], 24)
             out = idist.sweep_sharded(x, y, W, 4, mi_batch=_oracle_mi_batch, device="cpu")
             q.put((rank, {f: out[f].tolist() for f in out}))
+        elif task == "chunks":
+            wl = datagen.cfg1()
+            res, st = idist.search_sharded(wl.series, [(0, 1, 7)], search=_oracle_search, merge=_cpu_merge,
+                                           device="cpu", units="pair_chunk", k=4, s_min=64, s_max=256,
+                                           method=3, noise=1, n_chunks=3)
+            q.put((rank, (res, st)))
         else:
             wl = datagen.cfg4(n=6000, n_series=4, n_planted=1)
             pairs = [(a, b, 10 + i) for i, (a, b) in enumerate(wl.pairs)]
@@ -121,3 +137,29 @@ def test_search_sharded_world2_equals_single(orc):
                 assert st[f] == pytest.approx(v, rel=1e-12, abs=1e-12), f
             else:
                 assert st[f] == v, f
+
+
+def test_search_pair_chunk_units_world2_equals_single(orc):
+    """(pair, chunk) units (Alg. 4 line 14) split over 2 ranks, gathered and merged by
+    isycos_merge_windows, equal the single-process n_chunks = 3 search."""
+    out = _run("chunks", 2)
+    wl = datagen.cfg1()
+    ref, rst = _oracle_search(wl.series, [(0, 1, 7)], k=4, s_min=64, s_max=256, method=3, noise=1, n_chunks=3)
+    assert len(ref) > 0
+    for rank in (0, 1):
+        res, st = out[rank]
+        assert res == ref
+        for f in ("td_windows", "td_noise_checks", "td_skips", "td_accepted", "bu_climbs", "bu_iterations",
+                  "bu_neighbors", "bu_noise_checks", "bu_prunes", "bu_accepted"):
+            assert st[f] == rst[f], f
+
+
+def test_shard_units_cover_every_unit():
+    from paper_2204_09131_b200 import dist as idist
+
+    for world in (1, 2, 3, 8):
+        calls = idist.shard_units(10_000, [(0, 1)] * 5, "pair_chunk", world, n_chunks=4, s_min=64, s_max=512)
+        seen = sorted((p, c[0]) for r in calls for (ps, c) in r for p in ps)
+        assert seen == [(p, c) for p in range(5) for c in range(4)]
+        calls = idist.shard_units(10_000, [(0, 1)] * 5, "pair", world)
+        assert sorted(p for r in calls for (ps, _) in r for p in ps) == list(range(5))
