@@ -77,6 +77,8 @@ enum {
                                results are bit-identical either way — an A/B and test knob */
 #define ISYCOS_F_PROFILE_SORTED_ONLY 8u /* with ISYCOS_F_PROFILE: events around sorted-path launches only */
 #define ISYCOS_F_PROFILE_BRUTE_ONLY 16u  /* with ISYCOS_F_PROFILE: events around brute-force launches only */
+#define ISYCOS_F_NO_BLOCK 32u /* no NEXT-3 shared-block sorts (every sorted-path window sorted from scratch);
+                                 A/B knob, results identical */
 #define ISYCOS_F_UNFUSED 4u /* sorted-marginal windows always take the throughput form (sort kernel, then
                                scan kernel), never the fused latency kernel; results identical */
 
@@ -104,6 +106,9 @@ typedef struct {
     /* isycos_search with ISYCOS_F_PROFILE times every ISYCOS_PROFILE_EVERY-th round (env, default 1):
      * the work of the profiled rounds, to divide by the *_kernel_ms above */
     int64_t profiled_rounds, prof_brute_point_pairs, prof_scan_steps, prof_search_probes;
+    /* NEXT-3 (incremental MI, GPU analogue): windows whose sorted layout was merged from shared
+     * beta-blocks (each block sorted once per batch), and the block points sorted */
+    int64_t block_windows, block_points;
 } isycos_kernel_stats;
 
 /*

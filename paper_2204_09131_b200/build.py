@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libisycos.so")
-SOURCES = ["ksg_small.cu", "ksg_tile.cu", "ksg_sorted.cu", "ksg_fused.cu", "ksg_wsorted.cu", "ksg_misc.cu",
+SOURCES = ["ksg_small.cu", "ksg_tile.cu", "ksg_lat.cu", "ksg_sorted.cu", "ksg_fused.cu", "ksg_wsorted.cu", "ksg_misc.cu",
            "engine.cu", "search.cpp", "capi.cpp"]
 HEADERS = ["engine.h", "ksg_device.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

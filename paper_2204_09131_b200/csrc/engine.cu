@@ -10,6 +10,8 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <numeric>
+#include <unordered_map>
 
 #include "engine.h"
 
@@ -70,6 +72,8 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
     s->prof_brute_point_pairs += prof_brute_pairs;
     s->prof_scan_steps += prof_scan_steps;
     s->prof_search_probes += prof_probes;
+    s->block_windows += block_windows;
+    s->block_points += block_points;
 }
 
 // ---------------------------------------------------------------- engine registry (one per device)
@@ -131,6 +135,9 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_FUSED_SMALL_MIN_W")) fused_small_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED_MAX_PTS")) fused_max_pts_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
+    if (const char* m = std::getenv("ISYCOS_BLOCK_SORT")) block_sort_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_LAT_SPLIT")) lat_split_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_SCAN_UNIFIED")) scan_unified_ = std::atoi(m);
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
@@ -190,7 +197,8 @@ Status Engine::ensure_psi(int64_t w_max, cudaStream_t st) {
     return Status{};
 }
 
-Status Engine::ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists) {
+Status Engine::ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists,
+                               int64_t extra_bytes) {
     if (S.acc_cap < n_wins) {
         int64_t c = std::max<int64_t>(n_wins, S.acc_cap * 2);
         cudaFree(S.acc);
@@ -216,7 +224,7 @@ Status Engine::ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t
         S.ddrec_cap = c;
     }
     const int64_t bytes = 64 + n_pairs * (int64_t)sizeof(PairPtrs) + n_wins * (int64_t)sizeof(KsgWin) +
-                          n_lists * 4 + n_items * (int64_t)sizeof(KsgItem) + 16 * 64;
+                          n_lists * 4 + n_items * (int64_t)sizeof(KsgItem) + extra_bytes + 16 * 64;
     if (S.dstage_cap < bytes) {
         int64_t c = std::max<int64_t>(bytes, S.dstage_cap * 2);
         cudaFree(S.dstage);
@@ -322,12 +330,20 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // walking 32R points (brute force) or sorting and scanning them (warp-sorted) would set the latency
     // (all of a round's latency-mode windows go into one launch: per-class launches measured slower)
     // (windows >= fused_small_min_w_ take the fused sort+scan kernel when the round is in latency mode)
+    auto& lat = bins_.lat;
+    lat.clear();
+    const int lat_pts = lat_points_per_cta();
     auto to_latency = [&](std::vector<int32_t>& v) {
         for (int32_t q : v) {
             const int w = wins[q].w;
             if (fuse && w >= fused_small_min_w_) {
                 fused.push_back(q);
                 while (fused_n2 < w) fused_n2 <<= 1;
+                continue;
+            }
+            if (lat_split_on_ && variant == 0 && w <= 256) {  // 8 lanes per point (KSG-1)
+                lat.push_back(q);
+                n_items += (w + lat_pts - 1) / lat_pts;
                 continue;
             }
             tile[2].push_back(q);
@@ -339,6 +355,90 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         if (!small[s].empty() && (int64_t)small[s].size() < lat_windows_) to_latency(small[s]);
     for (int e = 0; e < 3; ++e)
         if (!wsorted[e].empty() && (int64_t)wsorted[e].size() < lat_windows_) to_latency(wsorted[e]);
+    // NEXT-3 block plan (the GPU analogue of the paper's incremental MI): sorted-path windows of one
+    // (pair, size) whose starts differ by d share beta-blocks, beta = the power-of-two part of gcd(d, w) in
+    // [256, kSortedMaxW] (TD: the delta-grid of a partition, delta = s/4, shared by the layer's windows and
+    // their noise sub-windows; sweeps: the stride).  Each block is sorted once per batch; its windows merge
+    // the sorted blocks (the merge levels from beta up) instead of sorting from scratch.
+    auto& wbeta = bins_.beta;
+    auto& blks = bins_.blks;
+    auto& segb = bins_.segb;
+    blks.clear();
+    segb.clear();
+    wbeta.assign(sorted.size(), 0);
+    std::vector<int64_t> wboff;
+    int blk_beta_max = 0;
+    int64_t blk_store = 0, blk_pts = 0, blk_windows = 0;
+    if (block_sort_on_ && !(flags & ISYCOS_F_NO_BLOCK) && sorted.size() >= 2) {
+        auto& ord = bins_.ord;
+        ord.resize(sorted.size());
+        std::iota(ord.begin(), ord.end(), 0);
+        std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t c) {
+            const KsgWin& A = wins[sorted[a]];
+            const KsgWin& C = wins[sorted[c]];
+            if (A.pair != C.pair) return A.pair < C.pair;
+            if (A.w != C.w) return A.w < C.w;
+            return A.t0 < C.t0;
+        });
+        for (size_t i = 0; i + 1 < ord.size(); ++i) {
+            const KsgWin& A = wins[sorted[ord[i]]];
+            const KsgWin& C = wins[sorted[ord[i + 1]]];
+            if (A.pair != C.pair || A.w != C.w || C.t0 == A.t0) continue;
+            const int64_t g = std::gcd<int64_t>(C.t0 - A.t0, (int64_t)A.w);
+            int64_t bt = g & -g;
+            if (bt > kSortedMaxW) bt = kSortedMaxW;
+            if (bt < 256) continue;
+            wbeta[ord[i]] = std::max<int32_t>(wbeta[ord[i]], (int32_t)bt);
+            wbeta[ord[i + 1]] = std::max<int32_t>(wbeta[ord[i + 1]], (int32_t)bt);
+        }
+        struct Grid {
+            int64_t jmin = INT64_MAX, jmax = -1, off = 0;
+            std::vector<char> need;
+        };
+        std::unordered_map<uint64_t, Grid> grids;
+        auto gkey = [](const KsgWin& W, int32_t bt) {
+            int lg = 0;
+            while ((1 << lg) < bt) ++lg;
+            return ((uint64_t)(uint32_t)W.pair << 17) | ((uint64_t)lg << 13) | (uint64_t)(W.t0 % bt);
+        };
+        for (size_t b = 0; b < sorted.size(); ++b) {
+            const int32_t bt = wbeta[b];
+            if (!bt) continue;
+            const KsgWin& W = wins[sorted[b]];
+            Grid& G = grids[gkey(W, bt)];
+            const int64_t j0 = W.t0 / bt;
+            G.jmin = std::min(G.jmin, j0);
+            G.jmax = std::max(G.jmax, j0 + W.w / bt - 1);
+        }
+        for (auto& kv : grids) {
+            const int32_t bt = 1 << ((kv.first >> 13) & 15);
+            kv.second.off = blk_store;
+            kv.second.need.assign(kv.second.jmax - kv.second.jmin + 1, 0);
+            blk_store += (kv.second.jmax - kv.second.jmin + 1) * bt;
+        }
+        wboff.assign(sorted.size(), 0);
+        for (size_t b = 0; b < sorted.size(); ++b) {
+            const int32_t bt = wbeta[b];
+            if (!bt) continue;
+            const KsgWin& W = wins[sorted[b]];
+            Grid& G = grids[gkey(W, bt)];
+            const int64_t j0 = W.t0 / bt;
+            for (int64_t j = j0; j < j0 + W.w / bt; ++j) G.need[j - G.jmin] = 1;
+            wboff[b] = G.off + (j0 - G.jmin) * bt;
+            ++blk_windows;
+            blk_beta_max = std::max(blk_beta_max, bt);
+        }
+        for (auto& kv : grids) {
+            const int32_t bt = 1 << ((kv.first >> 13) & 15);
+            const int32_t pair = (int32_t)(kv.first >> 17);
+            const int64_t o = (int64_t)(kv.first & 8191);
+            for (size_t j = 0; j < kv.second.need.size(); ++j)
+                if (kv.second.need[j]) {
+                    blks.push_back(KsgBlk{o + (kv.second.jmin + (int64_t)j) * bt, kv.second.off + (int64_t)j * bt, pair, bt});
+                    blk_pts += bt;
+                }
+        }
+    }
     // sorted scan: 1024 points per CTA when the batch fills the GPU (better lane balance in the per-warp
     // work queues), else 256 (more CTAs per window: latency-bound rounds)
     const int ppc = spts >= (int64_t)148 * 8 * 1024 ? sorted_ppc_ : 256;
@@ -358,12 +458,15 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
 
     {
         Status s = ensure_capacity(S, n + 1, n_items + n_sitems + n_segs + n_mblocks + n_fitems, n_pairs,
-                                   n_lists + 2 * (int64_t)sorted.size() + 16);
+                                   n_lists + 2 * (int64_t)sorted.size() + 16,
+                                   n_segs * (int64_t)sizeof(KsgSegB) + (int64_t)blks.size() * (int64_t)sizeof(KsgBlk) + 128);
         if (!s.ok()) return s;
     }
     // scratch per sorted point: P2 (8) | OX (4) | YS (4) | TX (4) | TI (4) | TY (4)
-    if (spts > 0 && S.sscratch_cap < spts * 28) {
-        const int64_t c = std::max<int64_t>(spts * 28, S.sscratch_cap * 2);
+    const int64_t blk_base = (spts * 28 + 15) & ~int64_t(15);  // block keys after the scan layout: BX (8) | BY (4)
+    const int64_t scratch_need = blk_base + blk_store * 12;
+    if (spts > 0 && S.sscratch_cap < scratch_need) {
+        const int64_t c = std::max<int64_t>(scratch_need, S.sscratch_cap * 2);
         cudaFree(S.sscratch);
         S.sscratch = nullptr;
         ISY_CK(cudaMalloc(&S.sscratch, c));
@@ -383,7 +486,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const int64_t off_sitems = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
     const int64_t off_segs = align64(off_sitems + n_sitems * (int64_t)sizeof(KsgItem));
     const int64_t off_mblk = align64(off_segs + n_segs * (int64_t)sizeof(KsgItem));
-    const int64_t total = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
+    const int64_t off_segb = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
+    const int64_t off_blks = align64(off_segb + (blks.empty() ? 0 : n_segs) * (int64_t)sizeof(KsgSegB));
+    const int64_t total = align64(off_blks + (int64_t)blks.size() * (int64_t)sizeof(KsgBlk));
     std::memcpy(S.hstage + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
     std::memcpy(S.hstage + off_wins, wins, n * sizeof(KsgWin));
     int64_t list_off[4], wlist_off[3];
@@ -413,7 +518,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         std::memcpy(S.hstage + off_slist, sorted.data(), sorted.size() * 4);
         std::memcpy(S.hstage + off_soff, soff.data(), soff.size() * 8);
     }
-    int64_t item_off[3];
+    int64_t item_off[3], item_off_lat = 0, n_litems = 0;
     {
         KsgItem* ip = reinterpret_cast<KsgItem*>(S.hstage + off_items);
         int64_t c = 0;
@@ -425,19 +530,31 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
                 for (int i0 = 0; i0 < w; i0 += kTileThreads * tr) ip[c++] = KsgItem{q, i0};
             }
         }
+        item_off_lat = c;
+        for (int32_t q : lat) {
+            const int w = wins[q].w;
+            for (int i0 = 0; i0 < w; i0 += lat_pts) ip[c++] = KsgItem{q, i0};
+        }
+        n_litems = c - item_off_lat;
         KsgItem* sp = reinterpret_cast<KsgItem*>(S.hstage + off_sitems);
         KsgItem* sg = reinterpret_cast<KsgItem*>(S.hstage + off_segs);
         KsgItem* mb = reinterpret_cast<KsgItem*>(S.hstage + off_mblk);
         int64_t cs = 0, cm = 0;
         c = 0;
+        KsgSegB* sbp = reinterpret_cast<KsgSegB*>(S.hstage + off_segb);
         for (size_t b = 0; b < sorted.size(); ++b) {
             const int w = wins[sorted[b]].w;
             for (int i0 = 0; i0 < w; i0 += ppc) sp[c++] = KsgItem{(int32_t)b, i0};
-            for (int s0 = 0; s0 < w; s0 += kSortedMaxW) sg[cs++] = KsgItem{(int32_t)b, s0};
+            for (int s0 = 0; s0 < w; s0 += kSortedMaxW) {
+                if (!blks.empty())  // the segment's blocks are contiguous in the block storage (s0 % beta == 0)
+                    sbp[cs] = wbeta[b] ? KsgSegB{wboff[b] + s0, wbeta[b], 0} : KsgSegB{0, 0, 0};
+                sg[cs++] = KsgItem{(int32_t)b, s0};
+            }
             if (w > kSortedMaxW)
                 for (int i0 = 0; i0 < w; i0 += kMergePts) mb[cm++] = KsgItem{(int32_t)b, i0};
         }
     }
+    if (!blks.empty()) std::memcpy(S.hstage + off_blks, blks.data(), blks.size() * sizeof(KsgBlk));
     // one H2D copy of the packed descriptors (kernels reading them from mapped host memory instead
     // measured 20 % slower on cfg2: a PCIe round trip on every CTA's critical path)
     char* dbase = S.dstage;
@@ -466,7 +583,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     L.two = 2;
     L.sorted_ppc = ppc;
     L.fused_n2 = fused_n2;
-    L.pad3_ = 0;
+    L.scan_unified = scan_unified_;
     const int32_t* dlists = reinterpret_cast<const int32_t*>(dbase + off_lists);
     const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dbase + off_items);
 
@@ -481,6 +598,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
 
     for (int s = 0; s < 3; ++s)
         for (int32_t q : tile[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
+    for (int32_t q : lat) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
     for (int32_t q : fused) {
         int lg = 0;
         while ((1 << lg) < wins[q].w) ++lg;
@@ -571,10 +689,19 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         float* TY = reinterpret_cast<float*>(S.sscratch + spts * 24);
         const KsgItem* dsg = reinterpret_cast<const KsgItem*>(dbase + off_segs);
         const KsgItem* dmb = reinterpret_cast<const KsgItem*>(dbase + off_mblk);
-        Status r = launch(0, n_mblocks ? 3 : 2, [&](cudaStream_t sg) {
+        const KsgSegB* dsb = reinterpret_cast<const KsgSegB*>(dbase + off_segb);
+        const KsgBlk* dbk = reinterpret_cast<const KsgBlk*>(dbase + off_blks);
+        unsigned long long* BX = reinterpret_cast<unsigned long long*>(S.sscratch + blk_base);
+        unsigned* BY = reinterpret_cast<unsigned*>(S.sscratch + blk_base + blk_store * 8);
+        Status r = launch(0, (n_mblocks ? 3 : 2) + (blks.empty() ? 0 : 1), [&](cudaStream_t sg) {
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
-                                 W2, dsi, (int32_t)n_sitems, sg);
+                                 W2, dsi, (int32_t)n_sitems, sg, dsb, dbk, (int32_t)blks.size(), blk_beta_max, BX, BY);
         });
+        if (!r.ok()) return r;
+    }
+    if (!lat.empty()) {
+        const KsgItem* ip = ditems + item_off_lat;
+        Status r = launch(1, 1, [&](cudaStream_t sg) { return launch_ksg_lat(L, ip, (int32_t)n_litems, sg); });
         if (!r.ok()) return r;
     }
     for (int s : {1, 0, 2}) {
@@ -615,6 +742,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     for (auto& v : wsorted)
         for (int32_t q : v) spoints += wins[q].w;
     S.spts = spoints;
+    S.block_windows = blk_windows;
+    S.block_points = blk_pts;
     return Status{};
 }
 
@@ -642,6 +771,8 @@ Status Engine::collect(int si, KsgRec* recs_host, BatchStats* bs) {
         bs->sorted_points += S.spts;
         bs->brute_pairs += S.brute_pairs;
         bs->search_probes += S.probes;
+        bs->block_windows += S.block_windows;
+        bs->block_points += S.block_points;
         if (S.profile) {
             bs->prof_rounds += 1;
             bs->prof_brute_pairs += S.brute_pairs;

@@ -35,6 +35,19 @@ struct KsgItem {             // one (window, i-tile) work item of the tile kerne
     int32_t i0;
 };
 
+struct KsgBlk {             // NEXT-3 shared block: beta points [t, t + beta) of a pair, sorted once per batch
+    int64_t t;
+    int64_t boff;            // offset (points) of its sorted keys in the block storage
+    int32_t pair;
+    int32_t beta;
+};
+
+struct KsgSegB {            // per sort segment: its first block's keys (beta = 0: sort from scratch)
+    int64_t boff;
+    int32_t beta;
+    int32_t pad;
+};
+
 struct KsgRec {              // per-window result (56 B), written by the kernels straight into mapped pinned host memory
     double mi, h, nmi;
     long long s_psi, s_log;
@@ -66,7 +79,7 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
     int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
     int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
-    int32_t pad3_;
+    int32_t scan_unified;    // sorted-path phase A: 1 one block per iteration from one side (default), 0 both sides
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -85,12 +98,18 @@ constexpr int kFusedThreads = 512;       // threads per fused CTA (16 warps: one
 // Launchers (ksg_*.cu).  Return cudaGetLastError().
 cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
 cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st);
+// latency mode, KSG-1, w <= 256: 8 lanes per point (ksg_lat.cu); items {window, first point}, 32 points each
+cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, cudaStream_t st);
+int lat_points_per_cta();
 // sorted path: sort kernel over segments {list pos, start}, XL rank merge over blocks {list pos, start},
 // then the scan kernel over `items` {list pos, first point}
+// NEXT-3: blocks {pair, t, beta} are sorted first into BX (x keys) / BY (y keys); segments with segb[i].beta > 0
+// merge their sorted blocks instead of sorting from scratch (blk_beta_max sizes the block-sort CTAs)
 cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const KsgItem* segs,
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
-                          int32_t n_items, cudaStream_t st);
+                          int32_t n_items, cudaStream_t st, const KsgSegB* segb, const KsgBlk* blks,
+                          int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY);
 // small windows on the sorted path: one warp per window, E = 2, 4, 8 keys per lane (w <= 32 E)
 cudaError_t launch_wsorted(const KsgLaunch& L, const int32_t* list, int32_t n, int E, cudaStream_t st);
 // fused latency path: items {list pos, slice start}; slices of fused_ppc(w, gmax) points
@@ -125,6 +144,7 @@ struct BatchStats {
     int64_t windows = 0, point_pairs = 0, launches = 0, ksg_launches = 0, rounds = 0;
     int64_t scan_steps = 0, sorted_windows = 0, sorted_points = 0;
     int64_t brute_pairs = 0, search_probes = 0;
+    int64_t block_windows = 0, block_points = 0;  // NEXT-3: windows merged from shared blocks, block points sorted
     double sorted_ms = 0.0, brute_ms = 0.0;
     int64_t prof_rounds = 0, prof_brute_pairs = 0, prof_scan_steps = 0, prof_probes = 0;
     double kernel_ms = 0.0;
@@ -193,12 +213,14 @@ private:
         bool busy = false, profile = false;
         cudaStream_t st = nullptr;
         int64_t n = 0, pp = 0, brute_pairs = 0, probes = 0, sorted_windows = 0, spts = 0;
+        int64_t block_windows = 0, block_points = 0;
         int n_ksg = 0, n_launch = 0;
         std::vector<int> launch_cls;
     };
 
     Status ensure_psi(int64_t w_max, cudaStream_t st);
-    Status ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists);
+    Status ensure_capacity(Slot& S, int64_t n_wins, int64_t n_items, int32_t n_pairs, int64_t n_lists,
+                           int64_t extra_bytes);
 
     int dev_ = -1;
     cudaStream_t stream_ = nullptr;
@@ -213,9 +235,15 @@ private:
     int* dflag_ = nullptr;
     Slot slots_[2];
     struct Bins {                    // size-class lists of the batch being packed (reused)
-        std::vector<int32_t> small[4], tile[3], sorted, fused, wsorted[3];
+        std::vector<int32_t> small[4], tile[3], sorted, fused, wsorted[3], lat;
         std::vector<int64_t> soff;
+        std::vector<int32_t> ord, beta;      // NEXT-3 block plan scratch
+        std::vector<KsgBlk> blks;
+        std::vector<KsgSegB> segb;
     } bins_;
+    int32_t scan_unified_ = 1;       // ISYCOS_SCAN_UNIFIED (A/B knob; results identical)
+    bool lat_split_on_ = true;       // latency-mode small windows on the 8-lanes-per-point kernel (ISYCOS_LAT_SPLIT=0: tile R=1)
+    bool block_sort_on_ = true;      // NEXT-3 shared-block sorts (env ISYCOS_BLOCK_SORT=0 disables; A/B knob)
     bool sorted_on_ = true;
     bool fused_on_ = true;           // sorted windows w <= kFusedMaxW: fused sort+scan kernel ...
     int64_t fused_max_pts_ = 148 * 2 * 512;  // ... when the batch has at most this many such points

@@ -617,7 +617,8 @@ __device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const f
 // not idle on their slowest lane (per-point scan lengths vary several-fold with the local density ratio).
 template <int K1>
 __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0, int wb, int we, float* eps_s,
-                                               unsigned long long& steps, int2* stop_s = nullptr) {
+                                               unsigned long long& steps, int2* stop_s = nullptr,
+                                               bool unified = true) {
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     constexpr int B = kScanB;
@@ -653,9 +654,43 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
         }
     };
     if (act) start(mloc);
+    bool toggle = false;
     while (__any_sync(0xffffffffu, act)) {
         bool fin = false;
-        if (act) {
+        if (act && unified) {
+            // one block per iteration from one side (alternating while both sides are open): every lane runs
+            // the same instruction stream whichever side it scans, so the warp does not diverge on the side
+            // tests.  |fl(x_j - x_i)| == fl(x_i - x_j) for x_j <= x_i (IEEE subtraction is antisymmetric), so
+            // both sides use the same distance code; the sentinels give +inf either way.
+            const bool useL = lact && (!ract || toggle);
+            toggle = !toggle;
+            const int base = useL ? lj : rj;
+            const int stp = useL ? -1 : 1;
+            float d[B], far = 0.f;
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const float2 c = P2[base + stp * u];
+                const float dx = fabsf(c.x - xi);
+                d[u] = fmaxf(dx, fabsf(yi - c.y));
+                far = dx;
+            }
+            visit(d);
+            const float r = rk[K1 - 1];
+            if (useL) {
+                steps += max(0, min(B, lj + 1));
+                lj -= B;
+                lact = far < r;
+            } else {
+                steps += max(0, min(B, w - rj));
+                rj += B;
+                ract = far < r;
+            }
+            if (!lact && !ract) {
+                fin = true;
+                eps_s[mloc] = r;
+                if (stop_s) stop_s[mloc] = make_int2(lj, rj);
+            }
+        } else if (act) {
             if (lact) {
                 float d[B], far = 0.f;
 #pragma unroll
@@ -770,7 +805,7 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
     const int wb = min(warp * kPerWarp, cta_n);
     const int we = min(wb + kPerWarp, cta_n);
     unsigned long long steps = 0;
-    sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s);
+    sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s, L.scan_unified != 0);
     __syncthreads();
     long long sp = 0, sl = 0;
     int z = 0;

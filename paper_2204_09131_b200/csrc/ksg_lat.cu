@@ -1,0 +1,87 @@
+// Latency mode for small windows (w <= 256) in rounds too sparse to fill the GPU (a1-a6, KSG-1).
+//
+// The search rounds of a BU climb carry a few hundred small windows; one thread walking all w candidates
+// of its point sets the round's latency.  Here every point is owned by kLatP = 8 lanes of a warp: lane s
+// scans the candidate groups g = s, s + 8, ... (4 candidates per float4 group) with its own register
+// top-(k+1) list, the 8 lists are merged by a 3-step butterfly (each lane inserts its partner's k+1
+// entries: after the xor-1/2/4 exchanges every lane holds the (k+1) smallest of the union — the same
+// multiset order statistic as one lane scanning everything), then the marginal counts are split the same
+// way and summed by shuffles.  The critical path per window drops ~8x; results are bit-identical.
+#include "ksg_device.cuh"
+
+namespace isy {
+namespace {
+
+constexpr int kLatThreads = 256;
+constexpr int kLatP = 8;                              // lanes per point
+constexpr int kLatPts = kLatThreads / kLatP;          // points per CTA
+
+template <int K1>
+__global__ void __launch_bounds__(kLatThreads)
+    ksg_lat_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items) {
+    __shared__ __align__(16) float sx[256];
+    __shared__ __align__(16) float sy[256];
+    const KsgItem it = items[blockIdx.x];
+    const int q = it.win;
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    const float* gx = L.pairs[W.pair].x + W.t0;
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    const int wpad = (w + 3) & ~3;
+    for (int j = threadIdx.x; j < wpad; j += kLatThreads) {
+        sx[j] = j < w ? gx[j] : kInf;  // +inf pads: d = +inf, never inserted, never counted
+        sy[j] = j < w ? gy[j] : kInf;
+    }
+    __syncthreads();
+    const int s = threadIdx.x & (kLatP - 1);
+    const int i = it.i0 + (threadIdx.x >> 3);
+    const bool live = i < w;
+    const float xi0 = live ? sx[i] : 0.0f, yi0 = live ? sy[i] : 0.0f;
+    float xi[1] = {xi0}, yi[1] = {yi0};
+    float rk[1][K1];
+#pragma unroll
+    for (int m = 0; m < K1; ++m) rk[0][m] = kInf;
+    const int ng = wpad >> 2;
+    const float4* sx4 = reinterpret_cast<const float4*>(sx);
+    const float4* sy4 = reinterpret_cast<const float4*>(sy);
+    for (int g = s; g < ng; g += kLatP) knn_step<K1, 1, false>(xi, yi, rk, sx4[g], sy4[g]);
+    // butterfly merge of the 8 partial top lists (lanes of one point are 8 consecutive lanes)
+#pragma unroll
+    for (int off = 1; off < kLatP; off <<= 1) {
+        float other[K1];
+#pragma unroll
+        for (int m = 0; m < K1; ++m) other[m] = __shfl_xor_sync(0xffffffffu, rk[0][m], off);
+#pragma unroll
+        for (int m = 0; m < K1; ++m) topk_insert<K1>(rk[0], other[m]);
+    }
+    float eps[1] = {rk[0][K1 - 1]};
+    unsigned cx[1] = {0u}, cy[1] = {0u};
+    for (int g = s; g < ng; g += kLatP) count_step<1>(xi, yi, eps, eps, cx, cy, sx4[g], sy4[g], (unsigned)L.two);
+#pragma unroll
+    for (int off = 1; off < kLatP; off <<= 1) {
+        cx[0] += __shfl_xor_sync(0xffffffffu, cx[0], off);
+        cy[0] += __shfl_xor_sync(0xffffffffu, cy[0], off);
+    }
+    long long sp = 0, sl = 0;
+    int z = 0;
+    if (s == 0 && live) point_terms<1, false>(L, w, W.dbg_off, i, kLatPts, eps, cx, cy, sp, sl, z);
+    cta_finish(L, q, w, (w + kLatPts - 1) / kLatPts, sp, sl, z, 0ull);
+}
+
+template <int K1>
+cudaError_t lat_k(const KsgLaunch& L, const KsgItem* items, int32_t n, cudaStream_t st) {
+    ksg_lat_kernel<K1><<<n, kLatThreads, 0, st>>>(L, items, n);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int lat_points_per_cta() { return kLatPts; }
+
+cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, cudaStream_t st) {
+    if (n_items <= 0) return cudaSuccess;
+    if (L.variant != 0) return cudaErrorInvalidValue;  // KSG-2 latency windows take the tile kernel (R = 1)
+    ISY_K_CASES(lat_k, L, items, n_items, st)
+}
+
+}  // namespace isy

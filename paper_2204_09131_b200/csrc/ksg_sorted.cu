@@ -5,11 +5,54 @@
 namespace isy {
 namespace {
 
+// NEXT-3 (the GPU analogue of the paper's incremental MI): windows of one (pair, size) on a
+// common grid share their beta-point blocks; block_sort_kernel sorts every block ONCE per batch (x keys with
+// the absolute sample index, y keys), and the window's sort below starts from those sorted runs: it only
+// runs the merge levels from beta up (a delta-shifted window re-merges the blocks it shares with its
+// neighbours instead of re-sorting them).  Same keys, same total order: bit-identical layouts.
+__global__ void __launch_bounds__(1024) block_sort_kernel(const KsgLaunch L, const KsgBlk* __restrict__ blks,
+                                                          unsigned long long* __restrict__ BX,
+                                                          unsigned* __restrict__ BY) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const KsgBlk B = blks[blockIdx.x];
+    const int n2 = B.beta;  // power of two in [256, kSortedMaxW]
+    const float* gx = L.pairs[B.pair].x + B.t;
+    const float* gy = L.pairs[B.pair].y + B.t;
+    unsigned long long* X0 = reinterpret_cast<unsigned long long*>(sm);
+    unsigned long long* X1 = X0 + n2;
+    unsigned* Y0 = reinterpret_cast<unsigned*>(X1 + n2);
+    unsigned* Y1 = reinterpret_cast<unsigned*>(X0);  // y merges through the x buffers once x is out
+    chunk_sort<8>(gx, gy, n2, n2, X0, Y0, nullptr, threadIdx.x >> 5, threadIdx.x & 31, (int)B.t);
+    __syncthreads();
+    unsigned long long* xs = X0;
+    unsigned long long* xd = X1;
+    for (int r = 256; r < n2; r <<= 1) {
+        merge_level(xs, xd, n2, r);
+        __syncthreads();
+        unsigned long long* tx = xs;
+        xs = xd;
+        xd = tx;
+    }
+    for (int m = threadIdx.x; m < n2; m += blockDim.x) BX[B.boff + m] = xs[m];
+    __syncthreads();
+    unsigned* ys = Y0;
+    unsigned* yd = Y1;
+    for (int r = 256; r < n2; r <<= 1) {
+        merge_level(ys, yd, n2, r);
+        __syncthreads();
+        unsigned* ty = ys;
+        ys = yd;
+        yd = ty;
+    }
+    for (int m = threadIdx.x; m < n2; m += blockDim.x) BY[B.boff + m] = ys[m];
+}
+
 __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, const int32_t* __restrict__ list,
                                    const int64_t* __restrict__ soff, const KsgItem* __restrict__ segs,
                                    float2* __restrict__ P2, int32_t* __restrict__ OX, float* __restrict__ YS,
                                    float* __restrict__ TX, int32_t* __restrict__ TI, float* __restrict__ TY,
-                                   int W2) {
+                                   int W2, const KsgSegB* __restrict__ segb,
+                                   const unsigned long long* __restrict__ BX, const unsigned* __restrict__ BY) {
     extern __shared__ __align__(16) unsigned char sm[];
     const KsgItem sg = segs[blockIdx.x];  // win = position in the sorted list, i0 = segment start
     const int b = sg.win;
@@ -25,18 +68,31 @@ __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, co
     const float* gy = L.pairs[W.pair].y + W.t0;
     const int64_t o = soff[b];  // the window's region has kScanB spare entries on either side (scan sentinels)
     if (s0 == 0 && threadIdx.x < 2 * kScanB) put_sentinels(P2 + o, w, threadIdx.x);
+    const KsgSegB sb = segb ? segb[blockIdx.x] : KsgSegB{0, 0, 0};
     if (n2 >= 256) {
         // register chunk sorts (256 keys per warp) + merge-path levels in SMEM (the fused kernel's sort, ~2x
         // the SMEM-bandwidth-bound bitonic below).  x (with the window index) is merged and written out
-        // first, then y is merged through the freed x buffers: 20 n2 bytes of SMEM.
+        // first, then y is merged through the freed x buffers: 20 n2 bytes of SMEM.  Block mode: the runs of
+        // beta keys come sorted from block_sort_kernel (x keys carry the absolute index t0 + i).
         unsigned long long* X0 = reinterpret_cast<unsigned long long*>(sm);
         unsigned long long* X1 = X0 + n2;
         unsigned* Y0 = reinterpret_cast<unsigned*>(X1 + n2);
-        chunk_sort<8>(gx + s0, gy + s0, len, n2, X0, Y0, nullptr, threadIdx.x >> 5, threadIdx.x & 31, s0);
+        int r0 = 256;
+        unsigned isub = 0;  // index base of the keys (block mode: absolute sample index)
+        if (sb.beta > 0) {
+            for (int m = threadIdx.x; m < n2; m += blockDim.x) {
+                X0[m] = m < len ? BX[sb.boff + m] : ~0ull;
+                Y0[m] = m < len ? BY[sb.boff + m] : ~0u;
+            }
+            r0 = sb.beta;
+            isub = (unsigned)W.t0;
+        } else {
+            chunk_sort<8>(gx + s0, gy + s0, len, n2, X0, Y0, nullptr, threadIdx.x >> 5, threadIdx.x & 31, s0);
+        }
         __syncthreads();
         unsigned long long* xs = X0;
         unsigned long long* xd = X1;
-        for (int r = 256; r < n2; r <<= 1) {
+        for (int r = r0; r < n2; r <<= 1) {
             merge_level(xs, xd, n2, r);
             __syncthreads();
             unsigned long long* tx = xs;
@@ -46,7 +102,7 @@ __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, co
         for (int m = threadIdx.x; m < len; m += blockDim.x) {
             const unsigned long long v = xs[m];
             const float xv = unsortable((unsigned)(v >> 32));
-            const int32_t idx = (int32_t)(v & 0xffffffffu);
+            const int32_t idx = (int32_t)((unsigned)(v & 0xffffffffu) - isub);
             if (whole) {
                 P2[o + m] = make_float2(xv, gy[idx]);
                 OX[o + m] = idx;
@@ -58,7 +114,7 @@ __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, co
         __syncthreads();
         unsigned* ys = Y0;
         unsigned* yd = reinterpret_cast<unsigned*>(X0);  // x buffers are free now
-        for (int r = 256; r < n2; r <<= 1) {
+        for (int r = r0; r < n2; r <<= 1) {
             merge_level(ys, yd, n2, r);
             __syncthreads();
             unsigned* ty = ys;
@@ -170,18 +226,28 @@ cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* sof
 cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const KsgItem* segs,
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
-                          int32_t n_items, cudaStream_t st) {
+                          int32_t n_items, cudaStream_t st, const KsgSegB* segb, const KsgBlk* blks,
+                          int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY) {
     static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
     if (n_segs <= 0) return cudaSuccess;
     {
         cudaError_t e = smem_optin(reinterpret_cast<const void*>(sort_window_kernel), kSortedMaxW * 20);
+        if (e != cudaSuccess) return e;
+        e = smem_optin(reinterpret_cast<const void*>(block_sort_kernel), kSortedMaxW * 20);
+        if (e != cudaSuccess) return e;
+    }
+    if (n_blks > 0) {  // NEXT-3 shared blocks: sorted once, before the windows that merge them
+        const int bt = std::min(1024, std::max(64, blk_beta_max / 8));
+        block_sort_kernel<<<n_blks, bt, (size_t)blk_beta_max * 20, st>>>(L, blks, BX, BY);
+        cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     // one thread per 8 keys (= one merge-path output run; chunk sorts are 256 keys per warp): smaller CTAs
     // for small segments keep every warp busy and let more CTAs share an SM
     const int threads = std::min(1024, std::max(64, W2 / 8));
     const size_t smem = (size_t)W2 * 20;  // chunk + merge sort (bitonic for n2 < 256 needs 8 n2)
-    sort_window_kernel<<<n_segs, threads, smem, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2);
+    sort_window_kernel<<<n_segs, threads, smem, st>>>(L, list, soff, segs, P2, OX, YS, TX, TI, TY, W2,
+                                                      n_blks > 0 ? segb : nullptr, BX, BY);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (n_mblocks > 0) {

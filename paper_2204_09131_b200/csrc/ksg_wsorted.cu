@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     }
     __syncwarp();
     unsigned long long steps = 0;
-    sorted_phase_a<K1>(P2, w, 0, 0, w, seps[warp], steps);
+    sorted_phase_a<K1>(P2, w, 0, 0, w, seps[warp], steps, nullptr, L.scan_unified != 0);
     __syncwarp();
     long long sp = 0, sl = 0;
     int z = 0;

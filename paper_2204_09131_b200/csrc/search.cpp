@@ -128,7 +128,7 @@ struct FlatMap {
 
 struct PairCache {
     FlatMap map;
-    std::vector<uint64_t> pending;
+    std::vector<Entry*> pending;  // requested, not yet staged (entries never move)
 };
 
 // t_w ~ w log w per MI request: Alg. 3's deterministic runtime proxy (DESIGN reading R24)
@@ -163,22 +163,22 @@ struct AlgStats {
 // owning step commits, so speculative work never enters the algorithm-level counters.
 struct View {
     PairCache* c;
-    std::vector<uint64_t>* touched;
+    std::vector<Entry*>* touched;
     const Eval* get(int64_t t0, int64_t t1) {
         const uint64_t k = wkey(t0, t1);
         auto r = c->map.try_emplace(k);
         if (r.second) {
-            c->pending.push_back(k);
+            c->pending.push_back(r.first);
             return nullptr;
         }
         if (!r.first->ready) return nullptr;
-        touched->push_back(k);
+        touched->push_back(r.first);
         return &r.first->e;
     }
     void want(int64_t t0, int64_t t1) {
         const uint64_t k = wkey(t0, t1);
         auto r = c->map.try_emplace(k);
-        if (r.second) c->pending.push_back(k);
+        if (r.second) c->pending.push_back(r.first);
     }
     const Eval* peek(int64_t t0, int64_t t1) {  // no request, no consumption
         Entry* e = c->map.find(wkey(t0, t1));
@@ -186,8 +186,8 @@ struct View {
     }
 };
 
-void commit_touched(PairCache* c, const std::vector<uint64_t>& t) {
-    for (uint64_t k : t) c->map.find(k)->consumed = true;
+void commit_touched(PairCache*, const std::vector<Entry*>& t) {
+    for (Entry* e : t) e->consumed = true;
 }
 
 // ------------------------------------------------------------------ SYCOS_TD job
@@ -230,7 +230,7 @@ struct TdJob {
     }
 
     void request_layer(int64_t s) {
-        std::vector<uint64_t> dummy;
+        std::vector<Entry*> dummy;
         View v{cache, &dummy};
         for (auto [a, b] : parts)
             if (b - a >= s) request_grid(v, a, b, s, true);
@@ -244,7 +244,7 @@ struct TdJob {
         AlgStats ls;
         std::vector<isycos_result_window> lr;
         std::vector<std::pair<int64_t, int64_t>> next;
-        std::vector<uint64_t> touched;
+        std::vector<Entry*> touched;
         View v{cache, &touched};
         for (auto [a, b] : parts) {
             if (b - a < s) {
@@ -260,7 +260,7 @@ struct TdJob {
                 if (!e) {
                     // off the layer-start grid (an accept or a noise skip moved t by s, s % delta != 0):
                     // queue the rest of this partition anchored at t, so it costs one round, not one per window
-                    std::vector<uint64_t> dummy;
+                    std::vector<Entry*> dummy;
                     View w{cache, &dummy};
                     request_grid(w, t, b, s, !shifted);
                     return false;
@@ -347,7 +347,7 @@ struct Climb {
     bool pruned[2] = {false, false};
     Rng rng{0};
     AlgStats st;
-    std::vector<uint64_t> touched;
+    std::vector<Entry*> touched;
     bool accepted = false;
     bool finished = false;
     Eval fin{0, 0, 0};
@@ -617,7 +617,7 @@ struct BuJob {
     // chain will most likely re-anchor at max(t1, lo + s_min); start the climbs of that chain now.
     void speculate_anchor(const Climb& c) {
         if (P->anchor_lookahead <= 0 || c.state != 1 || c.idle < 1) return;
-        std::vector<uint64_t> none;
+        std::vector<Entry*> none;
         View v{cache, &none};
         const Eval* e = v.peek(c.t0, c.t1);
         if (!e || !(e->nmi >= P->sigma)) return;
@@ -892,7 +892,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
-    double eval_ms = 0.0, adv_ms = 0.0, wait_ms = 0.0;
+    double eval_ms = 0.0, adv_ms = 0.0, wait_ms = 0.0, dlv_ms = 0.0, ret_ms = 0.0, asm_ms = 0.0;
     int64_t round_no = 0;
     std::FILE* trace = nullptr;
     if (const char* tp = std::getenv("ISYCOS_TRACE")) trace = std::fopen(tp, "a");
@@ -940,6 +940,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         eval_ms += wms;
         wait_ms += wms;
         if (!s.ok()) return s;
+        const auto t_dl = clk::now();
         // records -> entries, pairs in parallel for big batches (each pair's records are a contiguous slice)
         pool.run(F.owners.size() >= 512 ? (int)F.pws.size() : 1, [&](int p) {
             if (F.owners.size() < 512) p = -1;
@@ -951,6 +952,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             }
         });
         for (PairWork* pw : F.pws) pw->inflight -= 1;
+        dlv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_dl).count();
         F.busy = false;
         F.owners.clear();
         F.pws.clear();
@@ -1018,7 +1020,8 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 pw->stage_w.clear();
                 pw->stage_o.clear();
                 if (!pw->finished()) {
-                    for (uint64_t k : pw->cache.pending) {
+                    for (Entry* en : pw->cache.pending) {
+                        const uint64_t k = en->key;
                         const int64_t t0 = key_t0(k), w = key_w(k);
                         if (t0 < 0 || t0 + w > n || w <= P.k) {  // never hand the kernels an out-of-range window
                             pw->stage_bad = true;
@@ -1026,87 +1029,117 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                             pw->bad_t1 = t0 + w;
                         }
                         pw->stage_w.push_back(KsgWin{t0, (int32_t)w, -1, -1});
-                        pw->stage_o.push_back(pw->cache.map.find(k));
+                        pw->stage_o.push_back(en);
                     }
                 }
                 pw->cache.pending.clear();
             });
             adv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_adv).count();
-            // retire finished pairs (none of their entries may be in flight)
-            for (size_t i = 0; i < active.size();) {
-                PairWork* pw = active[i].get();
-                if (pw->finished() && pw->inflight == 0) {
-                    pw->cache.pending.clear();  // leftover speculative requests of discarded climbs
-                    AlgStats ps;
-                    for (int m = 1; m <= 2; ++m) {
-                        std::vector<isycos_result_window> per;
-                        if (m == 1)
-                            for (auto& j : pw->td) {
-                                per.insert(per.end(), j.results.begin(), j.results.end());
-                                ps.add(j.stats);
-                            }
-                        else
-                            for (auto& j : pw->bu) {
-                                per.insert(per.end(), j.results.begin(), j.results.end());
-                                ps.add(j.stats);
-                            }
-                        if (!(pw->method & m)) continue;
-                        if (pw->kind == 1) {  // trial run: countWindows, |w| <= rho * s_max is small
-                            AutoState& A = autos[pw->auto_id];
-                            const double rho = P.auto_rho > 0.0 ? P.auto_rho : 0.5;
-                            for (const auto& r : per) {
-                                const bool small = (double)(r.t1 - r.t0) <= rho * (double)P.s_max;
-                                if (m == 1 && !small) A.nL_td += 1;
-                                if (m == 2 && small) A.nS_bu += 1;
-                            }
-                            continue;
+            // retire finished pairs (none of their entries may be in flight): the per-pair work (result merge,
+            // distinct-window count over the pair's cache, freeing the cache) runs on the host pool; the
+            // bookkeeping that orders results and feeds Alg. 3 stays sequential in admission order
+            const auto t_ret = clk::now();
+            struct Retired {
+                AlgStats ps;
+                std::vector<isycos_result_window> res;  // merged result windows (searches)
+                int64_t nL_td = 0, nS_bu = 0;           // Alg. 3 trial counts (trial runs)
+                int64_t dw = 0, dpp = 0;
+            };
+            std::vector<int32_t> fin;
+            for (size_t i = 0; i < active.size(); ++i)
+                if (active[i]->finished() && active[i]->inflight == 0) fin.push_back((int32_t)i);
+            std::vector<Retired> rt(fin.size());
+            pool.run((int)fin.size(), [&](int f) {
+                PairWork* pw = active[fin[f]].get();
+                Retired& R = rt[f];
+                pw->cache.pending.clear();  // leftover speculative requests of discarded climbs
+                for (int m = 1; m <= 2; ++m) {
+                    std::vector<isycos_result_window> per;
+                    if (m == 1)
+                        for (auto& j : pw->td) {
+                            per.insert(per.end(), j.results.begin(), j.results.end());
+                            R.ps.add(j.stats);
                         }
-                        if (chunk_sel) {  // merged by isycos_merge_windows once every chunk is gathered
-                            all.insert(all.end(), per.begin(), per.end());
-                            continue;
+                    else
+                        for (auto& j : pw->bu) {
+                            per.insert(per.end(), j.results.begin(), j.results.end());
+                            R.ps.add(j.stats);
                         }
-                        auto merged = merge_windows(per);
-                        all.insert(all.end(), merged.begin(), merged.end());
+                    if (!(pw->method & m)) continue;
+                    if (pw->kind == 1) {  // trial run: countWindows, |w| <= rho * s_max is small
+                        const double rho = P.auto_rho > 0.0 ? P.auto_rho : 0.5;
+                        for (const auto& r : per) {
+                            const bool small = (double)(r.t1 - r.t0) <= rho * (double)P.s_max;
+                            if (m == 1 && !small) R.nL_td += 1;
+                            if (m == 2 && small) R.nS_bu += 1;
+                        }
+                        continue;
                     }
-                    pw->cache.map.for_each([&](const Entry& en) {
-                        if (en.consumed) {
-                            const int64_t w = key_w(en.key);
-                            distinct_w += 1;
-                            distinct_pp += w * (w - 1);
-                            ps.eval_cost += wcost(w);
-                        }
-                    });
-
-                    total.add(ps);
-                    if (pw->kind == 1) {
-                        AutoState& A = autos[pw->auto_id];
-                        (pw->method == 1 ? A.cost_td : A.cost_bu) += ps.eval_cost;
-                        if (--A.left == 0) {
-                            // Alg. 3 lines 6-15, Eqs. 6-9 (fixed fp64 op order, as the oracle)
-                            const double alpha = P.auto_alpha > 0.0 ? P.auto_alpha : 0.5;
-                            const double tbar_td = (double)A.cost_td / (double)am;
-                            const double tbar_bu = (double)A.cost_bu / (double)am;
-                            const double tt_td = tbar_td / (tbar_bu + tbar_td);
-                            const double tt_bu = tbar_bu / (tbar_bu + tbar_td);
-                            double nl = 0.5, ns = 0.5;
-                            if (A.nS_bu + A.nL_td > 0) {
-                                nl = (double)A.nL_td / (double)(A.nS_bu + A.nL_td);
-                                ns = (double)A.nS_bu / (double)(A.nS_bu + A.nL_td);
-                            }
-                            const double beta = 1.0 - alpha;
-                            A.nscore_td = alpha * (1.0 / tt_td) + beta * nl;
-                            A.nscore_bu = alpha * (1.0 / tt_bu) + beta * ns;
-                            A.chosen = A.nscore_td > A.nscore_bu ? 1 : 2;
-                            queue.push_front(Unit{A.pair_idx, A.chosen, 0, -1, plan});
-                        }
+                    if (chunk_sel) {  // merged by isycos_merge_windows once every chunk is gathered
+                        R.res.insert(R.res.end(), per.begin(), per.end());
+                        continue;
                     }
-
-                    active.erase(active.begin() + i);
-                    progress = true;
-                } else {
-                    ++i;
+                    auto merged = merge_windows(per);
+                    R.res.insert(R.res.end(), merged.begin(), merged.end());
+                }
+                pw->cache.map.for_each([&](const Entry& en) {
+                    if (en.consumed) {
+                        const int64_t w = key_w(en.key);
+                        R.dw += 1;
+                        R.dpp += w * (w - 1);
+                        R.ps.eval_cost += wcost(w);
+                    }
+                });
+            });
+            for (size_t f = 0; f < fin.size(); ++f) {
+                PairWork* pw = active[fin[f]].get();
+                Retired& R = rt[f];
+                all.insert(all.end(), R.res.begin(), R.res.end());
+                distinct_w += R.dw;
+                distinct_pp += R.dpp;
+                total.add(R.ps);
+                if (pw->kind == 1) {
+                    AutoState& A = autos[pw->auto_id];
+                    A.nL_td += R.nL_td;
+                    A.nS_bu += R.nS_bu;
+                    (pw->method == 1 ? A.cost_td : A.cost_bu) += R.ps.eval_cost;
+                    if (--A.left == 0) {
+                        // Alg. 3 lines 6-15, Eqs. 6-9 (fixed fp64 op order, as the oracle)
+                        const double alpha = P.auto_alpha > 0.0 ? P.auto_alpha : 0.5;
+                        const double tbar_td = (double)A.cost_td / (double)am;
+                        const double tbar_bu = (double)A.cost_bu / (double)am;
+                        const double tt_td = tbar_td / (tbar_bu + tbar_td);
+                        const double tt_bu = tbar_bu / (tbar_bu + tbar_td);
+                        double nl = 0.5, ns = 0.5;
+                        if (A.nS_bu + A.nL_td > 0) {
+                            nl = (double)A.nL_td / (double)(A.nS_bu + A.nL_td);
+                            ns = (double)A.nS_bu / (double)(A.nS_bu + A.nL_td);
+                        }
+                        const double beta = 1.0 - alpha;
+                        A.nscore_td = alpha * (1.0 / tt_td) + beta * nl;
+                        A.nscore_bu = alpha * (1.0 / tt_bu) + beta * ns;
+                        A.chosen = A.nscore_td > A.nscore_bu ? 1 : 2;
+                        queue.push_front(Unit{A.pair_idx, A.chosen, 0, -1, plan});
+                    }
                 }
             }
+            if (!fin.empty()) {
+                std::vector<std::unique_ptr<PairWork>> dead;
+                size_t keep = 0, fi = 0;
+                for (size_t i = 0; i < active.size(); ++i) {
+                    if (fi < fin.size() && (int32_t)i == fin[fi]) {
+                        dead.push_back(std::move(active[i]));
+                        ++fi;
+                    } else {
+                        active[keep++] = std::move(active[i]);
+                    }
+                }
+                active.resize(keep);
+                pool.run((int)dead.size(), [&](int i) { dead[i].reset(); });  // free the caches in parallel
+                progress = true;
+            }
+            const auto t_asm = clk::now();
+            ret_ms += std::chrono::duration<double, std::milli>(t_asm - t_ret).count();
             // one batch of every pending window of every active pair (finished pairs: leftovers dropped)
             std::vector<PairPtrs> table;
             batch.clear();
@@ -1148,6 +1181,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             }
             F.offs.push_back((int64_t)batch.size());
             const auto t_ev = clk::now();
+            asm_ms += std::chrono::duration<double, std::milli>(t_ev - t_asm).count();
             // kernel timing samples every profile_every-th round (event records are host time per round)
             uint32_t fl_round = P.flags;
             if ((fl_round & ISYCOS_F_PROFILE) && P.profile_every > 1 && (round_no % P.profile_every) != 0)
@@ -1211,9 +1245,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         bs.host_ms = wall - eval_ms;
         bs.add_to(&stats->kernel);
         if (trace)
-            std::fprintf(trace, "# host: advance %.3f ms (%d threads), other %.3f ms, eval %.3f ms (collect wait %.3f), "
-                         "rounds %lld\n", adv_ms, pool.size(), wall - eval_ms - adv_ms, eval_ms, wait_ms,
-                         (long long)round_no);
+            std::fprintf(trace, "# host: advance %.3f ms (%d threads), other %.3f ms (deliver %.3f, retire %.3f, "
+                         "assemble %.3f), eval %.3f ms (collect wait %.3f), rounds %lld\n", adv_ms, pool.size(),
+                         wall - eval_ms - adv_ms, dlv_ms, ret_ms, asm_ms, eval_ms, wait_ms, (long long)round_no);
     }
     return Status{};
 }

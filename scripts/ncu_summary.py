@@ -102,20 +102,37 @@ def launches(path, dst):
     rows = [r for r in csv.reader(open(path)) if r]
     hdr = next(r for r in rows if r[0] == "ID")
     idx = {h: i for i, h in enumerate(hdr)}
-    agg = collections.defaultdict(lambda: [0, 0.0])
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0, 0.0])  # launches, us, grid sum, small grids, small us
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    per = collections.defaultdict(dict)
     for r in rows:
-        if r[0] == "ID" or len(r) != len(hdr) or r[idx["Metric Name"]] != "gpu__time_duration.sum":
+        if r[0] == "ID" or len(r) != len(hdr):
             continue
-        name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "")
-        agg[name][0] += 1
-        agg[name][1] += float(r[idx["Metric Value"]].replace(",", "")) * scale.get(r[idx["Metric Unit"]], 1.0)
+        m = r[idx["Metric Name"]]
+        v = float(r[idx["Metric Value"]].replace(",", ""))
+        if m == "gpu__time_duration.sum":
+            v *= scale.get(r[idx["Metric Unit"]], 1.0)
+        per[r[idx["ID"]]][m] = v
+        per[r[idx["ID"]]]["name"] = r[idx["Kernel Name"]].split("(")[0].replace("void ", "")
+    for d in per.values():
+        if "gpu__time_duration.sum" not in d:
+            continue
+        a = agg[d["name"]]
+        a[0] += 1
+        a[1] += d["gpu__time_duration.sum"]
+        g = d.get("launch__grid_size", 0.0)
+        a[2] += g
+        if g and g < 148:
+            a[3] += 1
+            a[4] += d["gpu__time_duration.sum"]
     tot = sum(v[1] for v in agg.values())
     lines = [f"# launch list summary: `{path.split('/')[-1]}` (ncu --metrics gpu__time_duration.sum, "
              "cold-cache, serialised: compare shares, not absolutes)", "",
-             "| kernel | launches | total us | share | avg us |", "|---|---|---|---|---|"]
-    for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        lines.append(f"| `{k}` | {n} | {us:.1f} | {100 * us / tot:.1f}% | {us / n:.2f} |")
+             "| kernel | launches | total us | share | avg us | avg grid | launches with grid < 148 (their us) |",
+             "|---|---|---|---|---|---|---|"]
+    for k, (n, us, gs, ns, nus) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"| `{k}` | {n} | {us:.1f} | {100 * us / tot:.1f}% | {us / n:.2f} | {gs / n:.0f} | "
+                     f"{ns} ({nus:.0f}) |")
     open(dst, "w").write("\n".join(lines) + "\n")
 
 

@@ -290,3 +290,24 @@ def test_theorem1_mixture_direction(orc):
     izw = orc.window(z, w).mi
     assert izw < ixy
     assert 0.1 <= izw / ixy <= 0.4  # Eq. 18 predicts 0.25
+
+
+def test_table2_alternative_reading_evaluated(orc):
+    """Reading R5 evaluation: the scale-free alternative normalizer I~_L = 1 - exp(-2 MI)
+    (Linfoot's informational coefficient, squared) flags all ten Table 2 relations incl. the exponential
+    family and not the independent pair -- but it also flags pure-background windows of configs[0]
+    at w = 64 (KSG's small-w bias: MI up to ~0.12 nats on independent data), which would break the planted-
+    recovery pins; so the KL normalizer stays and test_table2_exponential_flagged stays a strict xfail."""
+    lin = lambda mi: 1.0 - math.exp(-2.0 * max(mi, 0.0))
+    for kind in RELATIONS + ["exponential"]:
+        x, y = datagen.table2_relation(kind, 1000, seed=1)
+        assert lin(orc.window(x, y, k=4).mi) >= 0.2, kind
+    x, y = datagen.table2_relation("independent", 1000, seed=1)
+    assert lin(orc.window(x, y, k=4).mi) < 0.2
+    wl = datagen.cfg1()
+    x, y = wl.series
+    W = [(a, b) for a, b in datagen.sweep_windows(len(x), [64], 8)            # configs[0] sweep, w = 64,
+         if b <= 500 or (a >= 800 and b <= 1200) or a >= 1500]               # background windows only
+    r = orc.mi_batch(x, y, W, 4)
+    assert max(lin(v) for v in r["mi"]) >= 0.2   # a background false positive under the alternative
+    assert max(r["nmi"]) < 0.2                   # none under the KL reading
