@@ -138,6 +138,10 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_BLOCK_SORT")) block_sort_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_LAT_SPLIT")) lat_split_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_SCAN_UNIFIED")) scan_unified_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_POISON")) {  // T5 substitute (compute-sanitizer is closed on the pool)
+        const uint32_t b = (uint32_t)std::strtoul(m, nullptr, 0) & 0xffu;
+        poison_ = (b * 0x01010101u) | 0x80000000u;  // never 0: the flag is the value
+    }
     ISY_CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     ISY_CK(cudaMalloc(&dflag_, sizeof(int)));
     ISY_CK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
@@ -584,6 +588,17 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     L.sorted_ppc = ppc;
     L.fused_n2 = fused_n2;
     L.scan_unified = scan_unified_;
+    L.poison = poison_;
+    L.pad4_ = 0;
+    if (poison_) {  // every byte the kernels read must have been written in this batch
+        const int pb = (int)(poison_ & 0xffu);
+        if (S.sscratch) ISY_CK(cudaMemsetAsync(S.sscratch, pb, S.sscratch_cap, st));
+        if (S.ddrec) ISY_CK(cudaMemsetAsync(S.ddrec, pb, S.ddrec_cap * sizeof(KsgRec), st));
+        if (n <= kZeroCopyMaxRecs) {
+            ISY_CK(cudaStreamSynchronize(st));
+            std::memset(S.hrec, pb, n * sizeof(KsgRec));
+        }
+    }
     const int32_t* dlists = reinterpret_cast<const int32_t*>(dbase + off_lists);
     const KsgItem* ditems = reinterpret_cast<const KsgItem*>(dbase + off_items);
 

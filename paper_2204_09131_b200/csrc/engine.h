@@ -79,7 +79,9 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
     int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
     int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
-    int32_t scan_unified;    // sorted-path phase A: 1 one block per iteration from one side (default), 0 both sides
+    int32_t scan_unified;    // sorted-path phase A: 0 both sides per iteration (default), 1 one side per iteration
+    uint32_t poison;         // T5 check (ISYCOS_POISON=<byte>): kernels fill their shared memory with this pattern first
+    int32_t pad4_;
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -241,7 +243,8 @@ private:
         std::vector<KsgBlk> blks;
         std::vector<KsgSegB> segb;
     } bins_;
-    int32_t scan_unified_ = 1;       // ISYCOS_SCAN_UNIFIED (A/B knob; results identical)
+    int32_t scan_unified_ = 0;       // ISYCOS_SCAN_UNIFIED=1: one side per iteration (measured 5-15 % slower; results identical)
+    uint32_t poison_ = 0;            // ISYCOS_POISON=<byte>: shared memory, scan scratch and records pre-filled (T5)
     bool lat_split_on_ = true;       // latency-mode small windows on the 8-lanes-per-point kernel (ISYCOS_LAT_SPLIT=0: tile R=1)
     bool block_sort_on_ = true;      // NEXT-3 shared-block sorts (env ISYCOS_BLOCK_SORT=0 disables; A/B knob)
     bool sorted_on_ = true;

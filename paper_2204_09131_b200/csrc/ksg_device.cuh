@@ -57,6 +57,30 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         : "memory");
 }
 
+// ------------------------------------------------------------------ T5 check: shared-memory poisoning
+// With L.poison set (env ISYCOS_POISON, tests only) a kernel first fills its shared memory with the pattern:
+// a read of a shared byte the kernel did not write then changes results, which the poison test detects
+// (compute-sanitizer initcheck/racecheck are unavailable on the GPU pool).
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void poison_smem(const KsgLaunch& L, void* p, unsigned bytes) {
+    if (!L.poison) return;
+    unsigned* q = reinterpret_cast<unsigned*>(p);
+    const unsigned pat = L.poison & 0xffffffu ? (L.poison & 0xffu) * 0x01010101u : 0u;
+    for (unsigned i = threadIdx.x; i < bytes / 4; i += blockDim.x) q[i] = pat;
+}
+
+__device__ __forceinline__ void poison_warp(const KsgLaunch& L, void* p, unsigned bytes) {
+    if (!L.poison) return;
+    unsigned* q = reinterpret_cast<unsigned*>(p);
+    const unsigned pat = L.poison & 0xffffffu ? (L.poison & 0xffu) * 0x01010101u : 0u;
+    for (unsigned i = threadIdx.x & 31u; i < bytes / 4; i += 32) q[i] = pat;
+    __syncwarp();
+}
+
 // ------------------------------------------------------------------ canonical fp64 numerics (§8(c).3)
 __device__ __forceinline__ long long q32(double v) { return __double2ll_rn(__dmul_rn(v, 4294967296.0)); }
 

@@ -26,6 +26,10 @@ __global__ void __launch_bounds__(kFusedThreads)
     fused_sorted_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const KsgItem* __restrict__ items,
                         int gmax) {
     extern __shared__ __align__(16) unsigned long long fsm[];
+    if (L.poison) {
+        poison_smem(L, fsm, dyn_smem_bytes());
+        __syncthreads();
+    }
     const KsgItem it = items[blockIdx.x];
     const int q = list[it.win];
     const KsgWin W = L.wins[q];

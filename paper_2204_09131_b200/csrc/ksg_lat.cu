@@ -21,6 +21,11 @@ __global__ void __launch_bounds__(kLatThreads)
     ksg_lat_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items) {
     __shared__ __align__(16) float sx[256];
     __shared__ __align__(16) float sy[256];
+    if (L.poison) {
+        poison_smem(L, sx, sizeof(sx));
+        poison_smem(L, sy, sizeof(sy));
+        __syncthreads();
+    }
     const KsgItem it = items[blockIdx.x];
     const int q = it.win;
     const KsgWin W = L.wins[q];

@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int idx = blockIdx.x * kSmallWarps + warp;
     if (idx >= n) return;  // warp-uniform
+    poison_warp(L, sbuf[warp], sizeof(sbuf[0]));
     const int q = list[idx];
     const KsgWin W = L.wins[q];
     const int w = W.w;

@@ -14,6 +14,10 @@ __global__ void __launch_bounds__(1024) block_sort_kernel(const KsgLaunch L, con
                                                           unsigned long long* __restrict__ BX,
                                                           unsigned* __restrict__ BY) {
     extern __shared__ __align__(16) unsigned char sm[];
+    if (L.poison) {
+        poison_smem(L, sm, dyn_smem_bytes());
+        __syncthreads();
+    }
     const KsgBlk B = blks[blockIdx.x];
     const int n2 = B.beta;  // power of two in [256, kSortedMaxW]
     const float* gx = L.pairs[B.pair].x + B.t;
@@ -54,6 +58,10 @@ __global__ void __launch_bounds__(1024) sort_window_kernel(const KsgLaunch L, co
                                    int W2, const KsgSegB* __restrict__ segb,
                                    const unsigned long long* __restrict__ BX, const unsigned* __restrict__ BY) {
     extern __shared__ __align__(16) unsigned char sm[];
+    if (L.poison) {
+        poison_smem(L, sm, dyn_smem_bytes());
+        __syncthreads();
+    }
     const KsgItem sg = segs[blockIdx.x];  // win = position in the sorted list, i0 = segment start
     const int b = sg.win;
     const int q = list[b];
@@ -203,6 +211,11 @@ __global__ void __launch_bounds__(kSortedThreads)
     const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
     __shared__ float eps_s[kSortedPts];
     __shared__ int2 stop_s[kSortedPts];
+    if (L.poison) {
+        poison_smem(L, eps_s, sizeof(eps_s));
+        poison_smem(L, stop_s, sizeof(stop_s));
+        __syncthreads();
+    }
     const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list, it.i0 = first point
     const int b = it.win;
     const int q = list[b];

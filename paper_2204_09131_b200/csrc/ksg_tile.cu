@@ -11,6 +11,10 @@ __global__ void __launch_bounds__(kTileThreads)
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ long long red_sp[kTileThreads / 32], red_sl[kTileThreads / 32];
     __shared__ int red_z[kTileThreads / 32];
+    if (L.poison) {
+        poison_smem(L, dyn, dyn_smem_bytes());
+        __syncthreads();
+    }
 
     const KsgItem it = items[blockIdx.x];
     const int q = it.win;

@@ -19,6 +19,10 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int idx = blockIdx.x * kSmallWarps + warp;
     if (idx >= n) return;  // warp-uniform
+    poison_warp(L, sP2[warp], sizeof(sP2[0]));
+    poison_warp(L, sYS[warp], sizeof(sYS[0]));
+    poison_warp(L, sOX[warp], sizeof(sOX[0]));
+    poison_warp(L, seps[warp], sizeof(seps[0]));
     const int q = list[idx];
     const KsgWin W = L.wins[q];
     const int w = W.w;

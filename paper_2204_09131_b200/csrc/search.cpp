@@ -826,6 +826,108 @@ struct PairWork {
     }
 };
 
+// A finished pair's share of the output: result windows (merged per method unless chunks are selected),
+// algorithm counters, Alg. 3 trial counts, and the distinct windows its algorithms consumed.
+struct Retired {
+    AlgStats ps;
+    std::vector<isycos_result_window> res;
+    int64_t nL_td = 0, nS_bu = 0;
+    int64_t dw = 0, dpp = 0;
+};
+
+void retire_pair(PairWork& pw, Retired& R, const SearchParams& P, bool chunk_sel) {
+    pw.cache.pending.clear();  // leftover speculative requests of discarded climbs
+    for (int m = 1; m <= 2; ++m) {
+        std::vector<isycos_result_window> per;
+        if (m == 1)
+            for (auto& j : pw.td) {
+                per.insert(per.end(), j.results.begin(), j.results.end());
+                R.ps.add(j.stats);
+            }
+        else
+            for (auto& j : pw.bu) {
+                per.insert(per.end(), j.results.begin(), j.results.end());
+                R.ps.add(j.stats);
+            }
+        if (!(pw.method & m)) continue;
+        if (pw.kind == 1) {  // trial run: countWindows, |w| <= rho * s_max is small
+            const double rho = P.auto_rho > 0.0 ? P.auto_rho : 0.5;
+            for (const auto& r : per) {
+                const bool small = (double)(r.t1 - r.t0) <= rho * (double)P.s_max;
+                if (m == 1 && !small) R.nL_td += 1;
+                if (m == 2 && small) R.nS_bu += 1;
+            }
+            continue;
+        }
+        if (chunk_sel) {  // merged by isycos_merge_windows once every chunk is gathered
+            R.res.insert(R.res.end(), per.begin(), per.end());
+            continue;
+        }
+        auto merged = merge_windows(per);
+        R.res.insert(R.res.end(), merged.begin(), merged.end());
+    }
+    pw.cache.map.for_each([&](const Entry& en) {
+        if (en.consumed) {
+            const int64_t w = key_w(en.key);
+            R.dw += 1;
+            R.dpp += w * (w - 1);
+            R.ps.eval_cost += wcost(w);
+        }
+    });
+}
+
+// Retires finished searches off the critical path: counts, merges and frees each pair's cache on its own
+// thread; the outputs are collected in retire order when the search ends.
+class Reaper {
+public:
+    Reaper(const SearchParams& P, bool chunk_sel) : P_(P), sel_(chunk_sel), th_([this] { loop(); }) {}
+    ~Reaper() { finish(); }
+    void push(std::unique_ptr<PairWork> pw) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(pw));
+            out_.emplace_back();
+        }
+        cv_.notify_one();
+    }
+    std::deque<Retired>& finish() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_one();
+        if (th_.joinable()) th_.join();
+        return out_;
+    }
+
+private:
+    void loop() {
+        size_t next = 0;
+        for (;;) {
+            std::unique_ptr<PairWork> pw;
+            Retired* slot = nullptr;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || next < out_.size(); });
+                if (next >= out_.size()) return;
+                pw = std::move(q_[next]);
+                slot = &out_[next];  // deque: element addresses are stable under push_back
+                ++next;
+            }
+            retire_pair(*pw, *slot, P_, sel_);
+            pw.reset();
+        }
+    }
+    const SearchParams& P_;
+    bool sel_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::unique_ptr<PairWork>> q_;
+    std::deque<Retired> out_;
+    bool stop_ = false;
+    std::thread th_;
+};
+
 }  // namespace
 
 Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std::vector<int32_t>& pair_ids,
@@ -864,6 +966,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     if (n_threads <= 0) n_threads = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
     if (n_pairs <= 1 && P.method != 4) n_threads = 1;  // one pair: nothing to spread
     HostPool pool(n_threads);
+    Reaper reaper(P, chunk_sel);
     const int32_t aM = P.auto_M > 0 ? P.auto_M : 20, am = P.auto_m > 0 ? P.auto_m : 6;
     for (int32_t p = 0; p < n_pairs; ++p) {
         if (P.method != 4) {
@@ -1039,88 +1142,47 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             // distinct-window count over the pair's cache, freeing the cache) runs on the host pool; the
             // bookkeeping that orders results and feeds Alg. 3 stays sequential in admission order
             const auto t_ret = clk::now();
-            struct Retired {
-                AlgStats ps;
-                std::vector<isycos_result_window> res;  // merged result windows (searches)
-                int64_t nL_td = 0, nS_bu = 0;           // Alg. 3 trial counts (trial runs)
-                int64_t dw = 0, dpp = 0;
-            };
             std::vector<int32_t> fin;
             for (size_t i = 0; i < active.size(); ++i)
                 if (active[i]->finished() && active[i]->inflight == 0) fin.push_back((int32_t)i);
-            std::vector<Retired> rt(fin.size());
-            pool.run((int)fin.size(), [&](int f) {
-                PairWork* pw = active[fin[f]].get();
+            // searches (kind 0) retire on the reaper thread, off the round's critical path; Alg. 3 trial runs
+            // (kind 1) retire here, their costs decide the method of the pair's next unit
+            std::vector<int32_t> sync_fin;
+            for (int32_t i : fin) {
+                if (active[i]->kind == 0)
+                    reaper.push(std::move(active[i]));
+                else
+                    sync_fin.push_back(i);
+            }
+            std::vector<Retired> rt(sync_fin.size());
+            pool.run((int)sync_fin.size(), [&](int f) { retire_pair(*active[sync_fin[f]], rt[f], P, chunk_sel); });
+            for (size_t f = 0; f < sync_fin.size(); ++f) {
+                PairWork* pw = active[sync_fin[f]].get();
                 Retired& R = rt[f];
-                pw->cache.pending.clear();  // leftover speculative requests of discarded climbs
-                for (int m = 1; m <= 2; ++m) {
-                    std::vector<isycos_result_window> per;
-                    if (m == 1)
-                        for (auto& j : pw->td) {
-                            per.insert(per.end(), j.results.begin(), j.results.end());
-                            R.ps.add(j.stats);
-                        }
-                    else
-                        for (auto& j : pw->bu) {
-                            per.insert(per.end(), j.results.begin(), j.results.end());
-                            R.ps.add(j.stats);
-                        }
-                    if (!(pw->method & m)) continue;
-                    if (pw->kind == 1) {  // trial run: countWindows, |w| <= rho * s_max is small
-                        const double rho = P.auto_rho > 0.0 ? P.auto_rho : 0.5;
-                        for (const auto& r : per) {
-                            const bool small = (double)(r.t1 - r.t0) <= rho * (double)P.s_max;
-                            if (m == 1 && !small) R.nL_td += 1;
-                            if (m == 2 && small) R.nS_bu += 1;
-                        }
-                        continue;
-                    }
-                    if (chunk_sel) {  // merged by isycos_merge_windows once every chunk is gathered
-                        R.res.insert(R.res.end(), per.begin(), per.end());
-                        continue;
-                    }
-                    auto merged = merge_windows(per);
-                    R.res.insert(R.res.end(), merged.begin(), merged.end());
-                }
-                pw->cache.map.for_each([&](const Entry& en) {
-                    if (en.consumed) {
-                        const int64_t w = key_w(en.key);
-                        R.dw += 1;
-                        R.dpp += w * (w - 1);
-                        R.ps.eval_cost += wcost(w);
-                    }
-                });
-            });
-            for (size_t f = 0; f < fin.size(); ++f) {
-                PairWork* pw = active[fin[f]].get();
-                Retired& R = rt[f];
-                all.insert(all.end(), R.res.begin(), R.res.end());
                 distinct_w += R.dw;
                 distinct_pp += R.dpp;
                 total.add(R.ps);
-                if (pw->kind == 1) {
-                    AutoState& A = autos[pw->auto_id];
-                    A.nL_td += R.nL_td;
-                    A.nS_bu += R.nS_bu;
-                    (pw->method == 1 ? A.cost_td : A.cost_bu) += R.ps.eval_cost;
-                    if (--A.left == 0) {
-                        // Alg. 3 lines 6-15, Eqs. 6-9 (fixed fp64 op order, as the oracle)
-                        const double alpha = P.auto_alpha > 0.0 ? P.auto_alpha : 0.5;
-                        const double tbar_td = (double)A.cost_td / (double)am;
-                        const double tbar_bu = (double)A.cost_bu / (double)am;
-                        const double tt_td = tbar_td / (tbar_bu + tbar_td);
-                        const double tt_bu = tbar_bu / (tbar_bu + tbar_td);
-                        double nl = 0.5, ns = 0.5;
-                        if (A.nS_bu + A.nL_td > 0) {
-                            nl = (double)A.nL_td / (double)(A.nS_bu + A.nL_td);
-                            ns = (double)A.nS_bu / (double)(A.nS_bu + A.nL_td);
-                        }
-                        const double beta = 1.0 - alpha;
-                        A.nscore_td = alpha * (1.0 / tt_td) + beta * nl;
-                        A.nscore_bu = alpha * (1.0 / tt_bu) + beta * ns;
-                        A.chosen = A.nscore_td > A.nscore_bu ? 1 : 2;
-                        queue.push_front(Unit{A.pair_idx, A.chosen, 0, -1, plan});
+                AutoState& A = autos[pw->auto_id];
+                A.nL_td += R.nL_td;
+                A.nS_bu += R.nS_bu;
+                (pw->method == 1 ? A.cost_td : A.cost_bu) += R.ps.eval_cost;
+                if (--A.left == 0) {
+                    // Alg. 3 lines 6-15, Eqs. 6-9 (fixed fp64 op order, as the oracle)
+                    const double alpha = P.auto_alpha > 0.0 ? P.auto_alpha : 0.5;
+                    const double tbar_td = (double)A.cost_td / (double)am;
+                    const double tbar_bu = (double)A.cost_bu / (double)am;
+                    const double tt_td = tbar_td / (tbar_bu + tbar_td);
+                    const double tt_bu = tbar_bu / (tbar_bu + tbar_td);
+                    double nl = 0.5, ns = 0.5;
+                    if (A.nS_bu + A.nL_td > 0) {
+                        nl = (double)A.nL_td / (double)(A.nS_bu + A.nL_td);
+                        ns = (double)A.nS_bu / (double)(A.nS_bu + A.nL_td);
                     }
+                    const double beta = 1.0 - alpha;
+                    A.nscore_td = alpha * (1.0 / tt_td) + beta * nl;
+                    A.nscore_bu = alpha * (1.0 / tt_bu) + beta * ns;
+                    A.chosen = A.nscore_td > A.nscore_bu ? 1 : 2;
+                    queue.push_front(Unit{A.pair_idx, A.chosen, 0, -1, plan});
                 }
             }
             if (!fin.empty()) {
@@ -1128,7 +1190,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 size_t keep = 0, fi = 0;
                 for (size_t i = 0; i < active.size(); ++i) {
                     if (fi < fin.size() && (int32_t)i == fin[fi]) {
-                        dead.push_back(std::move(active[i]));
+                        if (active[i]) dead.push_back(std::move(active[i]));
                         ++fi;
                     } else {
                         active[keep++] = std::move(active[i]);
@@ -1212,6 +1274,12 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     if (n_groups == 2) {
         Status s = eng->join_second_stream(st);
         if (!s.ok()) return s;
+    }
+    for (Retired& R : reaper.finish()) {  // retire order (deterministic: it follows the rounds)
+        all.insert(all.end(), R.res.begin(), R.res.end());
+        distinct_w += R.dw;
+        distinct_pp += R.dpp;
+        total.add(R.ps);
     }
     std::stable_sort(all.begin(), all.end(), [](const isycos_result_window& a, const isycos_result_window& b) {
         if (a.pair != b.pair) return a.pair < b.pair;
