@@ -766,14 +766,24 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
 // scan-step counts) into mapped pinned host memory (or a device buffer copied back by submit): the stream
 // synchronisation makes them visible.
 Status Engine::collect(int si, KsgRec* recs_host, BatchStats* bs) {
+    const KsgRec* view = nullptr;
+    const int64_t n = slots_[si].busy ? slots_[si].n : 0;
+    Status s = collect_view(si, &view, bs, true);
+    if (s.ok() && recs_host && n > 0) std::memcpy(recs_host, view, n * sizeof(KsgRec));
+    return s;
+}
+
+Status Engine::collect_view(int si, const KsgRec** view, BatchStats* bs, bool count_steps, bool* profiled) {
     Slot& S = slots_[si];
+    *view = S.hrec;
+    if (profiled) *profiled = S.busy && S.profile;
     if (!S.busy) return Status{};
     S.busy = false;
     const int64_t n = S.n;
     ISY_CK(cudaStreamSynchronize(S.st));
     unsigned long long steps = 0;
-    for (int64_t i = 0; i < n; ++i) steps += S.hrec[i].steps;
-    if (recs_host) std::memcpy(recs_host, S.hrec, n * sizeof(KsgRec));
+    if (count_steps)
+        for (int64_t i = 0; i < n; ++i) steps += S.hrec[i].steps;
     if (bs) {
         bs->d2h_bytes += n * (int64_t)sizeof(KsgRec);
         bs->windows += n;

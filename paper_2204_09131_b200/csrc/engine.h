@@ -186,6 +186,9 @@ public:
     Status submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgWin* wins, int64_t n, int32_t k,
                   int32_t variant, const DebugOut& dbg, cudaStream_t st, uint32_t flags, BatchStats* bs);
     Status collect(int si, KsgRec* recs_host, BatchStats* bs);
+    // collect() without the copy: *view points at the slot's pinned records (valid until the slot's next
+    // submit); the caller adds the records' scan steps to bs->scan_steps itself (count_steps = false)
+    Status collect_view(int si, const KsgRec** view, BatchStats* bs, bool count_steps, bool* profiled = nullptr);
     cudaStream_t second_stream() const { return stream2_; }
     Status fork_second_stream(cudaStream_t st);  // second stream waits for work queued on st so far
     Status join_second_stream(cudaStream_t st);  // st waits for the second stream

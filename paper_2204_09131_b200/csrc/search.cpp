@@ -990,8 +990,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             queue.push_back(Unit{p, 2, 1, aid, {{lo, lo + Lp}}});
         }
     }
-    std::vector<KsgWin> batch;
-    std::vector<KsgRec> recs;
+    // the round's batch: grown, never re-initialised (a value-initialising resize of a 10^7-window TD round
+    // costs more host time than the copy itself)
+    std::unique_ptr<KsgWin[]> batch;
+    int64_t batch_cap = 0, batch_n = 0;
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
@@ -1015,6 +1017,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         std::vector<Entry*> owners;
         std::vector<PairWork*> pws;
         std::vector<int64_t> offs;  // batch offset of each pair in pws (+ end)
+        int64_t n = 0;              // windows in flight (owners[0..n))
     };
     Flight fl[2];
     // error exits leave no batch in flight: the slot's staging buffer and mapped records would otherwise be
@@ -1036,28 +1039,38 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     auto deliver = [&](int g) -> Status {
         Flight& F = fl[g];
         if (!F.busy) return Status{};
-        recs.resize(F.owners.size());
+        const KsgRec* recs = nullptr;
         const auto t_ev = clk::now();
-        Status s = eng->collect(g, recs.data(), &bs);
+        bool profiled = false;
+        Status s = eng->collect_view(g, &recs, &bs, false, &profiled);
         const double wms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
         eval_ms += wms;
         wait_ms += wms;
         if (!s.ok()) return s;
         const auto t_dl = clk::now();
-        // records -> entries, pairs in parallel for big batches (each pair's records are a contiguous slice)
-        pool.run(F.owners.size() >= 512 ? (int)F.pws.size() : 1, [&](int p) {
-            if (F.owners.size() < 512) p = -1;
-            const int64_t i0 = p < 0 ? 0 : F.offs[p], i1 = p < 0 ? (int64_t)F.owners.size() : F.offs[p + 1];
+        // records -> entries, pairs in parallel for big batches (each pair's records are a contiguous slice),
+        // read straight from the pinned records; the per-pair scan-step sums feed the kernel stats
+        const bool par = F.n >= 512;
+        std::vector<unsigned long long> steps(par ? F.pws.size() : 1, 0ull);
+        pool.run(par ? (int)F.pws.size() : 1, [&](int p) {
+            const int64_t i0 = par ? F.offs[p] : 0, i1 = par ? F.offs[p + 1] : F.n;
+            unsigned long long st = 0;
             for (int64_t i = i0; i < i1; ++i) {
                 Entry& e = *F.owners[i];
                 e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
                 e.ready = true;
+                st += recs[i].steps;
             }
+            steps[par ? p : 0] = st;
         });
+        for (unsigned long long v : steps) {
+            bs.scan_steps += (int64_t)v;
+            if (profiled) bs.prof_scan_steps += (int64_t)v;
+        }
         for (PairWork* pw : F.pws) pw->inflight -= 1;
         dlv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_dl).count();
         F.busy = false;
-        F.owners.clear();
+        F.n = 0;
         F.pws.clear();
         F.offs.clear();
         return Status{};
@@ -1204,7 +1217,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             ret_ms += std::chrono::duration<double, std::milli>(t_asm - t_ret).count();
             // one batch of every pending window of every active pair (finished pairs: leftovers dropped)
             std::vector<PairPtrs> table;
-            batch.clear();
+            batch_n = 0;
             Flight& F = fl[g];
             int64_t tot = 0;
             for (auto& pw : active) {
@@ -1221,8 +1234,13 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 F.pws.push_back(pw.get());
             }
             // each pair copies its staged requests to its slice of the batch (in parallel when large)
-            batch.resize(tot);
-            F.owners.resize(tot);
+            if (batch_cap < tot) {
+                batch_cap = std::max<int64_t>(tot, batch_cap * 2);
+                batch.reset(new KsgWin[batch_cap]);
+            }
+            batch_n = tot;
+            if ((int64_t)F.owners.size() < tot) F.owners.resize(std::max<int64_t>(tot, 2 * (int64_t)F.owners.size()));
+            F.n = tot;
             pool.run(tot >= 512 ? (int)F.pws.size() : 1, [&](int p) {
                 const int p0 = tot >= 512 ? p : 0, p1 = tot >= 512 ? p + 1 : (int)F.pws.size();
                 for (int q = p0; q < p1; ++q) {
@@ -1237,18 +1255,18 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                     pw->stage_o.clear();
                 }
             });
-            if (batch.empty()) {
+            if (batch_n == 0) {
                 F.offs.clear();
                 continue;
             }
-            F.offs.push_back((int64_t)batch.size());
+            F.offs.push_back(batch_n);
             const auto t_ev = clk::now();
             asm_ms += std::chrono::duration<double, std::milli>(t_ev - t_asm).count();
             // kernel timing samples every profile_every-th round (event records are host time per round)
             uint32_t fl_round = P.flags;
             if ((fl_round & ISYCOS_F_PROFILE) && P.profile_every > 1 && (round_no % P.profile_every) != 0)
                 fl_round &= ~ISYCOS_F_PROFILE;
-            Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.data(), (int64_t)batch.size(), P.k,
+            Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.get(), batch_n, P.k,
                                    P.variant, DebugOut{}, sts[g], fl_round, &bs);
             const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
             eval_ms += ev_ms;
@@ -1257,12 +1275,13 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             progress = true;
             if (trace) {  // per-round trace (ISYCOS_TRACE=<path>): round, host ms since last submit, submit ms, batch
                 int64_t sw2 = 0, wmax = 0;
-                for (const KsgWin& kw : batch) {
+                for (int64_t bi = 0; bi < batch_n; ++bi) {
+                    const KsgWin& kw = batch[bi];
                     sw2 += (int64_t)kw.w * kw.w;
                     wmax = std::max<int64_t>(wmax, kw.w);
                 }
                 const double host = std::chrono::duration<double, std::milli>(t_ev - t_last).count();
-                std::fprintf(trace, "%lld %.4f %.4f %zu %lld %lld\n", (long long)round_no, host, ev_ms, batch.size(),
+                std::fprintf(trace, "%lld %.4f %.4f %lld %lld %lld\n", (long long)round_no, host, ev_ms, (long long)batch_n,
                              (long long)sw2, (long long)wmax);
             }
             ++round_no;

@@ -12,8 +12,8 @@ timeout 300 python __graft_entry__.py --smoke > $O/${TAG}_smoke.log 2>&1; echo "
 timeout 1500 python -m pytest tests -m gpu -q > $O/${TAG}_gpu_tests.log 2>&1; echo "gpu tests rc=$?"; tail -2 $O/${TAG}_gpu_tests.log
 timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err; echo "ref rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv --log-file /tmp/${TAG}_launches.csv \
-  python bench.py --steps 1 --warmup 3 --pairs-per-gpu 16 --no-side --no-cpu-baseline > $O/${TAG}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+timeout 1500 ncu --nvtx --nvtx-include "timed_step/" --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv \
+  --log-file /tmp/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --no-side --no-cpu-baseline > $O/${TAG}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
 python scripts/ncu_summary.py launches /tmp/${TAG}_launches.csv $O/${TAG}_launches_bench.md
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sorted_knn|sort_window|block_sort" -c 3 \
   -o /tmp/${TAG}_sweep4096 python scripts/kernel_bench.py --only 4096 --reps 1 --target 1e11 > $O/${TAG}_ncu_sweep.log 2>&1; echo "ncu sweep rc=$?"

@@ -120,6 +120,12 @@ Status Engine::collect(int si, KsgRec* recs_host, BatchStats*) {
     std::memcpy(recs_host, g_slot_recs[si].data(), g_slot_recs[si].size() * sizeof(KsgRec));
     return Status{};
 }
+Status Engine::collect_view(int si, const KsgRec** view, BatchStats*, bool, bool* profiled) {
+    *view = g_slot_recs[si].data();
+    if (profiled) *profiled = false;
+    g_slot_busy[si] = false;
+    return Status{};
+}
 Status Engine::fork_second_stream(cudaStream_t) { return Status{}; }
 Status Engine::join_second_stream(cudaStream_t) { return Status{}; }
 Engine::~Engine() {}
