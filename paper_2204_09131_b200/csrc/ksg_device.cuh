@@ -380,6 +380,7 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
 //          monotone on each side of x_i), found by two binary searches with the identical predicate;
 //          n_y likewise on the sorted y.  Bit-identical to the brute-force counts.
 constexpr int kSortedThreads = 128;  // points per CTA of the scan kernel (one point per thread)
+constexpr int kLockstepMinW = 2048;  // phase B: lockstep binary searches from this window size up (measured)
 constexpr int kMergeThreads = kMergePts;  // elements per CTA of the XL rank merge
 
 // Order-preserving map of float bits to unsigned (finite values; -0 sorts just before +0, equal as floats).
@@ -779,24 +780,60 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
     float ex = eps, ey = eps;
     if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
     if (V2 || eps > 0.0f) {
-        // x: left part [0, m] uses fl(x_i - x_j) < ex, right part [m, w) uses fl(x_j - x_i) < ex
-        int lo = V2 ? 0 : xlo, hi = m;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (xv - XS[2 * mid] < ex) hi = mid; else lo = mid + 1;
+        // The searches run in lockstep so their loads are in flight together (memory-level parallelism; one
+        // search at a time was latency-bound): first the two x bounds with the y pivot p, then the two y
+        // bounds.  Each search finds the end of the prefix of [b, b + n) on which its predicate holds.
+        //   x left  [lo, m):  !(fl(x_i - x_j) < ex)      x right [m, hi): fl(x_j - x_i) < ex
+        //   y pivot [0, w):   YS[j] < y_i                y left  [0, p):  !(fl(y_i - y_j) < ey)
+        //   y right [p, w):   fl(y_j - y_i) < ey
+        const int xl0 = V2 ? 0 : xlo, xr1 = V2 ? w : min(w, xhi);
+        if (w < kLockstepMinW) {  // short searches: one at a time (the lockstep predication costs more there)
+            int lo = xl0, hi = m;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (xv - XS[2 * mid] < ex) hi = mid; else lo = mid + 1;
+            }
+            const int Lx = lo;
+            lo = m;
+            hi = xr1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
+            }
+            nx = lo - Lx - 1;
+            const int p = lower_bound_f(YS, w, yv);
+            ny = right_bound(YS, p, w, yv, ey) - left_bound_f(YS, p, yv, ey) - 1;
+        } else {
+        int b0 = xl0, n0 = m - xl0, b1 = m, n1 = xr1 - m, b2 = 0, n2 = w;
+        while ((n0 | n1 | n2) > 0) {
+            if (n0 > 0) {
+                const int h = n0 >> 1;
+                if (!(xv - XS[2 * (b0 + h)] < ex)) { b0 += h + 1; n0 -= h + 1; } else n0 = h;
+            }
+            if (n1 > 0) {
+                const int h = n1 >> 1;
+                if (XS[2 * (b1 + h)] - xv < ex) { b1 += h + 1; n1 -= h + 1; } else n1 = h;
+            }
+            if (n2 > 0) {
+                const int h = n2 >> 1;
+                if (YS[b2 + h] < yv) { b2 += h + 1; n2 -= h + 1; } else n2 = h;
+            }
         }
-        const int Lx = lo;
-        lo = m;
-        hi = V2 ? w : min(w, xhi);
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
+        nx = b1 - b0 - 1;
+        const int p = b2;
+        int b3 = 0, n3 = p, b4 = p, n4 = w - p;
+        while ((n3 | n4) > 0) {
+            if (n3 > 0) {
+                const int h = n3 >> 1;
+                if (!(yv - YS[b3 + h] < ey)) { b3 += h + 1; n3 -= h + 1; } else n3 = h;
+            }
+            if (n4 > 0) {
+                const int h = n4 >> 1;
+                if (YS[b4 + h] - yv < ey) { b4 += h + 1; n4 -= h + 1; } else n4 = h;
+            }
         }
-        nx = lo - Lx - 1;
-        const int p = lower_bound_f(YS, w, yv);
-        const int Ly = left_bound_f(YS, p, yv, ey);
-        const int Ry = right_bound(YS, p, w, yv, ey);
-        ny = Ry - Ly - 1;
+        ny = b4 - b3 - 1;
+        }
     }
     sp += V2 ? L.psiq[nx] + L.psiq[ny] : L.psiq[nx + 1] + L.psiq[ny + 1];
     if (eps > 0.0f)
