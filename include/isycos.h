@@ -77,8 +77,10 @@ enum {
                                results are bit-identical either way — an A/B and test knob */
 #define ISYCOS_F_PROFILE_SORTED_ONLY 8u /* with ISYCOS_F_PROFILE: events around sorted-path launches only */
 #define ISYCOS_F_PROFILE_BRUTE_ONLY 16u  /* with ISYCOS_F_PROFILE: events around brute-force launches only */
-#define ISYCOS_F_NO_BLOCK 32u /* no NEXT-3 shared-block sorts (every sorted-path window sorted from scratch);
-                                 A/B knob, results identical */
+#define ISYCOS_F_NO_BLOCK 32u /* no NEXT-3 shared-block sorts (every sorted-path window sorted from scratch)
+                                 and no incremental radii; A/B knob, results identical */
+#define ISYCOS_F_INCREMENTAL 64u /* NEXT-3 incremental radii and counts along block-grid chains (KSG-1; results
+                                    identical; off by default: measured time-neutral on B200) */
 #define ISYCOS_F_UNFUSED 4u /* sorted-marginal windows always take the throughput form (sort kernel, then
                                scan kernel), never the fused latency kernel; results identical */
 
@@ -109,6 +111,9 @@ typedef struct {
     /* NEXT-3 (incremental MI, GPU analogue): windows whose sorted layout was merged from shared
      * beta-blocks (each block sorted once per batch), and the block points sorted */
     int64_t block_windows, block_points;
+    /* NEXT-3 incremental radii: windows that followed their predecessor on a grid chain, and the points of
+     * those windows whose k-NN radius carried over (no removed / inserted point could change it) */
+    int64_t inc_windows, eps_reused_points;
 } isycos_kernel_stats;
 
 /*

@@ -19,7 +19,8 @@ F_BRUTE = 2   # force the brute-force kernels (A/B and test knob; results identi
 F_UNFUSED = 4  # sorted path in its throughput form only (no fused latency kernel)
 F_PROFILE_SORTED_ONLY = 8
 F_PROFILE_BRUTE_ONLY = 16
-F_NO_BLOCK = 32  # no NEXT-3 shared-block sorts (A/B knob; results identical)
+F_NO_BLOCK = 32  # no NEXT-3 shared-block sorts nor incremental radii (A/B knob; results identical)
+F_INCREMENTAL = 64  # NEXT-3 incremental radii / counts along block-grid chains (off by default; results identical)
 MAX_K = 16
 MAX_W = 262144
 ERROR_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_RANGE", -3: "E_TOO_FEW", -4: "E_TRUNC", -5: "E_CUDA",
@@ -48,7 +49,8 @@ class KernelStats(C.Structure):
                 ("sorted_points", C.c_int64), ("brute_point_pairs", C.c_int64), ("search_probes", C.c_int64),
                 ("sorted_kernel_ms", C.c_double), ("brute_kernel_ms", C.c_double), ("profiled_rounds", C.c_int64),
                 ("prof_brute_point_pairs", C.c_int64), ("prof_scan_steps", C.c_int64),
-                ("prof_search_probes", C.c_int64), ("block_windows", C.c_int64), ("block_points", C.c_int64)]
+                ("prof_search_probes", C.c_int64), ("block_windows", C.c_int64), ("block_points", C.c_int64),
+                ("inc_windows", C.c_int64), ("eps_reused_points", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -212,7 +214,8 @@ def isycos_mi_batch(x, y, windows, k: int = 4):
 
 def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", "s_psi", "s_log", "zero_eps"),
                        debug: bool = False, profile: bool = False, stream=None, out=None, variant: int = 0,
-                       brute: bool = False, unfused: bool = False, no_block: bool = False):
+                       brute: bool = False, unfused: bool = False, no_block: bool = False,
+                       incremental: bool = False):
     """Full per-window records (and optional per-point eps/n_x/n_y).  variant 0 = KSG-1, 1 = KSG-2.
 
     x, y: float32 numpy arrays or torch tensors (CPU or CUDA); windows: (n, 2) int64 array/tensor.
@@ -227,7 +230,7 @@ def isycos_mi_batch_ex(x, y, windows, k: int = 4, *, outputs=("mi", "h", "nmi", 
     o = MiOpts()
     o.variant = int(variant)
     o.flags = ((F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
-               | (F_NO_BLOCK if no_block else 0))
+               | (F_NO_BLOCK if no_block else 0) | (F_INCREMENTAL if incremental else 0))
     o.stream = _stream_ptr(stream)
     keep = []
 
@@ -274,7 +277,7 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
                   seed: int = 0, variant: int = 0, profile: bool = False, brute: bool = False,
                   unfused: bool = False, stream=None, capacity: int | None = None, auto_M: int = 0, auto_m: int = 0,
                   auto_alpha: float = 0.0, auto_rho: float = 0.0, profile_only: str | None = None,
-                  chunks: tuple | None = None, no_block: bool = False):
+                  chunks: tuple | None = None, no_block: bool = False, incremental: bool = False):
     """SYCOS search over series pairs.  Returns (results, stats).
 
     series: list of float32 arrays / tensors (host or CUDA, all alike, same length)
@@ -306,7 +309,7 @@ def isycos_search(series, pairs, *, s_min: int, s_max: int, k: int = 4, sizes=No
     if chunks is not None:  # (pair, chunk) units: chunks [begin, end) of the plan, windows unmerged
         o.chunk_begin, o.chunk_end = int(chunks[0]), int(chunks[1])
     o.flags = ((F_PROFILE if profile else 0) | (F_BRUTE if brute else 0) | (F_UNFUSED if unfused else 0)
-               | (F_NO_BLOCK if no_block else 0))
+               | (F_NO_BLOCK if no_block else 0) | (F_INCREMENTAL if incremental else 0))
     if profile and profile_only:  # events around one path's launches only ("sorted" or "brute")
         o.flags |= F_PROFILE_SORTED_ONLY if profile_only == "sorted" else F_PROFILE_BRUTE_ONLY
     o.stream = _stream_ptr(stream)

@@ -74,6 +74,8 @@ void BatchStats::add_to(isycos_kernel_stats* s) const {
     s->prof_search_probes += prof_probes;
     s->block_windows += block_windows;
     s->block_points += block_points;
+    s->inc_windows += inc_windows;
+    s->eps_reused_points += eps_reused;
 }
 
 // ---------------------------------------------------------------- engine registry (one per device)
@@ -137,6 +139,8 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_AUX_MIN_WINDOWS")) aux_min_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_BLOCK_SORT")) block_sort_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_LAT_SPLIT")) lat_split_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_INCREMENTAL")) inc_on_ = std::atoi(m) != 0;
+    if (const char* m = std::getenv("ISYCOS_INC_CHAIN")) inc_chain_ = std::max(2, std::atoi(m));
     if (const char* m = std::getenv("ISYCOS_SCAN_UNIFIED")) scan_unified_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_POISON")) {  // T5 substitute (compute-sanitizer is closed on the pool)
         const uint32_t b = (uint32_t)std::strtoul(m, nullptr, 0) & 0xffu;
@@ -166,6 +170,7 @@ Engine::~Engine() {
         cudaFree(S.dstage);
         cudaFree(S.ddrec);
         cudaFree(S.sscratch);
+        cudaFree(S.sync);
         cudaFreeHost(S.hstage);
         cudaFreeHost(S.hrec);
         for (auto e : S.events) cudaEventDestroy(e);
@@ -443,10 +448,47 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
                 }
         }
     }
+    // NEXT-3 incremental radii (the paper's IR): a window that follows its predecessor on a block grid
+    // (same pair and size, start + beta, w >= 8 beta: at most 1/8 of the points change) reuses the predecessor's
+    // radii wherever the removed / inserted block cannot change them (ksg_device.cuh, inc_unchanged).  Chains
+    // restart from scratch every kIncChain windows; level j runs in the j-th scan launch.
+    auto& incs = bins_.incs;
+    incs.assign(sorted.size(), KsgInc{-1, 0, 0, 0, -1, -1, 0});
+    int n_lv = 1, inc_d_max = 0;
+    int64_t inc_windows = 0;
+    if (!blks.empty() && (inc_on_ || (flags & ISYCOS_F_INCREMENTAL)) && variant == 0) {  // KSG-1 (counts carried)
+        auto& ord = bins_.ord;  // sorted by (pair, w, t0) by the block plan
+        for (size_t i = 0; i + 1 < ord.size(); ++i) {
+            const int32_t a = ord[i], c = ord[i + 1];
+            const KsgWin& A = wins[sorted[a]];
+            const KsgWin& C = wins[sorted[c]];
+            const int32_t bt = wbeta[a];
+            if (A.pair != C.pair || A.w != C.w || bt == 0 || wbeta[c] != bt || C.t0 - A.t0 != bt || A.w < 8 * bt ||
+                bt > kIncMaxD)
+                continue;
+            if (incs[a].level < 0) incs[a].level = 0;
+            const int lv = incs[a].level + 1 < inc_chain_ ? incs[a].level + 1 : 0;
+            incs[c].level = lv;
+            if (lv > 0) {
+                incs[c].pred = a;
+                incs[c].eps_prev = soff[a];
+                incs[c].boffR = wboff[a];
+                incs[c].boffI = wboff[c] + C.w - bt;
+                incs[c].d = bt;
+                inc_d_max = std::max(inc_d_max, (int)bt);
+                ++inc_windows;
+                n_lv = std::max(n_lv, lv + 1);
+            }
+        }
+    }
     // sorted scan: 1024 points per CTA when the batch fills the GPU (better lane balance in the per-warp
     // work queues), else 256 (more CTAs per window: latency-bound rounds)
     const int ppc = spts >= (int64_t)148 * 8 * 1024 ? sorted_ppc_ : 256;
     for (int32_t q : sorted) n_sitems += (wins[q].w + ppc - 1) / ppc;
+    std::vector<int32_t> lv_off(n_lv + 1, 0);  // scan items grouped by launch level
+    for (size_t b = 0; b < sorted.size(); ++b)
+        lv_off[std::max(0, incs[b].level) + 1] += (wins[sorted[b]].w + ppc - 1) / ppc;
+    for (int l = 0; l < n_lv; ++l) lv_off[l + 1] += lv_off[l];
     // fused: split windows into up to ceil(w / 512) slices while the batch has fewer than 2 CTAs per SM
     const int gmax = std::max<int>(1, (int)(2 * 148 / std::max<size_t>(1, fused.size())));
     int64_t n_fitems = 0;
@@ -463,11 +505,14 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     {
         Status s = ensure_capacity(S, n + 1, n_items + n_sitems + n_segs + n_mblocks + n_fitems, n_pairs,
                                    n_lists + 2 * (int64_t)sorted.size() + 16,
-                                   n_segs * (int64_t)sizeof(KsgSegB) + (int64_t)blks.size() * (int64_t)sizeof(KsgBlk) + 128);
+                                   n_segs * (int64_t)sizeof(KsgSegB) + (int64_t)blks.size() * (int64_t)sizeof(KsgBlk) +
+                                       (int64_t)sorted.size() * (int64_t)sizeof(KsgInc) + 192);
         if (!s.ok()) return s;
     }
     // scratch per sorted point: P2 (8) | OX (4) | YS (4) | TX (4) | TI (4) | TY (4)
-    const int64_t blk_base = (spts * 28 + 15) & ~int64_t(15);  // block keys after the scan layout: BX (8) | BY (4)
+    // scratch per sorted point: P2 (8) | OX | YS | TX | TI | TY | EPS (4 each) | CNT (8); then the NEXT-3 block keys
+    // BX (8) | BY (4)
+    const int64_t blk_base = (spts * 40 + 15) & ~int64_t(15);
     const int64_t scratch_need = blk_base + blk_store * 12;
     if (spts > 0 && S.sscratch_cap < scratch_need) {
         const int64_t c = std::max<int64_t>(scratch_need, S.sscratch_cap * 2);
@@ -490,7 +535,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const int64_t off_sitems = align64(off_items + n_items * (int64_t)sizeof(KsgItem));
     const int64_t off_segs = align64(off_sitems + n_sitems * (int64_t)sizeof(KsgItem));
     const int64_t off_mblk = align64(off_segs + n_segs * (int64_t)sizeof(KsgItem));
-    const int64_t off_segb = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
+    const int64_t off_inc = align64(off_mblk + n_mblocks * (int64_t)sizeof(KsgItem));
+    const int64_t off_segb = align64(off_inc + (inc_windows ? (int64_t)sorted.size() : 0) * (int64_t)sizeof(KsgInc));
     const int64_t off_blks = align64(off_segb + (blks.empty() ? 0 : n_segs) * (int64_t)sizeof(KsgSegB));
     const int64_t total = align64(off_blks + (int64_t)blks.size() * (int64_t)sizeof(KsgBlk));
     std::memcpy(S.hstage + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
@@ -546,9 +592,11 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         int64_t cs = 0, cm = 0;
         c = 0;
         KsgSegB* sbp = reinterpret_cast<KsgSegB*>(S.hstage + off_segb);
+        std::vector<int32_t> lv_fill(lv_off.begin(), lv_off.end() - 1);
         for (size_t b = 0; b < sorted.size(); ++b) {
             const int w = wins[sorted[b]].w;
-            for (int i0 = 0; i0 < w; i0 += ppc) sp[c++] = KsgItem{(int32_t)b, i0};
+            int32_t& f = lv_fill[std::max(0, incs[b].level)];
+            for (int i0 = 0; i0 < w; i0 += ppc) sp[f++] = KsgItem{(int32_t)b, i0};
             for (int s0 = 0; s0 < w; s0 += kSortedMaxW) {
                 if (!blks.empty())  // the segment's blocks are contiguous in the block storage (s0 % beta == 0)
                     sbp[cs] = wbeta[b] ? KsgSegB{wboff[b] + s0, wbeta[b], 0} : KsgSegB{0, 0, 0};
@@ -559,6 +607,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         }
     }
     if (!blks.empty()) std::memcpy(S.hstage + off_blks, blks.data(), blks.size() * sizeof(KsgBlk));
+    if (inc_windows) std::memcpy(S.hstage + off_inc, incs.data(), incs.size() * sizeof(KsgInc));
     // one H2D copy of the packed descriptors (kernels reading them from mapped host memory instead
     // measured 20 % slower on cfg2: a PCIe round trip on every CTA's critical path)
     char* dbase = S.dstage;
@@ -708,9 +757,26 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         const KsgBlk* dbk = reinterpret_cast<const KsgBlk*>(dbase + off_blks);
         unsigned long long* BX = reinterpret_cast<unsigned long long*>(S.sscratch + blk_base);
         unsigned* BY = reinterpret_cast<unsigned*>(S.sscratch + blk_base + blk_store * 8);
+        float* EPS = reinterpret_cast<float*>(S.sscratch + spts * 28);
+        int2* CNT = reinterpret_cast<int2*>(S.sscratch + spts * 32);
+        const KsgInc* dinc = inc_windows ? reinterpret_cast<const KsgInc*>(dbase + off_inc) : nullptr;
+        if (inc_windows) {  // work ticket + per-window finished-CTA counters, zeroed for this launch
+            const int64_t need = 1 + (int64_t)sorted.size();
+            if (S.sync_cap < need) {
+                cudaFree(S.sync);
+                S.sync = nullptr;
+                S.sync_cap = std::max<int64_t>(need, S.sync_cap * 2);
+                ISY_CK(cudaMalloc(&S.sync, S.sync_cap * sizeof(unsigned)));
+            }
+        }
         Status r = launch(0, (n_mblocks ? 3 : 2) + (blks.empty() ? 0 : 1), [&](cudaStream_t sg) {
+            if (inc_windows) {
+                cudaError_t e = cudaMemsetAsync(S.sync, 0, (1 + sorted.size()) * sizeof(unsigned), sg);
+                if (e != cudaSuccess) return e;
+            }
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
-                                 W2, dsi, (int32_t)n_sitems, sg, dsb, dbk, (int32_t)blks.size(), blk_beta_max, BX, BY);
+                                 W2, dsi, (int32_t)n_sitems, sg, dsb, dbk, (int32_t)blks.size(), blk_beta_max, BX, BY,
+                                 dinc, EPS, CNT, lv_off.data(), n_lv, inc_d_max, inc_windows ? S.sync : nullptr);
         });
         if (!r.ok()) return r;
     }
@@ -759,6 +825,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.spts = spoints;
     S.block_windows = blk_windows;
     S.block_points = blk_pts;
+    S.inc_windows = inc_windows;
     return Status{};
 }
 
@@ -783,7 +850,10 @@ Status Engine::collect_view(int si, const KsgRec** view, BatchStats* bs, bool co
     ISY_CK(cudaStreamSynchronize(S.st));
     unsigned long long steps = 0;
     if (count_steps)
-        for (int64_t i = 0; i < n; ++i) steps += S.hrec[i].steps;
+        for (int64_t i = 0; i < n; ++i) {
+            steps += S.hrec[i].steps;
+            if (bs) bs->eps_reused += S.hrec[i].reused;
+        }
     if (bs) {
         bs->d2h_bytes += n * (int64_t)sizeof(KsgRec);
         bs->windows += n;
@@ -798,6 +868,7 @@ Status Engine::collect_view(int si, const KsgRec** view, BatchStats* bs, bool co
         bs->search_probes += S.probes;
         bs->block_windows += S.block_windows;
         bs->block_points += S.block_points;
+        bs->inc_windows += S.inc_windows;
         if (S.profile) {
             bs->prof_rounds += 1;
             bs->prof_brute_pairs += S.brute_pairs;

@@ -52,7 +52,7 @@ struct KsgRec {              // per-window result (56 B), written by the kernels
     double mi, h, nmi;
     long long s_psi, s_log;
     int32_t zero_eps;
-    int32_t pad;
+    int32_t reused;            // NEXT-3 incremental windows: points whose radius carried over from the previous window
     unsigned long long steps;  // sorted path: outward-scan candidate visits of this window (algorithmic work)
 };
 
@@ -60,6 +60,16 @@ struct KsgAcc {              // self-cleaning accumulator of a multi-tile window
     unsigned long long s_psi, s_log;
     unsigned int zero, done;
     unsigned long long steps;
+    unsigned int reused, pad;
+};
+
+struct KsgInc {              // NEXT-3 incremental window: its predecessor on the grid (sorted-list position)
+    int64_t eps_prev;        // offset (points) of the predecessor's radii in the EPS scratch
+    int64_t boffR, boffI;    // block storage offsets of the removed and the inserted block (d points each)
+    int32_t d;               // grid step = block size
+    int32_t level;           // chain level (-1: no chain, 0: scanned from scratch, >= 1: follows `pred`)
+    int32_t pred;            // sorted-list position of the predecessor (level >= 1)
+    int32_t pad;
 };
 
 struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
@@ -111,7 +121,11 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
                           int32_t n_items, cudaStream_t st, const KsgSegB* segb, const KsgBlk* blks,
-                          int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY);
+                          int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY, const KsgInc* inc,
+                          float* EPS, int2* CNT, const int32_t* lv_off, int n_lv, int inc_d_max,
+                          unsigned* sync);
+constexpr int kIncChain = 16;  // NEXT-3 incremental chains: a window scanned from scratch every this many
+constexpr int kIncMaxD = 1024; // NEXT-3 incremental chains: grid steps up to this (two blocks staged in SMEM)
 // small windows on the sorted path: one warp per window, E = 2, 4, 8 keys per lane (w <= 32 E)
 cudaError_t launch_wsorted(const KsgLaunch& L, const int32_t* list, int32_t n, int E, cudaStream_t st);
 // fused latency path: items {list pos, slice start}; slices of fused_ppc(w, gmax) points
@@ -147,6 +161,7 @@ struct BatchStats {
     int64_t scan_steps = 0, sorted_windows = 0, sorted_points = 0;
     int64_t brute_pairs = 0, search_probes = 0;
     int64_t block_windows = 0, block_points = 0;  // NEXT-3: windows merged from shared blocks, block points sorted
+    int64_t inc_windows = 0, eps_reused = 0;      // NEXT-3: incremental windows, points whose radius carried over
     double sorted_ms = 0.0, brute_ms = 0.0;
     int64_t prof_rounds = 0, prof_brute_pairs = 0, prof_scan_steps = 0, prof_probes = 0;
     double kernel_ms = 0.0;
@@ -210,6 +225,8 @@ private:
         int64_t ddrec_cap = 0;
         char* sscratch = nullptr;    // sorted path scratch: [P2 | OX | YS | TX | TI | TY] per point
         int64_t sscratch_cap = 0;
+        unsigned* sync = nullptr;    // NEXT-3 chains: [work ticket | per-window finished scan CTAs]
+        int64_t sync_cap = 0;
         std::vector<cudaEvent_t> events;
         cudaStream_t aux[kAux] = {};
         cudaEvent_t fork_ev = nullptr;
@@ -218,7 +235,7 @@ private:
         bool busy = false, profile = false;
         cudaStream_t st = nullptr;
         int64_t n = 0, pp = 0, brute_pairs = 0, probes = 0, sorted_windows = 0, spts = 0;
-        int64_t block_windows = 0, block_points = 0;
+        int64_t block_windows = 0, block_points = 0, inc_windows = 0;
         int n_ksg = 0, n_launch = 0;
         std::vector<int> launch_cls;
     };
@@ -245,7 +262,12 @@ private:
         std::vector<int32_t> ord, beta;      // NEXT-3 block plan scratch
         std::vector<KsgBlk> blks;
         std::vector<KsgSegB> segb;
+        std::vector<KsgInc> incs;
+        std::vector<int64_t> wboff;
     } bins_;
+    bool inc_on_ = false;            // NEXT-3 incremental radii along grid chains (ISYCOS_INCREMENTAL=1 or
+                                     // ISYCOS_F_INCREMENTAL enables; measured time-neutral, so off by default)
+    int32_t inc_chain_ = kIncChain;  // chain length (ISYCOS_INC_CHAIN)
     int32_t scan_unified_ = 0;       // ISYCOS_SCAN_UNIFIED=1: one side per iteration (measured 5-15 % slower; results identical)
     uint32_t poison_ = 0;            // ISYCOS_POISON=<byte>: shared memory, scan scratch and records pre-filled (T5)
     bool lat_split_on_ = true;       // latency-mode small windows on the 8-lanes-per-point kernel (ISYCOS_LAT_SPLIT=0: tile R=1)

@@ -106,7 +106,7 @@ __device__ inline double canon_ln(double v, const double* __restrict__ c) {
 }
 
 __device__ inline void finalize(const KsgLaunch& L, int w, long long s_psi, long long s_log, int zero, KsgRec* o,
-                         unsigned long long steps = 0) {
+                         unsigned long long steps = 0, unsigned reused = 0) {
     const double kQ = 2.3283064365386962890625e-10;  // 2^-32
     const double dw = (double)w;
     double a;
@@ -139,7 +139,7 @@ __device__ inline void finalize(const KsgLaunch& L, int w, long long s_psi, long
     o->s_psi = s_psi;
     o->s_log = s_log;
     o->zero_eps = zero;
-    o->pad = 0;
+    o->reused = (int32_t)reused;
     o->steps = steps;
 }
 
@@ -323,20 +323,25 @@ __device__ __forceinline__ int stage_tile(const float* gx, const float* gy, int6
 
 // ------------------------------------------------------------------ CTA reduce + window accumulate/finalize
 __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int ntiles, long long sp, long long sl,
-                                           int z, unsigned long long steps) {
+                                           int z, unsigned long long steps, unsigned reused = 0) {
     __shared__ long long r_sp[32], r_sl[32];
     __shared__ int r_z[32];
     __shared__ unsigned long long r_st[32];
     const int nw = blockDim.x >> 5;
     warp_sum(sp, sl, z);
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) steps += __shfl_down_sync(0xffffffffu, steps, off);
+    for (int off = 16; off >= 1; off >>= 1) {
+        steps += __shfl_down_sync(0xffffffffu, steps, off);
+        reused += __shfl_down_sync(0xffffffffu, reused, off);
+    }
+    __shared__ unsigned r_ru[32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
         r_sp[warp] = sp;
         r_sl[warp] = sl;
         r_z[warp] = z;
         r_st[warp] = steps;
+        r_ru[warp] = reused;
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
@@ -345,9 +350,10 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
         sl += r_sl[v];
         z += r_z[v];
         steps += r_st[v];
+        reused += r_ru[v];
     }
     if (ntiles == 1) {
-        finalize(L, w, sp, sl, z, &L.out[q], steps);
+        finalize(L, w, sp, sl, z, &L.out[q], steps, reused);
         return;
     }
     KsgAcc* A = &L.acc[q];
@@ -355,6 +361,7 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
     atomicAdd(&A->s_log, (unsigned long long)sl);
     atomicAdd(&A->zero, (unsigned)z);
     atomicAdd(&A->steps, steps);
+    if (reused) atomicAdd(&A->reused, reused);
     __threadfence();
     const unsigned ticket = atomicAdd(&A->done, 1u);
     if (ticket == (unsigned)(ntiles - 1)) {  // last tile of the window: finalize + reset the slot
@@ -363,8 +370,9 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
         const long long tl = (long long)atomicExch(&A->s_log, 0ull);
         const int tz = (int)atomicExch(&A->zero, 0u);
         const unsigned long long ts = atomicExch(&A->steps, 0ull);
+        const unsigned tr = atomicExch(&A->reused, 0u);
         atomicExch(&A->done, 0u);
-        finalize(L, w, tp, tl, tz, &L.out[q], ts);
+        finalize(L, w, tp, tl, tz, &L.out[q], ts, tr);
     }
 }
 
@@ -381,6 +389,7 @@ __device__ __forceinline__ void cta_finish(const KsgLaunch& L, int q, int w, int
 //          n_y likewise on the sorted y.  Bit-identical to the brute-force counts.
 constexpr int kSortedThreads = 128;  // points per CTA of the scan kernel (one point per thread)
 constexpr int kLockstepMinW = 2048;  // phase B: lockstep binary searches from this window size up (measured)
+constexpr int kCarried = -(1 << 20);  // stop_s.x <= this: NEXT-3 carried-over counts (n_x = kCarried - x)
 constexpr int kMergeThreads = kMergePts;  // elements per CTA of the XL rank merge
 
 // Order-preserving map of float bits to unsigned (finite values; -0 sorts just before +0, equal as floats).
@@ -643,12 +652,14 @@ __device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const f
 template <int K1>
 __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0, int wb, int we, float* eps_s,
                                                unsigned long long& steps, int2* stop_s = nullptr,
-                                               bool unified = true) {
+                                               bool unified = true, const uint16_t* wl = nullptr) {
+    // work items k in [wb, we): the points ml = k, or ml = wl[k] (the points an incremental window must scan)
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     constexpr int B = kScanB;
-    int mloc = wb + lane;
-    bool act = mloc < we;
+    int kcur = wb + lane;
+    bool act = kcur < we;
+    int mloc = act ? (wl ? (int)wl[kcur] : kcur) : 0;
     int next = wb + 32;
     float xi = 0.f, yi = 0.f;
     int lj = 0, rj = 0;  // next unvisited index on each side
@@ -755,7 +766,8 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
             if (fin) {
                 const int idx = next + __popc(fm & lt_mask);
                 if (idx < we) {
-                    mloc = idx;
+                    kcur = idx;
+                    mloc = wl ? (int)wl[idx] : idx;
                     start(mloc);
                 } else {
                     act = false;
@@ -772,12 +784,18 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
 template <bool V2>
 __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_t dbg, const float2* P2,
                                                const int32_t* OX, const float* YS, int m, float eps, long long& sp,
-                                               long long& sl, int& z, int xlo = 0, int xhi = INT_MAX) {
+                                               long long& sl, int& z, int xlo = 0, int xhi = INT_MAX,
+                                               int pre_nx = -1, int pre_ny = -1, int* out_nx = nullptr,
+                                               int* out_ny = nullptr) {
     const float* XS = reinterpret_cast<const float*>(P2);  // stride-2 view for the x binary searches
     const float2 me = P2[m];
     const float xv = me.x, yv = me.y;
     int nx = 0, ny = 0;
     float ex = eps, ey = eps;
+    if (!V2 && pre_nx >= 0) {  // NEXT-3: counts carried over (updated by the removed / inserted blocks)
+        nx = pre_nx;
+        ny = pre_ny;
+    } else {
     if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
     if (V2 || eps > 0.0f) {
         // The searches run in lockstep so their loads are in flight together (memory-level parallelism; one
@@ -835,6 +853,9 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
         ny = b4 - b3 - 1;
         }
     }
+    }
+    if (out_nx) *out_nx = nx;
+    if (out_ny) *out_ny = ny;
     sp += V2 ? L.psiq[nx] + L.psiq[ny] : L.psiq[nx + 1] + L.psiq[ny + 1];
     if (eps > 0.0f)
         sl += q32(canon_ln(__dmul_rn(2.0, (double)eps), L.lnc));
@@ -856,31 +877,202 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
 // with lj / rj the next unvisited indices, positions <= lj + 1 and >= rj - 1 are outside the strict
 // interval {|dx| < eps}: the x binary searches run on [lj + 2, m] and [m, rj - 1] (stop_s, optional).
 // (KSG-2's closed |dx| <= d_x, d_x <= eps, may include |dx| = eps: full ranges there.)
+// NEXT-3, incremental radius (the paper's influenced region, IR): window W' = W - R + I follows W
+// on a grid of step d (R = the d points that left, I = the d that entered; both are sorted blocks of the
+// NEXT-3 block storage, keys = sortable x << 32 | absolute index).  For a point kept from W with radius e,
+// if no removed point has d_ij <= e and no inserted point has d_ij < e, the (k+1) smallest distances of the
+// multiset are unchanged (removing elements > e and adding elements >= e), so eps in W' is exactly e.
+// Candidates with |fl(x_i - x_j)| <= e are one index range of a block (sorted x, monotone rounding): a
+// binary search for its start, then a walk while |dx| <= e.  Returns true if e carries over.
+__device__ __forceinline__ bool inc_unchanged(const float* __restrict__ bx, const float* __restrict__ by, int n,
+                                              float xv, float yv, float e, bool strict, unsigned long long& steps,
+                                              int& cx) {
+    // bx: the block's x ascending, by: the matching y (both in shared memory); cx = #{j : |fl(x_i - x_j)| < e}
+    int lo = 0, len = n;  // first j with fl(x_i - x_j) <= e  (x_j ascending: false ... true)
+    while (len > 0) {
+        ++steps;  // probes and candidate visits count as algorithmic work, like the scan's
+        const int h = len >> 1;
+        if (!(xv - bx[lo + h] <= e)) { lo += h + 1; len -= h + 1; } else len = h;
+    }
+    cx = 0;
+    for (int j = lo; j < n; ++j) {
+        ++steps;
+        const float xj = bx[j];
+        const float dx = fabsf(xv - xj);
+        if (xj > xv && !(dx <= e)) break;  // past the range on the right: fl(x_j - x_i) > e
+        cx += dx < e ? 1 : 0;
+        const float d = fmaxf(dx, fabsf(yv - by[j]));
+        if (strict ? (d < e) : (d <= e)) return false;
+    }
+    return true;
+}
+
+// #{j : |fl(y_i - y_j)| < e} in a y-ascending block (an index interval: two binary searches)
+__device__ __forceinline__ int inc_count_y(const float* __restrict__ ys, int n, float yv, float e,
+                                           unsigned long long& steps) {
+    int a = 0, la = n;  // first j with fl(y_i - y_j) < e
+    while (la > 0) {
+        ++steps;
+        const int h = la >> 1;
+        if (!(yv - ys[a + h] < e)) { a += h + 1; la -= h + 1; } else la = h;
+    }
+    int b = a, lb = n - a;  // first j >= a with !(fl(y_j - y_i) < e)
+    while (lb > 0) {
+        ++steps;
+        const int h = lb >> 1;
+        if (ys[b + h] - yv < e) { b += h + 1; lb -= h + 1; } else lb = h;
+    }
+    return b - a;
+}
+
+// Stage the removed (R) and inserted (I) blocks of an incremental window into shared memory: x ascending with
+// the matching y, and the block's y ascending: sb = [Rx | Ry | Rys | Ix | Iy | Iys], d floats each.
+__device__ __forceinline__ void inc_stage(const KsgInc& ic, const unsigned long long* __restrict__ BX,
+                                          const unsigned* __restrict__ BY, const float* __restrict__ gy, float* sb) {
+    const int d = ic.d;
+    for (int j = threadIdx.x; j < 2 * d; j += blockDim.x) {
+        const bool rr = j < d;
+        const int jj = rr ? j : j - d;
+        const int64_t off = (rr ? ic.boffR : ic.boffI) + jj;
+        const unsigned long long key = BX[off];
+        float* dst = sb + (rr ? 0 : 3 * d);
+        dst[jj] = unsortable((unsigned)(key >> 32));
+        dst[d + jj] = gy[(unsigned)(key & 0xffffffffu)];
+        dst[2 * d + jj] = unsortable(BY[off]);
+    }
+    __syncthreads();
+}
+
 template <int K1, bool V2>
 __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, int ntiles, const float2* P2,
                                             const int32_t* OX, const float* YS, int cta0, int cta_n, float* eps_s,
-                                            int2* stop_s = nullptr) {
+                                            int2* stop_s = nullptr, const KsgInc* inc = nullptr,
+                                            const float* eps_prev = nullptr, float* eps_out = nullptr,
+                                            const unsigned long long* BX = nullptr, uint16_t* wl_s = nullptr,
+                                            float* inc_sb = nullptr, const unsigned* BY = nullptr,
+                                            const int2* cnt_prev = nullptr, int2* cnt_out = nullptr,
+                                            unsigned* done = nullptr, int b_self = 0) {
     const int nwarps = blockDim.x >> 5;
     const int kPerWarp = (cta_n + nwarps - 1) / nwarps;
-    const int warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wb = min(warp * kPerWarp, cta_n);
     const int we = min(wb + kPerWarp, cta_n);
     unsigned long long steps = 0;
-    sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s, L.scan_unified != 0);
+    unsigned reused = 0;
+    int wl_cnt = -1;  // >= 0: incremental window, this warp's scan list length
+    if (inc && eps_prev && cnt_prev && stop_s && !V2) {
+        // incremental window: radii carried over where the removed / inserted blocks cannot change them; the
+        // remaining points (and the newly inserted ones) form this warp's scan list
+        const KsgWin W = L.wins[q];
+        if (done) {  // the predecessor's radii and counts must be complete (its CTAs took earlier work tickets)
+            if (threadIdx.x == 0) {
+                volatile unsigned* dp = done + inc->pred;
+                while (*dp < (unsigned)ntiles) __nanosleep(256);
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        inc_stage(*inc, BX, BY, L.pairs[W.pair].y, inc_sb);
+        const int d = inc->d;
+        const float* Rx = inc_sb;
+        const float* Ix = inc_sb + 3 * d;
+        uint16_t* wl = wl_s + wb;
+        int cnt = 0;
+        for (int k0 = wb; k0 < we; k0 += 32) {
+            const int ml = k0 + lane;
+            bool scan = false;
+            if (ml < we) {
+                const int m = cta0 + ml;
+                const int idx = OX[m];
+                scan = true;
+                if (idx < w - inc->d) {
+                    const float e = eps_prev[idx + d];
+                    const float2 me = P2[m];
+                    int rx = 0, ix = 0;
+                    if (!V2 && inc_unchanged(Rx, Rx + d, d, me.x, me.y, e, false, steps, rx) &&
+                        inc_unchanged(Ix, Ix + d, d, me.x, me.y, e, true, steps, ix)) {
+                        // the paper's IMR: the marginal counts of a kept point change only by the removed and inserted
+                        // points within eps of it (eps = 0: no counts); kCarried - n_x flags counts computed here
+                        // (phase A's stops are >= -kScanB - 1)
+                        eps_s[ml] = e;
+                        int2 st = make_int2(kCarried, 0);
+                        if (e > 0.0f) {
+                            const int2 c0 = cnt_prev[idx + d];
+                            const int ry = inc_count_y(Rx + 2 * d, d, me.y, e, steps);
+                            const int iy = inc_count_y(Ix + 2 * d, d, me.y, e, steps);
+                            st = make_int2(kCarried - (c0.x - rx + ix), c0.y - ry + iy);
+                        }
+                        stop_s[ml] = st;
+                        scan = false;
+                        ++reused;
+                    }
+                }
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, scan);
+            if (scan) wl[cnt + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)ml;
+            cnt += __popc(bm);
+        }
+        __syncwarp();
+        sorted_phase_a<K1>(P2, w, cta0, 0, cnt, eps_s, steps, stop_s, L.scan_unified != 0, wl);
+        wl_cnt = cnt;
+    } else {
+        sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s, L.scan_unified != 0);
+    }
     __syncthreads();
     long long sp = 0, sl = 0;
     int z = 0;
     const int64_t dbg = L.wins[q].dbg_off;
-    for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x) {
-        int xlo = 0, xhi = w;
+    if (wl_cnt >= 0) {
+        // incremental window: the carried points are cheap (terms from their counts), the scanned ones run the full
+        // phase B; both loops keep every lane busy (per-lane mixing would run the searches for the whole warp)
+        for (int ml = threadIdx.x; ml < cta_n; ml += blockDim.x) {
+            const int2 st = stop_s[ml];
+            if (st.x > kCarried) continue;
+            int nx = 0, ny = 0;
+            sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z, 0, w, kCarried - st.x, st.y,
+                               &nx, &ny);
+            const int i = OX[cta0 + ml];
+            eps_out[i] = eps_s[ml];
+            cnt_out[i] = make_int2(nx, ny);
+        }
+        const uint16_t* wl = wl_s + wb;
+        for (int k = lane; k < wl_cnt; k += 32) {
+            const int ml = wl[k];
+            const int2 st = stop_s[ml];
+            int nx = 0, ny = 0;
+            sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z, max(0, st.x + 2),
+                               min(w, st.y - 1), -1, -1, &nx, &ny);
+            const int i = OX[cta0 + ml];
+            eps_out[i] = eps_s[ml];
+            cnt_out[i] = make_int2(nx, ny);
+        }
+    }
+    for (int ml = threadIdx.x; wl_cnt < 0 && ml < cta_n; ml += blockDim.x) {
+        int xlo = 0, xhi = w, pnx = -1, pny = -1;
         if (stop_s) {
             const int2 st = stop_s[ml];
-            xlo = max(0, st.x + 2);
-            xhi = min(w, st.y - 1);
+            if (st.x <= kCarried) {  // counts carried over by the incremental pass
+                pnx = kCarried - st.x;
+                pny = st.y;
+            } else {
+                xlo = max(0, st.x + 2);
+                xhi = min(w, st.y - 1);
+            }
         }
-        sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z, xlo, xhi);
+        int nx = 0, ny = 0;
+        sorted_phase_b<V2>(L, w, dbg, P2, OX, YS, cta0 + ml, eps_s[ml], sp, sl, z, xlo, xhi, pnx, pny, &nx, &ny);
+        if (eps_out) {
+            const int i = OX[cta0 + ml];
+            eps_out[i] = eps_s[ml];
+            if (cnt_out) cnt_out[i] = make_int2(nx, ny);
+        }
     }
-    cta_finish(L, q, w, ntiles, sp, sl, z, steps);
+    if (done && eps_out) {  // publish this slice of the window's radii / counts to its successor
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(done + b_self, 1u);
+    }
+    cta_finish(L, q, w, ntiles, sp, sl, z, steps, reused);
 }
 
 // Throughput path scan kernel: the window was sorted by sort_window_kernel (+ rank_merge_kernel) into

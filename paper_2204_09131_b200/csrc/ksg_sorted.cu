@@ -207,31 +207,57 @@ template <int K1, bool V2>
 __global__ void __launch_bounds__(kSortedThreads)
     sorted_knn_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
                       const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
-                      const KsgItem* __restrict__ items) {
+                      const KsgItem* __restrict__ items, const KsgInc* __restrict__ inc, float* __restrict__ EPS,
+                      const unsigned long long* __restrict__ BX, const unsigned* __restrict__ BY,
+                      int2* __restrict__ CNT, unsigned* __restrict__ sync) {
     const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
     __shared__ float eps_s[kSortedPts];
     __shared__ int2 stop_s[kSortedPts];
+    __shared__ uint16_t wl_s[kSortedPts];  // NEXT-3 incremental windows: the points left to scan
+    extern __shared__ __align__(16) float inc_sb[];  // NEXT-3: removed / inserted blocks (x, y), 4 d floats
     if (L.poison) {
         poison_smem(L, eps_s, sizeof(eps_s));
         poison_smem(L, stop_s, sizeof(stop_s));
         __syncthreads();
     }
-    const KsgItem it = items[blockIdx.x];  // it.win = position in the sorted-class list, it.i0 = first point
+    // NEXT-3 chains: work items (level-major) are taken by ticket, so every item a CTA may wait for was taken by a
+    // CTA that is already running (forward progress without co-scheduling guarantees)
+    __shared__ int s_item;
+    if (sync) {
+        if (threadIdx.x == 0) s_item = (int)atomicAdd(sync, 1u);
+        __syncthreads();
+    }
+    const KsgItem it = items[sync ? s_item : blockIdx.x];  // it.win = position in the sorted list, it.i0 = first point
     const int b = it.win;
     const int q = list[b];
     const int w = L.wins[q].w;
     const int64_t o = soff[b];
+    const KsgInc* ic = inc ? &inc[b] : nullptr;
+    const bool chain = ic && ic->level >= 0;
     sorted_scan<K1, V2>(L, q, w, (w + ppc - 1) / ppc, P2g + o, OXg + o, YSg + o, it.i0, min(ppc, w - it.i0), eps_s,
-                        stop_s);
+                        stop_s, chain && ic->level > 0 ? ic : nullptr,
+                        chain && ic->level > 0 ? EPS + ic->eps_prev : nullptr, chain ? EPS + o : nullptr, BX, wl_s,
+                        inc_sb, BY, chain && ic->level > 0 ? CNT + ic->eps_prev : nullptr, chain ? CNT + o : nullptr,
+                        sync ? sync + 1 : nullptr, b);
 }
 
 template <int K1>
 cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const float2* P2,
-                     const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st) {
+                     const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st,
+                     const KsgInc* inc, float* EPS, const unsigned long long* BX, const unsigned* BY, int2* CNT,
+                     const int32_t* lv_off, int n_lv, int inc_d_max, unsigned* sync) {
+    // NEXT-3 chains: one launch over the level-ordered items; a level-j window's CTAs wait (per window) for the
+    // level-(j-1) predecessor's CTAs, which took earlier work tickets (no per-level launch tails)
+    (void)lv_off;
+    const bool chains = n_lv > 1 && sync;
+    const size_t smem = chains ? (size_t)6 * inc_d_max * sizeof(float) : 0;  // the two staged blocks
+    unsigned* sy = chains ? sync : nullptr;
     if (L.variant == 1)
-        sorted_knn_kernel<K1, true><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+        sorted_knn_kernel<K1, true><<<n_items, kSortedThreads, smem, st>>>(L, list, soff, P2, OX, YS, items, inc, EPS,
+                                                                           BX, BY, CNT, sy);
     else
-        sorted_knn_kernel<K1, false><<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, OX, YS, items);
+        sorted_knn_kernel<K1, false><<<n_items, kSortedThreads, smem, st>>>(L, list, soff, P2, OX, YS, items, inc, EPS,
+                                                                            BX, BY, CNT, sy);
     return cudaGetLastError();
 }
 }  // namespace
@@ -240,7 +266,9 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_segs, const KsgItem* mblocks, int32_t n_mblocks, float2* P2, int32_t* OX,
                           float* YS, float* TX, int32_t* TI, float* TY, int W2, const KsgItem* items,
                           int32_t n_items, cudaStream_t st, const KsgSegB* segb, const KsgBlk* blks,
-                          int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY) {
+                          int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY, const KsgInc* inc,
+                          float* EPS, int2* CNT, const int32_t* lv_off, int n_lv, int inc_d_max,
+                          unsigned* sync) {
     static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
     if (n_segs <= 0) return cudaSuccess;
     {
@@ -268,7 +296,8 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st)
+    ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st, inc, EPS, BX, BY, CNT, lv_off, n_lv, inc_d_max,
+                sync)
 }
 
 

@@ -1051,22 +1051,25 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         // records -> entries, pairs in parallel for big batches (each pair's records are a contiguous slice),
         // read straight from the pinned records; the per-pair scan-step sums feed the kernel stats
         const bool par = F.n >= 512;
-        std::vector<unsigned long long> steps(par ? F.pws.size() : 1, 0ull);
+        std::vector<unsigned long long> steps(par ? F.pws.size() : 1, 0ull), reuse(steps.size(), 0ull);
         pool.run(par ? (int)F.pws.size() : 1, [&](int p) {
             const int64_t i0 = par ? F.offs[p] : 0, i1 = par ? F.offs[p + 1] : F.n;
-            unsigned long long st = 0;
+            unsigned long long st = 0, ru = 0;
             for (int64_t i = i0; i < i1; ++i) {
                 Entry& e = *F.owners[i];
                 e.e = Eval{recs[i].mi, recs[i].h, recs[i].nmi};
                 e.ready = true;
                 st += recs[i].steps;
+                ru += (unsigned)recs[i].reused;
             }
             steps[par ? p : 0] = st;
+            reuse[par ? p : 0] = ru;
         });
         for (unsigned long long v : steps) {
             bs.scan_steps += (int64_t)v;
             if (profiled) bs.prof_scan_steps += (int64_t)v;
         }
+        for (unsigned long long v : reuse) bs.eps_reused += (int64_t)v;
         for (PairWork* pw : F.pws) pw->inflight -= 1;
         dlv_ms += std::chrono::duration<double, std::milli>(clk::now() - t_dl).count();
         F.busy = false;

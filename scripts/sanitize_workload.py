@@ -69,6 +69,7 @@ def main():
     check([(0, 1000), (2000, 4100), (7000, 7300)], "fused")
     check([(0, 9000), (100, 2100)] + [(37 + 256 * i, 37 + 256 * i + 1024) for i in range(6)], "sorted_xl_block",
           unfused=True)
+    check([(512 * i, 512 * i + 4096) for i in range(10)], "incremental", unfused=True, incremental=True)
     s = datagen.cfg1()
     ores, ost = oracle.search(s.series, s.pairs, oracle.make_params(s.search))
     for rep in range(args.repeat):

@@ -115,3 +115,42 @@ def test_latency_split_kernel_small_windows(isy, orc):
     r2 = orc.mi_batch(xi, yi, W2, 3)
     for f in FIELDS:
         assert np.array_equal(np.asarray(g2[f]), r2[f]), f
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_incremental_radii_chains(isy, orc, variant):
+    """NEXT-3 incremental radii (IR): windows that follow their predecessor by one 512-block (w = 4,096
+    and 16,384, as in the configs[2] sweep) reuse the predecessor's eps where the removed / inserted block cannot
+    change it.  Records and per-point outputs equal the from-scratch scan and the oracle (sampled windows)."""
+    wl = datagen.cfg3()
+    x, y = wl.series
+    x, y = x[200_000:260_000], y[200_000:260_000]
+    W = np.concatenate([grid_windows(len(x), 0, 512, [4096], 40), grid_windows(len(x), 1024, 512, [16384], 20)])
+    got = isy.isycos_mi_batch_ex(x, y, W, 4, variant=variant, unfused=True, debug=True, incremental=True)
+    st = got["stats"]
+    if variant == 0:  # KSG-2 windows are scanned from scratch (its kNN thresholds are not carried)
+        assert st["inc_windows"] > 0 and st["eps_reused_points"] > 0.5 * st["inc_windows"] * 4096
+    ref = isy.isycos_mi_batch_ex(x, y, W, 4, variant=variant, unfused=True, debug=True)
+    assert ref["stats"]["inc_windows"] == 0
+    for f in FIELDS + ("eps", "nx", "ny"):
+        assert np.array_equal(np.asarray(got[f]), np.asarray(ref[f])), f
+    sel = [0, 1, 17, 39, 41, 59]
+    o = orc.mi_batch(x, y, W[sel], 4, variant=variant)
+    for f in FIELDS:
+        assert np.array_equal(np.asarray(got[f])[sel], o[f]), f
+
+
+def test_incremental_radii_ties(isy, orc):
+    """Integer data: radii with many ties; a removed point at distance exactly eps forces a rescan."""
+    st = datagen.Stream(12, 1)
+    x = np.floor(st.uniform(30_000) * 24).astype(np.float32)
+    y = np.floor(st.uniform(30_000) * 24).astype(np.float32)
+    W = grid_windows(len(x), 100, 256, [2048, 4096], 30)
+    got = isy.isycos_mi_batch_ex(x, y, W, 3, unfused=True, debug=True, incremental=True)
+    assert got["stats"]["inc_windows"] > 0
+    ref = orc.mi_batch(x, y, W, 3)
+    for f in FIELDS:
+        assert np.array_equal(np.asarray(got[f]), ref[f]), f
+    scratch = isy.isycos_mi_batch_ex(x, y, W, 3, unfused=True, debug=True, no_block=True)
+    for f in ("eps", "nx", "ny"):
+        assert np.array_equal(got[f], scratch[f]), f
