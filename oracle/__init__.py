@@ -7,6 +7,7 @@ Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import os
 import subprocess
 from dataclasses import dataclass
@@ -19,11 +20,20 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC", "-pthread"]
 
 
+def _digest() -> str:  # content hash of the source and flags (an mtime can lie after a copy)
+    with open(_SRC, "rb") as fh:
+        return hashlib.sha256(fh.read() + " ".join(CXXFLAGS).encode()).hexdigest()
+
+
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    stamp = _LIB + ".sha256"
+    fresh = os.path.exists(_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == _digest()
+    if force or not fresh:
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["g++", *CXXFLAGS, "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
+        with open(stamp, "w") as fh:
+            fh.write(_digest() + "\n")
     return _LIB
 
 

@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libisycos.so")
+# ISYCOS_LIB: an alternative in-tree build of the same library (kernel A/B measurements only)
+LIB_PATH = os.environ.get("ISYCOS_LIB") or os.path.join(HERE, "libisycos.so")
 
 ISYCOS_OK, E_INVAL, E_RANGE, E_TOO_FEW, E_TRUNC, E_CUDA, E_NOMEM, E_NCCL = 0, -1, -2, -3, -4, -5, -6, -7
 F_PROFILE = 1

@@ -1,6 +1,7 @@
 """Build libisycos.so in-tree with nvcc for sm_100a (B200).  No JIT cache, no torch extension."""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -25,11 +26,25 @@ def _inputs():
     return files
 
 
+STAMP = LIB + ".sha256"
+
+
+def _digest() -> str:
+    """Content hash of every input plus the compiler command line (an mtime can lie after a copy or checkout)."""
+    h = hashlib.sha256()
+    for f in _inputs():
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join([NVCC, *ARCH, *FLAGS]).encode())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(f) > t for f in _inputs())
+    with open(STAMP) as fh:
+        return fh.read().strip() != _digest()
 
 
 def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
@@ -62,6 +77,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(_digest() + "\n")
     return LIB
 
 

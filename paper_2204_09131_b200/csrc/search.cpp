@@ -941,7 +941,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             return make_err(ISYCOS_E_INVAL, "chunk range outside the plan");
         plan = std::vector<std::pair<int64_t, int64_t>>(plan.begin() + P.chunk_begin, plan.begin() + P.chunk_end);
     }
-    const int max_active = 64;
+    // pairs (units) searched concurrently: every round batches the requests of all of them
+    int max_active = 64;
+    if (const char* ma = std::getenv("ISYCOS_MAX_ACTIVE")) max_active = std::max(1, std::atoi(ma));
     AlgStats total;
     BatchStats bs;
     int64_t distinct_w = 0, distinct_pp = 0;
