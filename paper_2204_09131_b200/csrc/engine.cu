@@ -13,6 +13,8 @@
 #include <numeric>
 #include <unordered_map>
 
+#include <chrono>
+
 #include "engine.h"
 
 namespace isy {
@@ -269,6 +271,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         S.busy = false;
     }
     S.n = 0;
+    using sclk = std::chrono::steady_clock;
+    const auto t_sub0 = sclk::now();
     const bool profile = (flags & ISYCOS_F_PROFILE) != 0;
     const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
@@ -521,6 +525,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         ISY_CK(cudaMalloc(&S.sscratch, c));
         S.sscratch_cap = c;
     }
+    const auto t_sub1 = sclk::now();
+    sub_ms[0] += std::chrono::duration<double, std::milli>(t_sub1 - t_sub0).count();
     // pack [pairs | wins | small lists | sorted list | sorted offsets | tile items | sorted items]
     const int64_t off_pairs = 0;
     const int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
@@ -611,6 +617,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // one H2D copy of the packed descriptors (kernels reading them from mapped host memory instead
     // measured 20 % slower on cfg2: a PCIe round trip on every CTA's critical path)
     char* dbase = S.dstage;
+    const auto t_sub2 = sclk::now();
+    sub_ms[1] += std::chrono::duration<double, std::milli>(t_sub2 - t_sub1).count();
     ISY_CK(cudaMemcpyAsync(S.dstage, S.hstage, total, cudaMemcpyHostToDevice, st));
     if (bs) bs->h2d_bytes += total;
     S.busy = true;  // from here on the slot's buffers are in use (an error return below leaves it to be synced)
@@ -655,7 +663,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     int n_launch = 0, n_ksg = 0;
     std::vector<int>& launch_cls = S.launch_cls;  // 0 sorted-marginal group, 1 brute-force launch
     launch_cls.clear();
-    // algorithmic work: brute-force ordered pairs; sorted path binary-search probes (5 searches per point)
+    // algorithmic work: brute-force ordered pairs; sorted path binary-search probes (4 searches per point: x and y interval ends)
     int64_t brute_pairs = 0, probes = 0;
     for (int s = 0; s < 4; ++s)
         for (int32_t q : small[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
@@ -666,18 +674,18 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     for (int32_t q : fused) {
         int lg = 0;
         while ((1 << lg) < wins[q].w) ++lg;
-        probes += (int64_t)wins[q].w * 5 * lg;
+        probes += (int64_t)wins[q].w * 4 * lg;
     }
     for (auto& v : wsorted)
         for (int32_t q : v) {
             int lg = 0;
             while ((1 << lg) < wins[q].w) ++lg;
-            probes += (int64_t)wins[q].w * 5 * lg;
+            probes += (int64_t)wins[q].w * 4 * lg;
         }
     for (int32_t q : sorted) {
         int lg = 0;
         while ((1 << lg) < wins[q].w) ++lg;
-        probes += (int64_t)wins[q].w * 5 * lg;
+        probes += (int64_t)wins[q].w * 4 * lg;
     }
     auto ev_pair = [&](int i) -> std::pair<cudaEvent_t, cudaEvent_t> {
         while ((int)S.events.size() < 2 * (i + 1)) {
@@ -826,6 +834,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.block_windows = blk_windows;
     S.block_points = blk_pts;
     S.inc_windows = inc_windows;
+    sub_ms[2] += std::chrono::duration<double, std::milli>(sclk::now() - t_sub2).count();
     return Status{};
 }
 

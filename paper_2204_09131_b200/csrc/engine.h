@@ -205,6 +205,9 @@ public:
     // submit); the caller adds the records' scan steps to bs->scan_steps itself (count_steps = false)
     Status collect_view(int si, const KsgRec** view, BatchStats* bs, bool count_steps, bool* profiled = nullptr);
     cudaStream_t second_stream() const { return stream2_; }
+    // host time of submit() (ms, accumulated over the engine's life): binning + block plan, descriptor packing,
+    // launches (ISYCOS_TRACE summaries)
+    double sub_ms[3] = {0.0, 0.0, 0.0};
     Status fork_second_stream(cudaStream_t st);  // second stream waits for work queued on st so far
     Status join_second_stream(cudaStream_t st);  // st waits for the second stream
 

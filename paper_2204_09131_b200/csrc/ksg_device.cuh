@@ -644,6 +644,53 @@ __device__ __forceinline__ void chunk_sort(const float* __restrict__ gx, const f
     }
 }
 
+// ---- phase A's top list: the K = k smallest d_ij over the visited j != i (self, d_ii = 0, is never visited
+// by the outward scan, so eps_i = the K-th entry = the (k+1)-th smallest of the multiset including self).
+__device__ __forceinline__ void cswap(float& a, float& b) {
+    const float lo = fminf(a, b);
+    b = fmaxf(a, b);
+    a = lo;
+}
+// r (sorted ascending, K entries) <- the K smallest of r U d[0..8), sorted: exact multiset order statistics.
+// K = 4 and K = 8 use merge networks (sorted block, then the bitonic half-cleaner min(r[i], b[K-1-i]), which
+// leaves exactly the K smallest of the union as a bitonic sequence, then a bitonic merger): 44 / 70 FMNMX per
+// block instead of 56 / 120 for eight insertions.  Other K: insertion network per candidate.
+template <int K>
+__device__ __forceinline__ void topk_merge8(float (&r)[K], float (&d)[8]) {
+    if constexpr (K == 4) {
+        // sort both halves of the block (5 comparators each)
+        cswap(d[0], d[1]); cswap(d[2], d[3]); cswap(d[0], d[2]); cswap(d[1], d[3]); cswap(d[1], d[2]);
+        cswap(d[4], d[5]); cswap(d[6], d[7]); cswap(d[4], d[6]); cswap(d[5], d[7]); cswap(d[5], d[6]);
+        // the block's 4 smallest (bitonic), then sorted
+        float b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b[i] = fminf(d[i], d[7 - i]);
+        cswap(b[0], b[2]); cswap(b[1], b[3]); cswap(b[0], b[1]); cswap(b[2], b[3]);
+        // the 4 smallest of r U b (bitonic), then sorted
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = fminf(r[i], b[3 - i]);
+        cswap(r[0], r[2]); cswap(r[1], r[3]); cswap(r[0], r[1]); cswap(r[2], r[3]);
+    } else if constexpr (K == 8) {
+        // Batcher odd-even merge sort of the block (19 comparators)
+        cswap(d[0], d[1]); cswap(d[2], d[3]); cswap(d[4], d[5]); cswap(d[6], d[7]);
+        cswap(d[0], d[2]); cswap(d[1], d[3]); cswap(d[4], d[6]); cswap(d[5], d[7]);
+        cswap(d[1], d[2]); cswap(d[5], d[6]);
+        cswap(d[0], d[4]); cswap(d[1], d[5]); cswap(d[2], d[6]); cswap(d[3], d[7]);
+        cswap(d[2], d[4]); cswap(d[3], d[5]);
+        cswap(d[1], d[2]); cswap(d[3], d[4]); cswap(d[5], d[6]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = fminf(r[i], d[7 - i]);
+        // bitonic merger of 8
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cswap(r[i], r[i + 4]);
+        cswap(r[0], r[2]); cswap(r[1], r[3]); cswap(r[4], r[6]); cswap(r[5], r[7]);
+        cswap(r[0], r[1]); cswap(r[2], r[3]); cswap(r[4], r[5]); cswap(r[6], r[7]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) topk_insert<K>(r, d[u]);
+    }
+}
+
 // Phase A of the sorted path for the points [wb, we) (positions relative to cta0) of one warp: exact
 // k-NN radius by outward scan in x order (a3).  Writes eps_s[ml]; adds the candidate visits to `steps`.
 // P2 must carry sentinels: P2[-kScanB..-1] = (-inf, 0), P2[w..w+kScanB-1] = (+inf, 0) (no bounds checks).
@@ -664,30 +711,34 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
     float xi = 0.f, yi = 0.f;
     int lj = 0, rj = 0;  // next unvisited index on each side
     bool lact = false, ract = false;
-    float rk[K1];
+    constexpr int K = K1 - 1;  // the k smallest over j != i (the scan never visits self)
+    float rk[K];
     auto start = [&](int ml) {
         const int m = cta0 + ml;
         const float2 me = P2[m];
         xi = me.x;
         yi = me.y;
-        rk[0] = 0.0f;  // self: d_ii = 0
 #pragma unroll
-        for (int t = 1; t < K1; ++t) rk[t] = kInf;
+        for (int t = 0; t < K; ++t) rk[t] = kInf;
         lj = m - 1;
         rj = m + 1;
         lact = true;  // the sentinels end a side
         ract = true;
     };
-    // a block with any candidate below r_{k+1}: all four through the min/max network (exact: inserting
+    // a block with any candidate below r_{k+1}: the whole block through the merge network (exact: merging
     // d >= r_{k+1} leaves the list unchanged), no per-candidate branches
-    auto visit = [&](const float (&d)[B]) {
+    static_assert(B == 8, "topk_merge8 takes blocks of 8");
+    auto visit = [&](float (&d)[B]) {
         float mn = d[0];
 #pragma unroll
         for (int u = 1; u < B; ++u) mn = fminf(mn, d[u]);
-        if (mn < rk[K1 - 1]) {
-#pragma unroll
-            for (int u = 0; u < B; ++u) topk_insert<K1>(rk, d[u]);
-        }
+        if (mn < rk[K - 1]) topk_merge8<K>(rk, d);
+    };
+    // candidate visits of the finished point (algorithmic work), from its final stops: the left side visited
+    // m-1 down to max(0, lj+1), the right side m+1 up to min(w-1, rj-1) (sentinels are not counted)
+    auto visited = [&]() -> unsigned long long {
+        const int m = cta0 + mloc;
+        return (unsigned long long)(min(m, m - 1 - lj) + min(w - 1 - m, rj - m - 1));
     };
     if (act) start(mloc);
     bool toggle = false;
@@ -711,18 +762,17 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                 far = dx;
             }
             visit(d);
-            const float r = rk[K1 - 1];
+            const float r = rk[K - 1];
             if (useL) {
-                steps += max(0, min(B, lj + 1));
                 lj -= B;
                 lact = far < r;
             } else {
-                steps += max(0, min(B, w - rj));
                 rj += B;
                 ract = far < r;
             }
             if (!lact && !ract) {
                 fin = true;
+                steps += visited();
                 eps_s[mloc] = r;
                 if (stop_s) stop_s[mloc] = make_int2(lj, rj);
             }
@@ -737,9 +787,8 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                     far = dx;
                 }
                 visit(d);
-                steps += max(0, min(B, lj + 1));
                 lj -= B;
-                lact = far < rk[K1 - 1];
+                lact = far < rk[K - 1];
             }
             if (ract) {
                 float d[B], far = 0.f;
@@ -751,13 +800,13 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                     far = dx;
                 }
                 visit(d);
-                steps += max(0, min(B, w - rj));
                 rj += B;
-                ract = far < rk[K1 - 1];
+                ract = far < rk[K - 1];
             }
             if (!lact && !ract) {
                 fin = true;
-                eps_s[mloc] = rk[K1 - 1];
+                steps += visited();
+                eps_s[mloc] = rk[K - 1];
                 if (stop_s) stop_s[mloc] = make_int2(lj, rj);  // next unvisited index on each side
             }
         }
@@ -799,11 +848,10 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
     if (V2) ksg2_sorted_radii(P2, XS, OX, m, w, xv, yv, eps, L.k, &ex, &ey);
     if (V2 || eps > 0.0f) {
         // The searches run in lockstep so their loads are in flight together (memory-level parallelism; one
-        // search at a time was latency-bound): first the two x bounds with the y pivot p, then the two y
-        // bounds.  Each search finds the end of the prefix of [b, b + n) on which its predicate holds.
+        // search at a time was latency-bound): the two x bounds and the two y bounds.  Each search finds the
+        // end of the prefix of [b, b + n) on which its predicate holds.
         //   x left  [lo, m):  !(fl(x_i - x_j) < ex)      x right [m, hi): fl(x_j - x_i) < ex
-        //   y pivot [0, w):   YS[j] < y_i                y left  [0, p):  !(fl(y_i - y_j) < ey)
-        //   y right [p, w):   fl(y_j - y_i) < ey
+        //   y left  [0, w):   !(fl(y_i - y_j) < ey)      y right [0, w):  fl(y_j - y_i) < ey
         const int xl0 = V2 ? 0 : xlo, xr1 = V2 ? w : min(w, xhi);
         if (w < kLockstepMinW) {  // short searches: one at a time (the lockstep predication costs more there)
             int lo = xl0, hi = m;
@@ -819,11 +867,14 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
                 if (XS[2 * mid] - xv < ex) lo = mid + 1; else hi = mid;
             }
             nx = lo - Lx - 1;
-            const int p = lower_bound_f(YS, w, yv);
-            ny = right_bound(YS, p, w, yv, ey) - left_bound_f(YS, p, yv, ey) - 1;
+            // y: both ends searched over the whole sorted array (no pivot search for y_i's own rank): for
+            // YS[j] >= y_i, fl(y_i - YS[j]) <= 0 < ey, and for YS[j] <= y_i, fl(YS[j] - y_i) <= 0 < ey, so each
+            // predicate is monotone on [0, w) and its first flip is the interval end
+            ny = right_bound(YS, 0, w, yv, ey) - left_bound_f(YS, w, yv, ey) - 1;
         } else {
-        int b0 = xl0, n0 = m - xl0, b1 = m, n1 = xr1 - m, b2 = 0, n2 = w;
-        while ((n0 | n1 | n2) > 0) {
+        int b0 = xl0, n0 = m - xl0, b1 = m, n1 = xr1 - m;
+        int b3 = 0, n3 = w, b4 = 0, n4 = w;  // y ends over [0, w) (monotone predicates, see above)
+        while ((n0 | n1 | n3 | n4) > 0) {
             if (n0 > 0) {
                 const int h = n0 >> 1;
                 if (!(xv - XS[2 * (b0 + h)] < ex)) { b0 += h + 1; n0 -= h + 1; } else n0 = h;
@@ -832,15 +883,6 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
                 const int h = n1 >> 1;
                 if (XS[2 * (b1 + h)] - xv < ex) { b1 += h + 1; n1 -= h + 1; } else n1 = h;
             }
-            if (n2 > 0) {
-                const int h = n2 >> 1;
-                if (YS[b2 + h] < yv) { b2 += h + 1; n2 -= h + 1; } else n2 = h;
-            }
-        }
-        nx = b1 - b0 - 1;
-        const int p = b2;
-        int b3 = 0, n3 = p, b4 = p, n4 = w - p;
-        while ((n3 | n4) > 0) {
             if (n3 > 0) {
                 const int h = n3 >> 1;
                 if (!(yv - YS[b3 + h] < ey)) { b3 += h + 1; n3 -= h + 1; } else n3 = h;
@@ -850,6 +892,7 @@ __device__ __forceinline__ void sorted_phase_b(const KsgLaunch& L, int w, int64_
                 if (YS[b4 + h] - yv < ey) { b4 += h + 1; n4 -= h + 1; } else n4 = h;
             }
         }
+        nx = b1 - b0 - 1;
         ny = b4 - b3 - 1;
         }
     }

@@ -1286,8 +1286,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                     wmax = std::max<int64_t>(wmax, kw.w);
                 }
                 const double host = std::chrono::duration<double, std::milli>(t_ev - t_last).count();
-                std::fprintf(trace, "%lld %.4f %.4f %lld %lld %lld\n", (long long)round_no, host, ev_ms, (long long)batch_n,
-                             (long long)sw2, (long long)wmax);
+                const double adv_r = std::chrono::duration<double, std::milli>(t_ret - t_adv).count();
+                const double asm_r = std::chrono::duration<double, std::milli>(t_ev - t_asm).count();
+                std::fprintf(trace, "%lld %.4f %.4f %lld %lld %lld %.4f %.4f\n", (long long)round_no, host, ev_ms,
+                             (long long)batch_n, (long long)sw2, (long long)wmax, adv_r, asm_r);
             }
             ++round_no;
             t_last = clk::now();
@@ -1340,6 +1342,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             std::fprintf(trace, "# host: advance %.3f ms (%d threads), other %.3f ms (deliver %.3f, retire %.3f, "
                          "assemble %.3f), eval %.3f ms (collect wait %.3f), rounds %lld\n", adv_ms, pool.size(),
                          wall - eval_ms - adv_ms, dlv_ms, ret_ms, asm_ms, eval_ms, wait_ms, (long long)round_no);
+        if (trace)
+            std::fprintf(trace, "# engine submit (cumulative): binning + plan %.3f ms, packing %.3f ms, launches %.3f ms\n",
+                         eng->sub_ms[0], eng->sub_ms[1], eng->sub_ms[2]);
     }
     return Status{};
 }
