@@ -47,16 +47,18 @@ def needs_build() -> bool:
         return fh.read().strip() != _digest()
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, defines=(), out: str = "") -> str:
+    """Build libisycos.so.  `defines` + `out`: an alternative build (kernel A/B measurements, loaded through
+    ISYCOS_LIB) into another file; it never replaces the product library."""
+    if not out and not force and not needs_build():
         return LIB
     objs = []
-    tmpdir = os.path.join(HERE, "build")
+    tmpdir = os.path.join(HERE, "build" + ("_" + os.path.basename(out).replace(".", "_") if out else ""))
     os.makedirs(tmpdir, exist_ok=True)
     procs = []
     for s in SOURCES:
         obj = os.path.join(tmpdir, s + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
                os.path.join(CSRC, s), "-o", obj]
         if ptxas_info and s.endswith(".cu"):
             cmd.insert(1, "-Xptxas=-v")
@@ -66,17 +68,20 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
         objs.append(obj)
     failed = []
     for s, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0:
-            failed.append((s, out))
-        elif verbose and out:
-            sys.stderr.write(out)
+            failed.append((s, log))
+        elif verbose and log:
+            sys.stderr.write(log)
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB + f".tmp{os.getpid()}"
+    target = out or LIB
+    tmp = target + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
+    if out:
+        return out
     with open(STAMP, "w") as fh:
         fh.write(_digest() + "\n")
     return LIB

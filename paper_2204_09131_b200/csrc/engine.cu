@@ -373,6 +373,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // [256, kSortedMaxW] (TD: the delta-grid of a partition, delta = s/4, shared by the layer's windows and
     // their noise sub-windows; sweeps: the stride).  Each block is sorted once per batch; its windows merge
     // the sorted blocks (the merge levels from beta up) instead of sorting from scratch.
+    const auto t_bin = sclk::now();
+    sub_ms[0] += std::chrono::duration<double, std::milli>(t_bin - t_sub0).count();
     auto& wbeta = bins_.beta;
     auto& blks = bins_.blks;
     auto& segb = bins_.segb;
@@ -382,10 +384,15 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     std::vector<int64_t> wboff;
     int blk_beta_max = 0;
     int64_t blk_store = 0, blk_pts = 0, blk_windows = 0;
+    auto& ord = bins_.ord;
+    ord.clear();
     if (block_sort_on_ && !(flags & ISYCOS_F_NO_BLOCK) && sorted.size() >= 2) {
-        auto& ord = bins_.ord;
-        ord.resize(sorted.size());
-        std::iota(ord.begin(), ord.end(), 0);
+        // only windows whose size is a multiple of 256 can share blocks (beta >= 256 divides w): search rounds
+        // of other sizes (BU: s_min + j delta_bu) skip the plan's sort and maps entirely
+        for (size_t b = 0; b < sorted.size(); ++b)
+            if ((wins[sorted[b]].w & 255) == 0) ord.push_back((int32_t)b);
+    }
+    if (ord.size() >= 2) {
         std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t c) {
             const KsgWin& A = wins[sorted[a]];
             const KsgWin& C = wins[sorted[c]];
@@ -485,6 +492,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             }
         }
     }
+    const auto t_plan = sclk::now();
+    sub_ms[1] += std::chrono::duration<double, std::milli>(t_plan - t_bin).count();
     // sorted scan: 1024 points per CTA when the batch fills the GPU (better lane balance in the per-warp
     // work queues), else 256 (more CTAs per window: latency-bound rounds)
     const int ppc = spts >= (int64_t)148 * 8 * 1024 ? sorted_ppc_ : 256;
@@ -526,7 +535,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         S.sscratch_cap = c;
     }
     const auto t_sub1 = sclk::now();
-    sub_ms[0] += std::chrono::duration<double, std::milli>(t_sub1 - t_sub0).count();
+    sub_ms[2] += std::chrono::duration<double, std::milli>(t_sub1 - t_plan).count();
     // pack [pairs | wins | small lists | sorted list | sorted offsets | tile items | sorted items]
     const int64_t off_pairs = 0;
     const int64_t off_wins = align64(off_pairs + n_pairs * (int64_t)sizeof(PairPtrs));
@@ -618,7 +627,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // measured 20 % slower on cfg2: a PCIe round trip on every CTA's critical path)
     char* dbase = S.dstage;
     const auto t_sub2 = sclk::now();
-    sub_ms[1] += std::chrono::duration<double, std::milli>(t_sub2 - t_sub1).count();
+    sub_ms[3] += std::chrono::duration<double, std::milli>(t_sub2 - t_sub1).count();
     ISY_CK(cudaMemcpyAsync(S.dstage, S.hstage, total, cudaMemcpyHostToDevice, st));
     if (bs) bs->h2d_bytes += total;
     S.busy = true;  // from here on the slot's buffers are in use (an error return below leaves it to be synced)
@@ -834,7 +843,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     S.block_windows = blk_windows;
     S.block_points = blk_pts;
     S.inc_windows = inc_windows;
-    sub_ms[2] += std::chrono::duration<double, std::milli>(sclk::now() - t_sub2).count();
+    sub_ms[4] += std::chrono::duration<double, std::milli>(sclk::now() - t_sub2).count();
     return Status{};
 }
 

@@ -85,7 +85,7 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t* dbg_ny;
     int32_t k;
     int32_t variant;
-    int32_t knn_mode;        // small-window kNN insertion: 1 branch-free network, 0 guarded
+    int32_t knn_mode;        // small-window kernel: bit 0 branch-free kNN insertion (else guarded), bit 1 ballot counts
     int32_t two;             // the constant 2, passed at run time (see acc_lt)
     int32_t sorted_ppc;      // sorted path: points per scan CTA (256 or 1024)
     int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
@@ -205,9 +205,9 @@ public:
     // submit); the caller adds the records' scan steps to bs->scan_steps itself (count_steps = false)
     Status collect_view(int si, const KsgRec** view, BatchStats* bs, bool count_steps, bool* profiled = nullptr);
     cudaStream_t second_stream() const { return stream2_; }
-    // host time of submit() (ms, accumulated over the engine's life): binning + block plan, descriptor packing,
-    // launches (ISYCOS_TRACE summaries)
-    double sub_ms[3] = {0.0, 0.0, 0.0};
+    // host time of submit() (ms, accumulated over the engine's life): binning, NEXT-3 block plan, other
+    // preparation, descriptor packing, launches (ISYCOS_TRACE summaries)
+    double sub_ms[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     Status fork_second_stream(cudaStream_t st);  // second stream waits for work queued on st so far
     Status join_second_stream(cudaStream_t st);  // st waits for the second stream
 

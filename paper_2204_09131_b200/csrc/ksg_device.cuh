@@ -729,10 +729,14 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
     // d >= r_{k+1} leaves the list unchanged), no per-candidate branches
     static_assert(B == 8, "topk_merge8 takes blocks of 8");
     auto visit = [&](float (&d)[B]) {
+#ifdef ISY_MERGE_ALWAYS
+        topk_merge8<K>(rk, d);
+#else
         float mn = d[0];
 #pragma unroll
         for (int u = 1; u < B; ++u) mn = fminf(mn, d[u]);
         if (mn < rk[K - 1]) topk_merge8<K>(rk, d);
+#endif
     };
     // candidate visits of the finished point (algorithmic work), from its final stops: the left side visited
     // m-1 down to max(0, lj+1), the right side m+1 up to min(w-1, rj-1) (sentinels are not counted)

@@ -65,8 +65,39 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
     unsigned cx[R], cy[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
-    const unsigned two = (unsigned)L.two;
-    for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], two);
+    if (L.knn_mode & 2) {
+        // a4, warp-ballot form (north star; SURVEY §8(a) a4 option 1, kept for the A/B): for each point i in
+        // turn (warp-uniform), lane l tests the candidates j = l + 32 c it holds in registers with the same
+        // predicate as acc_lt (sign bit of fl(|fl(x_i - x_j)| - e_i)); n(i) = sum of popc(ballot).  Measured
+        // slower than the per-lane form, so off by default (ISYCOS_KNN_MODE bit 1).
+        float xj[R], yj[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            const int j = lane + 32 * c;
+            xj[c] = j < w ? sx[j] : kInf;  // +inf: never counted
+            yj[c] = j < w ? sy[j] : kInf;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            for (int l = 0; l < 32 && l + 32 * r < w; ++l) {  // warp-uniform bounds
+                const float xb = __shfl_sync(0xffffffffu, xi[r], l), yb = __shfl_sync(0xffffffffu, yi[r], l);
+                const float eb = __shfl_sync(0xffffffffu, ex[r], l), fb = __shfl_sync(0xffffffffu, ey[r], l);
+                unsigned nx = 0, ny = 0;
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    nx += __popc(__ballot_sync(0xffffffffu, (__float_as_uint(fabsf(xb - xj[c]) - eb) >> 31) != 0u));
+                    ny += __popc(__ballot_sync(0xffffffffu, (__float_as_uint(fabsf(yb - yj[c]) - fb) >> 31) != 0u));
+                }
+                if (lane == l) {
+                    cx[r] = nx;
+                    cy[r] = ny;
+                }
+            }
+        }
+    } else {
+        const unsigned two = (unsigned)L.two;
+        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], two);
+    }
     long long sp = 0, sl = 0;
     int z = 0;
     point_terms<R, V2>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
@@ -91,7 +122,7 @@ cudaError_t small_kb(const KsgLaunch& L, const int32_t* list, int32_t n, int R, 
 template <int K1>
 cudaError_t small_k(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st) {
     if (L.variant == 1) return small_kb<K1, true, true>(L, list, n, R, st);
-    return L.knn_mode == 1 ? small_kb<K1, true, false>(L, list, n, R, st)
+    return (L.knn_mode & 1) ? small_kb<K1, true, false>(L, list, n, R, st)
                            : small_kb<K1, false, false>(L, list, n, R, st);
 }
 

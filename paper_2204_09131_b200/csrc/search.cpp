@@ -1343,8 +1343,9 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                          "assemble %.3f), eval %.3f ms (collect wait %.3f), rounds %lld\n", adv_ms, pool.size(),
                          wall - eval_ms - adv_ms, dlv_ms, ret_ms, asm_ms, eval_ms, wait_ms, (long long)round_no);
         if (trace)
-            std::fprintf(trace, "# engine submit (cumulative): binning + plan %.3f ms, packing %.3f ms, launches %.3f ms\n",
-                         eng->sub_ms[0], eng->sub_ms[1], eng->sub_ms[2]);
+            std::fprintf(trace, "# engine submit (cumulative): binning %.3f ms, block plan %.3f ms, other prep %.3f ms, "
+                         "packing %.3f ms, launches %.3f ms\n", eng->sub_ms[0], eng->sub_ms[1], eng->sub_ms[2],
+                         eng->sub_ms[3], eng->sub_ms[4]);
     }
     return Status{};
 }
