@@ -11,6 +11,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <thread>
 #include <unordered_map>
 
 #include <chrono>
@@ -277,8 +278,38 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const bool use_sorted = sorted_on_ && !(flags & ISYCOS_F_BRUTE);
     if (n <= 0) return Status{};
     if (n > INT32_MAX / 2) return make_err(ISYCOS_E_INVAL, "batch too large");
-    int64_t w_max = 0;
-    for (int64_t i = 0; i < n; ++i) w_max = std::max<int64_t>(w_max, wins[i].w);
+    // Binning (a1 on the device side): one pass for w_max and the fused-path point count, one for the size
+    // classes.  Large batches (TD layer starts: up to 10^7 windows, memory-bound single-threaded) split both
+    // passes into contiguous chunks on host threads; the chunks' class lists are concatenated in chunk order,
+    // so every list is in ascending window order exactly as in the serial pass.
+    const int n_chunks = n >= (int64_t)1 << 18 ? (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    auto par = [&](auto&& fn) {
+        if (n_chunks == 1) {
+            fn(0, (int64_t)0, n);
+            return;
+        }
+        std::vector<std::thread> th;
+        for (int c = 1; c < n_chunks; ++c) th.emplace_back(fn, c, n * c / n_chunks, n * (c + 1) / n_chunks);
+        fn(0, (int64_t)0, n / n_chunks);
+        for (auto& t : th) t.join();
+    };
+    const bool use_fused_path = use_sorted && fused_on_ && !(flags & ISYCOS_F_UNFUSED);
+    std::vector<int64_t> c_wmax(n_chunks, 0), c_fpts(n_chunks, 0);
+    par([&](int c, int64_t i0, int64_t i1) {
+        int64_t wm = 0, fp = 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const int64_t w = wins[i].w;
+            wm = std::max(wm, w);
+            fp += (w >= sorted_min_w_ && w <= kFusedMaxW) ? w : 0;
+        }
+        c_wmax[c] = wm;
+        c_fpts[c] = fp;
+    });
+    int64_t w_max = 0, fpts = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+        w_max = std::max(w_max, c_wmax[c]);
+        fpts += c_fpts[c];
+    }
     {
         Status s = ensure_psi(w_max + 1, st);
         if (!s.ok()) return s;
@@ -306,38 +337,68 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     int64_t pp = 0;
     // latency mode for the sorted path: few sorted points in the batch -> fused sort+scan kernel (a CTA
     // per window slice, no scratch round trip); otherwise the throughput form (sort once, then scan)
-    bool fuse = use_sorted && fused_on_ && !(flags & ISYCOS_F_UNFUSED);
-    if (fuse) {
-        int64_t fpts = 0;
-        for (int64_t i = 0; i < n; ++i)
-            if (wins[i].w >= sorted_min_w_ && wins[i].w <= kFusedMaxW) fpts += wins[i].w;
-        fuse = fpts <= fused_max_pts_;
-    }
-    for (int64_t i = 0; i < n; ++i) {
-        const int w = wins[i].w;
-        pp += (int64_t)w * (w - 1);
-        const int R = small_class_R(w);
-        if (R >= 2 && use_sorted && w >= wsorted_min_w_) {
-            wsorted[R == 2 ? 0 : R == 4 ? 1 : 2].push_back((int32_t)i);
-        } else if (R && !(use_sorted && w >= sorted_min_w_)) {
-            small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
-        } else if (fuse && w >= sorted_min_w_ && w <= kFusedMaxW) {
-            fused.push_back((int32_t)i);
-            while (fused_n2 < w) fused_n2 <<= 1;
-        } else if (use_sorted && w >= sorted_min_w_) {
-            sorted.push_back((int32_t)i);
-            soff.push_back(spts + kScanB);  // kScanB sentinel entries on either side of the window's region
-            spts += w + 2 * kScanB;
-            n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
-            if (w > kSortedMaxW) n_mblocks += (w + kMergePts - 1) / kMergePts;
-            int n2 = 1;
-            while (n2 < std::min(w, kSortedMaxW)) n2 <<= 1;
-            W2 = std::max(W2, n2);
-        } else {
-            const int tr = tile_R(w);
-            tile[tr == 2 ? 0 : 1].push_back((int32_t)i);
-            n_items += (w + kTileThreads * tr - 1) / (kTileThreads * tr);
+    const bool fuse = use_fused_path && fpts <= fused_max_pts_;
+    if ((int)cbins_.size() < n_chunks) cbins_.resize(n_chunks);
+    par([&](int c, int64_t i0, int64_t i1) {
+        ChunkBins& B = cbins_[c];
+        for (auto& v : B.small) v.clear();
+        for (auto& v : B.tile) v.clear();
+        for (auto& v : B.wsorted) v.clear();
+        B.sorted.clear();
+        B.fused.clear();
+        B.soff.clear();
+        B.spts = B.n_segs = B.n_mblocks = B.n_items = B.pp = 0;
+        B.W2 = 0;
+        B.fused_n2 = 256;
+        for (int64_t i = i0; i < i1; ++i) {
+            const int w = wins[i].w;
+            B.pp += (int64_t)w * (w - 1);
+            const int R = small_class_R(w);
+            if (R >= 2 && use_sorted && w >= wsorted_min_w_) {
+                B.wsorted[R == 2 ? 0 : R == 4 ? 1 : 2].push_back((int32_t)i);
+            } else if (R && !(use_sorted && w >= sorted_min_w_)) {
+                B.small[R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3].push_back((int32_t)i);
+            } else if (fuse && w >= sorted_min_w_ && w <= kFusedMaxW) {
+                B.fused.push_back((int32_t)i);
+                while (B.fused_n2 < w) B.fused_n2 <<= 1;
+            } else if (use_sorted && w >= sorted_min_w_) {
+                B.sorted.push_back((int32_t)i);
+                B.soff.push_back(B.spts + kScanB);  // kScanB sentinel entries on either side of the window's region
+                B.spts += w + 2 * kScanB;
+                B.n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
+                if (w > kSortedMaxW) B.n_mblocks += (w + kMergePts - 1) / kMergePts;
+                int n2 = 1;
+                while (n2 < std::min(w, kSortedMaxW)) n2 <<= 1;
+                B.W2 = std::max(B.W2, n2);
+            } else {
+                const int tr = tile_R(w);
+                B.tile[tr == 2 ? 0 : 1].push_back((int32_t)i);
+                B.n_items += (w + kTileThreads * tr - 1) / (kTileThreads * tr);
+            }
         }
+    });
+    // one chunk (every round below 2^18 windows): the lists move over (swap, no copy); else concatenate
+    auto cat = [&](std::vector<int32_t>& dst, std::vector<int32_t>& src, bool first) {
+        if (first && n_chunks == 1) dst.swap(src);
+        else if (first) dst.assign(src.begin(), src.end());
+        else dst.insert(dst.end(), src.begin(), src.end());
+    };
+    for (int c = 0; c < n_chunks; ++c) {
+        ChunkBins& B = cbins_[c];
+        for (int s = 0; s < 4; ++s) cat(small[s], B.small[s], c == 0);
+        for (int s = 0; s < 2; ++s) cat(tile[s], B.tile[s], c == 0);
+        for (int e = 0; e < 3; ++e) cat(wsorted[e], B.wsorted[e], c == 0);
+        cat(fused, B.fused, c == 0);
+        cat(sorted, B.sorted, c == 0);
+        if (n_chunks == 1) soff.swap(B.soff);
+        else for (int64_t o : B.soff) soff.push_back(spts + o);
+        spts += B.spts;
+        n_segs += B.n_segs;
+        n_mblocks += B.n_mblocks;
+        n_items += B.n_items;
+        pp += B.pp;
+        W2 = std::max(W2, B.W2);
+        fused_n2 = std::max(fused_n2, B.fused_n2);
     }
     // latency mode: a class too sparse to fill the GPU runs a CTA per window (tile R = 1), where a warp
     // walking 32R points (brute force) or sorting and scanning them (warp-sorted) would set the latency
@@ -555,7 +616,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     const int64_t off_blks = align64(off_segb + (blks.empty() ? 0 : n_segs) * (int64_t)sizeof(KsgSegB));
     const int64_t total = align64(off_blks + (int64_t)blks.size() * (int64_t)sizeof(KsgBlk));
     std::memcpy(S.hstage + off_pairs, pairs, n_pairs * sizeof(PairPtrs));
-    std::memcpy(S.hstage + off_wins, wins, n * sizeof(KsgWin));
+    par([&](int, int64_t i0, int64_t i1) {  // large batches: the copy into pinned memory on several threads
+        std::memcpy(S.hstage + off_wins + i0 * (int64_t)sizeof(KsgWin), wins + i0, (i1 - i0) * sizeof(KsgWin));
+    });
     int64_t list_off[4], wlist_off[3];
     {
         int32_t* lp = reinterpret_cast<int32_t*>(S.hstage + off_lists);

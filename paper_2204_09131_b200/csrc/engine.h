@@ -98,8 +98,10 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
 constexpr int kSmallWarps = 8;           // warps per CTA of the small kernel
 constexpr int kTileThreads = 256;        // threads per CTA of the tile kernel
 constexpr int kTileJ = 4096;             // j-tile (points) staged per cp.async.bulk round
-int small_class_R(int w);                // 1,2,4,8 for w <= 256; 0 => tile kernel
-int tile_R(int w);                       // points per thread of the tile kernel
+inline int small_class_R(int w) {        // 1,2,4,8 for w <= 256; 0 => tile kernel
+    return w <= 32 ? 1 : w <= 64 ? 2 : w <= 128 ? 4 : w <= 256 ? 8 : 0;
+}
+inline int tile_R(int w) { return w <= 2 * kTileThreads ? 2 : 4; }  // points per thread of the tile kernel
 constexpr int kSortedPts = 1024;         // max points per CTA of the sorted-path scan kernel (4 warps)
 constexpr int kSortedMaxW = 8192;        // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
 constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
@@ -268,6 +270,13 @@ private:
         std::vector<KsgInc> incs;
         std::vector<int64_t> wboff;
     } bins_;
+    struct ChunkBins {               // one host thread's share of a large batch's binning (merged in order)
+        std::vector<int32_t> small[4], tile[2], sorted, fused, wsorted[3];
+        std::vector<int64_t> soff;   // relative to the chunk's own sorted-point count
+        int64_t spts = 0, n_segs = 0, n_mblocks = 0, n_items = 0, pp = 0;
+        int W2 = 0, fused_n2 = 256;
+    };
+    std::vector<ChunkBins> cbins_;
     bool inc_on_ = false;            // NEXT-3 incremental radii along grid chains (ISYCOS_INCREMENTAL=1 or
                                      // ISYCOS_F_INCREMENTAL enables; measured time-neutral, so off by default)
     int32_t inc_chain_ = kIncChain;  // chain length (ISYCOS_INC_CHAIN)

@@ -7,15 +7,6 @@
 
 namespace isy {
 
-int small_class_R(int w) {
-    if (w <= 32) return 1;
-    if (w <= 64) return 2;
-    if (w <= 128) return 4;
-    if (w <= 256) return 8;
-    return 0;
-}
-
-int tile_R(int w) { return w <= 2 * kTileThreads ? 2 : 4; }
 
 namespace {
 // ------------------------------------------------------------------ digamma tables, input validation
