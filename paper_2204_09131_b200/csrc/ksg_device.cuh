@@ -691,6 +691,25 @@ __device__ __forceinline__ void topk_merge8(float (&r)[K], float (&d)[8]) {
     }
 }
 
+// a (sorted ascending, K entries) <- the K smallest of a U b, b sorted ascending (K entries): the bitonic
+// half-cleaner min(a[i], b[K-1-i]) keeps exactly the K smallest as a bitonic sequence, a bitonic merger sorts it
+// (K = 4: 12 FMNMX, K = 8: 32); other K insert b's entries one by one.
+template <int K>
+__device__ __forceinline__ void topk_merge_sorted(float (&a)[K], const float (&b)[K]) {
+    if constexpr (K == 4 || K == 8) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) a[i] = fminf(a[i], b[K - 1 - i]);
+#pragma unroll
+        for (int h = K / 2; h >= 1; h >>= 1)
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if ((i & h) == 0) cswap(a[i], a[i + h]);
+    } else {
+#pragma unroll
+        for (int m = 0; m < K; ++m) topk_insert<K>(a, b[m]);
+    }
+}
+
 // Phase A of the sorted path for the points [wb, we) (positions relative to cta0) of one warp: exact
 // k-NN radius by outward scan in x order (a3).  Writes eps_s[ml]; adds the candidate visits to `steps`.
 // P2 must carry sentinels: P2[-kScanB..-1] = (-inf, 0), P2[w..w+kScanB-1] = (+inf, 0) (no bounds checks).

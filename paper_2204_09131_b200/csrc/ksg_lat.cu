@@ -3,9 +3,9 @@
 // The search rounds of a BU climb carry a few hundred small windows; one thread walking all w candidates
 // of its point sets the round's latency.  Here every point is owned by kLatP = 8 lanes of a warp: lane s
 // scans the candidate groups g = s, s + 8, ... (4 candidates per float4 group) with its own register
-// top-(k+1) list, the 8 lists are merged by a 3-step butterfly (each lane inserts its partner's k+1
-// entries: after the xor-1/2/4 exchanges every lane holds the (k+1) smallest of the union — the same
-// multiset order statistic as one lane scanning everything), then the marginal counts are split the same
+// top-(k+1) list, the 8 lists (self's 0 removed: k entries each) are merged by a 3-step butterfly (bitonic
+// merge networks for k = 4, 8: after the xor-1/2/4 exchanges every lane holds the k smallest of the union over
+// j != i — the same multiset order statistic as one lane scanning everything), then the marginal counts are split the same
 // way and summed by shuffles.  The critical path per window drops ~8x; results are bit-identical.
 #include "ksg_device.cuh"
 
@@ -50,16 +50,24 @@ __global__ void __launch_bounds__(kLatThreads)
     const float4* sx4 = reinterpret_cast<const float4*>(sx);
     const float4* sy4 = reinterpret_cast<const float4*>(sy);
     for (int g = s; g < ng; g += kLatP) knn_step<K1, 1, false>(xi, yi, rk, sx4[g], sy4[g]);
+    // Drop self before merging: the lane that scanned j = i (group i/4 -> lane (i/4) mod 8) holds the K1 smallest
+    // of its candidates including d_ii = 0 at the front; removing that one 0 leaves the K = k smallest of the
+    // others.  Every other lane keeps its first K.  The merged K-lists then give eps = the k-th smallest over
+    // j != i = the (k+1)-th of the multiset with self, and K = 4 / 8 merge by bitonic networks.
+    constexpr int K = K1 - 1;
+    const bool self_lane = s == ((i >> 2) & (kLatP - 1));
+    float rl[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) rl[m] = self_lane ? rk[0][m + 1] : rk[0][m];
     // butterfly merge of the 8 partial top lists (lanes of one point are 8 consecutive lanes)
 #pragma unroll
     for (int off = 1; off < kLatP; off <<= 1) {
-        float other[K1];
+        float other[K];
 #pragma unroll
-        for (int m = 0; m < K1; ++m) other[m] = __shfl_xor_sync(0xffffffffu, rk[0][m], off);
-#pragma unroll
-        for (int m = 0; m < K1; ++m) topk_insert<K1>(rk[0], other[m]);
+        for (int m = 0; m < K; ++m) other[m] = __shfl_xor_sync(0xffffffffu, rl[m], off);
+        topk_merge_sorted<K>(rl, other);
     }
-    float eps[1] = {rk[0][K1 - 1]};
+    float eps[1] = {rl[K - 1]};
     unsigned cx[1] = {0u}, cy[1] = {0u};
     for (int g = s; g < ng; g += kLatP) count_step<1>(xi, yi, eps, eps, cx, cy, sx4[g], sy4[g], (unsigned)L.two);
 #pragma unroll

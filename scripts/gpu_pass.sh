@@ -12,9 +12,11 @@ timeout 300 python __graft_entry__.py --smoke > $O/${TAG}_smoke.log 2>&1; echo "
 timeout 1500 python -m pytest tests -m gpu -q > $O/${TAG}_gpu_tests.log 2>&1; echo "gpu tests rc=$?"; tail -2 $O/${TAG}_gpu_tests.log
 timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > $O/${TAG}_bench_ref.json 2> $O/${TAG}_bench_ref.err; echo "ref rc=$?"
-timeout 1500 ncu --nvtx --nvtx-include "timed_step/" --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv \
-  --log-file /tmp/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --no-side --no-cpu-baseline > $O/${TAG}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-python scripts/ncu_summary.py launches /tmp/${TAG}_launches.csv $O/${TAG}_launches_bench.md
+# launch list of a quarter of the bench step (16 of its 64 pairs, same search; a whole step under ncu exceeds the
+# time limit): per-kernel shares of the configs[3] search
+timeout 1500 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --csv \
+  --log-file /tmp/${TAG}_launches.csv python scripts/measure_full.py cfg4 --pairs 16 > $O/${TAG}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+python scripts/ncu_summary.py launches /tmp/${TAG}_launches.csv $O/${TAG}_launches_cfg4_16pairs.md
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sorted_knn|sort_window|block_sort" -c 3 \
   -o /tmp/${TAG}_sweep4096 python scripts/kernel_bench.py --only 4096 --reps 1 --target 1e11 > $O/${TAG}_ncu_sweep.log 2>&1; echo "ncu sweep rc=$?"
 python scripts/ncu_summary.py rep /tmp/${TAG}_sweep4096.ncu-rep $O/${TAG}_ncu_sweep4096.md
@@ -22,6 +24,7 @@ cp /tmp/${TAG}_sweep4096.ncu-rep $O/ 2>/dev/null
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"warp_sorted|sorted_knn|sort_window|fused_sorted|ksg_lat|ksg_small|ksg_tile|block_sort" \
   -s 3000 -c 8 -o /tmp/${TAG}_cfg4 python scripts/measure_full.py cfg4 --pairs 16 > $O/${TAG}_ncu_cfg4.log 2>&1; echo "ncu cfg4 rc=$?"
 python scripts/ncu_summary.py rep /tmp/${TAG}_cfg4.ncu-rep $O/${TAG}_ncu_cfg4.md
+cp /tmp/${TAG}_cfg4.ncu-rep $O/ 2>/dev/null
 cp profiles/issue.json profiles/traffic.json $O/ 2>/dev/null
 python scripts/ncu_summary.py issue /tmp/${TAG}_sweep4096.ncu-rep sorted_throughput "sorted_knn|sort_window|block_sort" $O/issue.json
 python scripts/ncu_summary.py issue /tmp/${TAG}_cfg4.ncu-rep sorted_marginal "warp_sorted|sorted_knn|sort_window|fused_sorted|block_sort" $O/issue.json

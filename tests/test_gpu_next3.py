@@ -117,6 +117,31 @@ def test_latency_split_kernel_small_windows(isy, orc):
         assert np.array_equal(np.asarray(g2[f]), r2[f]), f
 
 
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_latency_split_kernel_merge_networks(isy, orc, k):
+    """ksg_lat: self's 0 is dropped from the lane that scanned it and the 8 partial k-lists merge by bitonic
+    networks (k = 4, 8) or insertions (other k).  Per-point outputs bitwise equal the oracle with integer ties and
+    duplicated points, where the dropped 0 competes with other zero distances."""
+    st = datagen.Stream(11, 5)
+    n = 6000
+    xs = {"int": (np.floor(st.uniform(n) * 5).astype(np.float32), np.floor(st.uniform(n) * 5).astype(np.float32)),
+          "dup": (np.repeat(datagen.f32(st.normal(n // 3)), 3)[:n], np.repeat(datagen.f32(st.normal(n // 3)), 3)[:n]),
+          "gauss": (datagen.f32(st.normal(n)), datagen.f32(st.normal(n)))}
+    sizes = [w for w in (k + 1, 9, 16, 31, 33, 64, 100, 128, 200, 256) if w > k]
+    W = np.array([(170 * i, 170 * i + w) for i, w in enumerate(sizes * 3)], np.int64)
+    for name, (x, y) in xs.items():
+        got = isy.isycos_mi_batch_ex(x, y, W, k, debug=True)
+        ref = orc.mi_batch(x, y, W, k)
+        for f in FIELDS:
+            assert np.array_equal(np.asarray(got[f]), ref[f]), (name, f)
+        off = 0
+        for a, b in W:
+            o = orc.window(x[a:b], y[a:b], k=k)
+            for f, r in (("eps", o.eps), ("nx", o.nx), ("ny", o.ny)):
+                assert np.array_equal(got[f][off:off + b - a], r), (name, f, a, b)
+            off += b - a
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_incremental_radii_chains(isy, orc, variant):
     """NEXT-3 incremental radii (IR): windows that follow their predecessor by one 512-block (w = 4,096
