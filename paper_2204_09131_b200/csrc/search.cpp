@@ -762,6 +762,75 @@ private:
     int total_ = 0;
 };
 
+// Asynchronous submit (ISYCOS_ASYNC_SUBMIT, default on): one thread runs Engine::submit (binning, packing,
+// launches) for the batches the main thread posts, in posting order, so a group's submit overlaps the other
+// group's advance.  collect of a slot first waits for that slot's submit.  Results never depend on it.
+class Submitter {
+public:
+    struct Job {
+        int g = 0;
+        std::vector<PairPtrs> table;
+        const KsgWin* wins = nullptr;
+        int64_t n = 0;
+        int32_t k = 0, variant = 0;
+        cudaStream_t st = nullptr;
+        uint32_t flags = 0;
+    };
+    explicit Submitter(Engine* e) : eng_(e), th_([this] { loop(); }) {}
+    ~Submitter() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    void post(Job&& j) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            pending_[j.g] = true;
+            q_.push_back(std::move(j));
+        }
+        cv_.notify_all();
+    }
+    Status wait(int g) {  // the status of slot g's last posted submit, once it has run
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !pending_[g]; });
+        return st_[g];
+    }
+    BatchStats bs;  // the submit thread's share of the batch statistics (h2d bytes), merged by the caller
+
+private:
+    void loop() {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (q_.empty()) return;  // stop requested and nothing queued
+                j = std::move(q_.front());
+                q_.pop_front();
+            }
+            Status s = eng_->submit(j.g, j.table.data(), (int32_t)j.table.size(), j.wins, j.n, j.k, j.variant,
+                                    DebugOut{}, j.st, j.flags, &bs);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                st_[j.g] = s;
+                pending_[j.g] = false;
+            }
+            cv_.notify_all();
+        }
+    }
+    Engine* eng_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Job> q_;
+    bool pending_[2] = {false, false};
+    Status st_[2];
+    bool stop_ = false;
+    std::thread th_;  // last: starts after the members it reads are constructed
+};
+
 }  // namespace
 
 // ------------------------------------------------------------------ chunks + merge
@@ -994,8 +1063,8 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     }
     // the round's batch: grown, never re-initialised (a value-initialising resize of a 10^7-window TD round
     // costs more host time than the copy itself)
-    std::unique_ptr<KsgWin[]> batch;
-    int64_t batch_cap = 0, batch_n = 0;
+    std::unique_ptr<KsgWin[]> batches[2];  // one per group: an asynchronous submit may still read the other
+    int64_t batch_caps[2] = {0, 0}, batch_n = 0;
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
     auto t_last = t_start;
@@ -1022,16 +1091,24 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         int64_t n = 0;              // windows in flight (owners[0..n))
     };
     Flight fl[2];
+    bool async_submit = P.pipeline;
+    if (const char* a = std::getenv("ISYCOS_ASYNC_SUBMIT")) async_submit = async_submit && std::atoi(a) != 0;
+    std::unique_ptr<Submitter> submitter;
+    if (async_submit) submitter = std::make_unique<Submitter>(eng);
     // error exits leave no batch in flight: the slot's staging buffer and mapped records would otherwise be
-    // reused by the next call while the old copies and kernels still run
+    // reused by the next call while the old copies and kernels still run (queued submits run first)
     struct Drain {
         Engine* eng;
         Flight* fl;
+        std::unique_ptr<Submitter>* sub;
         ~Drain() {
             for (int g = 0; g < 2; ++g)
+                if (*sub) (*sub)->wait(g);
+            for (int g = 0; g < 2; ++g)
                 if (fl[g].busy) eng->collect(g, nullptr, nullptr);
+            sub->reset();
         }
-    } drain{eng, fl};
+    } drain{eng, fl, &submitter};
     const int n_groups = P.pipeline ? 2 : 1;
     cudaStream_t sts[2] = {st, eng->second_stream()};
     if (n_groups == 2) {  // the second slot's stream starts after everything already queued on st
@@ -1044,6 +1121,13 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
         const KsgRec* recs = nullptr;
         const auto t_ev = clk::now();
         bool profiled = false;
+        if (submitter) {
+            Status ss = submitter->wait(g);
+            if (!ss.ok()) {
+                F.busy = false;  // the slot never launched (or its submit failed part-way: the Drain syncs it)
+                return ss;
+            }
+        }
         Status s = eng->collect_view(g, &recs, &bs, false, &profiled);
         const double wms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
         eval_ms += wms;
@@ -1239,9 +1323,10 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 F.pws.push_back(pw.get());
             }
             // each pair copies its staged requests to its slice of the batch (in parallel when large)
-            if (batch_cap < tot) {
-                batch_cap = std::max<int64_t>(tot, batch_cap * 2);
-                batch.reset(new KsgWin[batch_cap]);
+            auto& batch = batches[g];
+            if (batch_caps[g] < tot) {
+                batch_caps[g] = std::max<int64_t>(tot, batch_caps[g] * 2);
+                batch.reset(new KsgWin[batch_caps[g]]);
             }
             batch_n = tot;
             if ((int64_t)F.owners.size() < tot) F.owners.resize(std::max<int64_t>(tot, 2 * (int64_t)F.owners.size()));
@@ -1271,11 +1356,24 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             uint32_t fl_round = P.flags;
             if ((fl_round & ISYCOS_F_PROFILE) && P.profile_every > 1 && (round_no % P.profile_every) != 0)
                 fl_round &= ~ISYCOS_F_PROFILE;
-            Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.get(), batch_n, P.k,
-                                   P.variant, DebugOut{}, sts[g], fl_round, &bs);
+            if (submitter) {
+                Submitter::Job j;
+                j.g = g;
+                j.table = std::move(table);
+                j.wins = batch.get();
+                j.n = batch_n;
+                j.k = P.k;
+                j.variant = P.variant;
+                j.st = sts[g];
+                j.flags = fl_round;
+                submitter->post(std::move(j));
+            } else {
+                Status s = eng->submit(g, table.data(), (int32_t)table.size(), batch.get(), batch_n, P.k,
+                                       P.variant, DebugOut{}, sts[g], fl_round, &bs);
+                if (!s.ok()) return s;
+            }
             const double ev_ms = std::chrono::duration<double, std::milli>(clk::now() - t_ev).count();
             eval_ms += ev_ms;
-            if (!s.ok()) return s;
             F.busy = true;
             progress = true;
             if (trace) {  // per-round trace (ISYCOS_TRACE=<path>): round, host ms since last submit, submit ms, batch
@@ -1335,6 +1433,7 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
             stats->auto_nscore_bu += A.nscore_bu;
         }
         const double wall = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+        if (submitter) bs.h2d_bytes += submitter->bs.h2d_bytes;  // every posted submit has run (all delivered)
         bs.wall_ms = wall;
         bs.host_ms = wall - eval_ms;
         bs.add_to(&stats->kernel);

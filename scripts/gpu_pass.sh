@@ -20,11 +20,12 @@ python scripts/ncu_summary.py launches /tmp/${TAG}_launches.csv $O/${TAG}_launch
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sorted_knn|sort_window|block_sort" -c 3 \
   -o /tmp/${TAG}_sweep4096 python scripts/kernel_bench.py --only 4096 --reps 1 --target 1e11 > $O/${TAG}_ncu_sweep.log 2>&1; echo "ncu sweep rc=$?"
 python scripts/ncu_summary.py rep /tmp/${TAG}_sweep4096.ncu-rep $O/${TAG}_ncu_sweep4096.md
-cp /tmp/${TAG}_sweep4096.ncu-rep $O/ 2>/dev/null
+# opcode mix of the scan kernel (the .ncu-rep files stay on the box: gpurun copies back <= 64 MiB)
+python scripts/ncu_summary.py opcodes /tmp/${TAG}_sweep4096.ncu-rep sorted_knn $O/${TAG}_sorted_knn_opcodes.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"warp_sorted|sorted_knn|sort_window|fused_sorted|ksg_lat|ksg_small|ksg_tile|block_sort" \
   -s 3000 -c 8 -o /tmp/${TAG}_cfg4 python scripts/measure_full.py cfg4 --pairs 16 > $O/${TAG}_ncu_cfg4.log 2>&1; echo "ncu cfg4 rc=$?"
 python scripts/ncu_summary.py rep /tmp/${TAG}_cfg4.ncu-rep $O/${TAG}_ncu_cfg4.md
-cp /tmp/${TAG}_cfg4.ncu-rep $O/ 2>/dev/null
+python scripts/ncu_summary.py opcodes /tmp/${TAG}_cfg4.ncu-rep warp_sorted $O/${TAG}_warp_sorted_opcodes.txt
 cp profiles/issue.json profiles/traffic.json $O/ 2>/dev/null
 python scripts/ncu_summary.py issue /tmp/${TAG}_sweep4096.ncu-rep sorted_throughput "sorted_knn|sort_window|block_sort" $O/issue.json
 python scripts/ncu_summary.py issue /tmp/${TAG}_cfg4.ncu-rep sorted_marginal "warp_sorted|sorted_knn|sort_window|fused_sorted|block_sort" $O/issue.json

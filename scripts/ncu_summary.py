@@ -7,6 +7,7 @@
 import collections
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -211,5 +212,39 @@ def issue(path, key, name_re=".*", dst="profiles/issue.json"):
     print(key, out)
 
 
+def opcodes(path, name_re, dst):
+    """Executed warp instructions per SASS opcode (summed over the matching launches of a --set full capture),
+    with the average active lanes and the share of warp-stall samples, from ncu's source page."""
+    rows = ncu_csv(["-i", path, "--page", "source", "--kernel-name", f"regex:{name_re}", "--print-source", "sass"])
+    ops, thr, st = collections.Counter(), collections.Counter(), collections.Counter()
+    hdr = None
+    for r in rows:
+        if "Source" in r and "Instructions Executed" in r:
+            hdr = r
+            i_src, i_ie = r.index("Source"), r.index("Instructions Executed")
+            i_te, i_s = r.index("Thread Instructions Executed"), r.index("Warp Stall Sampling (All Samples)")
+            continue
+        if hdr is None or len(r) <= max(i_src, i_ie, i_te, i_s):
+            continue
+        try:
+            ie, te, sm = int(r[i_ie]), int(r[i_te]), int(r[i_s])
+        except ValueError:
+            continue
+        t = r[i_src].split()
+        op = (t[1] if t and t[0].startswith("@") and len(t) > 1 else (t[0] if t else "?")).split(".")[0]
+        ops[op] += ie
+        thr[op] += te
+        st[op] += sm
+    tot, tt, ts = sum(ops.values()), sum(thr.values()), max(1, sum(st.values()))
+    with open(dst, "w") as f:
+        f.write(f"# {name_re} in {os.path.basename(path)}: executed warp instructions by SASS opcode\n")
+        if not tot:
+            f.write("no launches matched\n")
+            return
+        f.write(f"warp instructions {tot}  thread instructions {tt}  average lanes {tt / tot:.1f}\n")
+        for op, c in ops.most_common(30):
+            f.write(f"{op:10s} {c / tot * 100:5.1f}%  lanes {thr[op] / c:5.1f}  stall share {st[op] / ts * 100:5.1f}%\n")
+
+
 if __name__ == "__main__":
-    {"rep": rep, "launches": launches, "traffic": traffic, "issue": issue}[sys.argv[1]](*sys.argv[2:])
+    {"rep": rep, "launches": launches, "traffic": traffic, "issue": issue, "opcodes": opcodes}[sys.argv[1]](*sys.argv[2:])
