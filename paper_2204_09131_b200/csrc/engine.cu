@@ -133,6 +133,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_SORTED")) sorted_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
+    if (const char* m = std::getenv("ISYCOS_LAT_KEEP_SMALL_R")) lat_keep_small_R_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_SORTED_PPC"))
@@ -426,7 +427,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         v.clear();
     };
     for (int s = 0; s < 4; ++s)
-        if (!small[s].empty() && (int64_t)small[s].size() < lat_windows_) to_latency(small[s]);
+        if (!small[s].empty() && (1 << s) > lat_keep_small_R_ && (int64_t)small[s].size() < lat_windows_)
+            to_latency(small[s]);
     for (int e = 0; e < 3; ++e)
         if (!wsorted[e].empty() && (int64_t)wsorted[e].size() < lat_windows_) to_latency(wsorted[e]);
     // NEXT-3 block plan (the GPU analogue of the paper's incremental MI): sorted-path windows of one

@@ -293,6 +293,7 @@ private:
     int32_t sorted_ppc_ = kSortedPts;  // throughput scan: points per CTA
     int32_t fused_small_min_w_ = 1 << 30;  // latency mode: small windows >= this go to the fused kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
+    int32_t lat_keep_small_R_ = 0;   // brute small classes with R <= this stay warp-per-window even when sparse
 };
 
 // ---------------------------------------------------------------- search driver
