@@ -134,6 +134,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_SORTED_MIN_W")) sorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_LAT_KEEP_SMALL_R")) lat_keep_small_R_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_LAT_TINY_MAX_W")) lat_tiny_max_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_SORTED_PPC"))
@@ -406,7 +407,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // (all of a round's latency-mode windows go into one launch: per-class launches measured slower)
     // (windows >= fused_small_min_w_ take the fused sort+scan kernel when the round is in latency mode)
     auto& lat = bins_.lat;
+    auto& lat_tiny = bins_.lat_tiny;  // w <= lat_tiny_max_w_: a warp per window inside the latency launch
     lat.clear();
+    lat_tiny.clear();
     const int lat_pts = lat_points_per_cta();
     auto to_latency = [&](std::vector<int32_t>& v) {
         for (int32_t q : v) {
@@ -414,6 +417,10 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             if (fuse && w >= fused_small_min_w_) {
                 fused.push_back(q);
                 while (fused_n2 < w) fused_n2 <<= 1;
+                continue;
+            }
+            if (lat_split_on_ && variant == 0 && w <= lat_tiny_max_w_ && w <= 32) {  // warp per window (KSG-1)
+                lat_tiny.push_back(q);
                 continue;
             }
             if (lat_split_on_ && variant == 0 && w <= 256) {  // 8 lanes per point (KSG-1)
@@ -572,7 +579,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         const int fp = fused_ppc(wins[q].w, gmax);
         n_fitems += (wins[q].w + fp - 1) / fp;
     }
-    int64_t n_lists = (int64_t)sorted.size() + (int64_t)fused.size();
+    int64_t n_lists = (int64_t)sorted.size() + (int64_t)fused.size() + (int64_t)lat_tiny.size();
     for (auto& v : small) n_lists += (int64_t)v.size();
     int64_t n_wlist = 0;
     for (auto& v : wsorted) n_wlist += (int64_t)v.size();
@@ -621,7 +628,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     par([&](int, int64_t i0, int64_t i1) {  // large batches: the copy into pinned memory on several threads
         std::memcpy(S.hstage + off_wins + i0 * (int64_t)sizeof(KsgWin), wins + i0, (i1 - i0) * sizeof(KsgWin));
     });
-    int64_t list_off[4], wlist_off[3];
+    int64_t list_off[5], wlist_off[3];
     {
         int32_t* lp = reinterpret_cast<int32_t*>(S.hstage + off_lists);
         int64_t c = 0;
@@ -630,6 +637,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             std::memcpy(lp + c, small[s].data(), small[s].size() * 4);
             c += (int64_t)small[s].size();
         }
+        list_off[4] = c;  // the latency launch's tiny windows
+        std::memcpy(lp + c, lat_tiny.data(), lat_tiny.size() * 4);
         int32_t* wl = reinterpret_cast<int32_t*>(S.hstage + off_wlist);
         int64_t cw = 0;
         for (int e = 0; e < 3; ++e) {
@@ -745,6 +754,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     for (int s = 0; s < 3; ++s)
         for (int32_t q : tile[s]) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
     for (int32_t q : lat) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
+    for (int32_t q : lat_tiny) brute_pairs += (int64_t)wins[q].w * (wins[q].w - 1);
     for (int32_t q : fused) {
         int lg = 0;
         while ((1 << lg) < wins[q].w) ++lg;
@@ -862,9 +872,12 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         });
         if (!r.ok()) return r;
     }
-    if (!lat.empty()) {
+    if (!lat.empty() || !lat_tiny.empty()) {
         const KsgItem* ip = ditems + item_off_lat;
-        Status r = launch(1, 1, [&](cudaStream_t sg) { return launch_ksg_lat(L, ip, (int32_t)n_litems, sg); });
+        const int32_t* tp = dlists + list_off[4];
+        Status r = launch(1, 1, [&](cudaStream_t sg) {
+            return launch_ksg_lat(L, ip, (int32_t)n_litems, tp, (int32_t)lat_tiny.size(), sg);
+        });
         if (!r.ok()) return r;
     }
     for (int s : {1, 0, 2}) {

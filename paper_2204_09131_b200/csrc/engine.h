@@ -113,7 +113,8 @@ constexpr int kFusedThreads = 512;       // threads per fused CTA (16 warps: one
 cudaError_t launch_ksg_small(const KsgLaunch& L, const int32_t* list, int32_t n, int R, cudaStream_t st);
 cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_items, int R, cudaStream_t st);
 // latency mode, KSG-1, w <= 256: 8 lanes per point (ksg_lat.cu); items {window, first point}, 32 points each
-cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, cudaStream_t st);
+cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, const int32_t* tiny,
+                           int32_t n_tiny, cudaStream_t st);
 int lat_points_per_cta();
 // sorted path: sort kernel over segments {list pos, start}, XL rank merge over blocks {list pos, start},
 // then the scan kernel over `items` {list pos, first point}
@@ -262,7 +263,7 @@ private:
     int* dflag_ = nullptr;
     Slot slots_[2];
     struct Bins {                    // size-class lists of the batch being packed (reused)
-        std::vector<int32_t> small[4], tile[3], sorted, fused, wsorted[3], lat;
+        std::vector<int32_t> small[4], tile[3], sorted, fused, wsorted[3], lat, lat_tiny;
         std::vector<int64_t> soff;
         std::vector<int32_t> ord, beta;      // NEXT-3 block plan scratch
         std::vector<KsgBlk> blks;
@@ -294,6 +295,7 @@ private:
     int32_t fused_small_min_w_ = 1 << 30;  // latency mode: small windows >= this go to the fused kernel
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
     int32_t lat_keep_small_R_ = 0;   // brute small classes with R <= this stay warp-per-window even when sparse
+    int32_t lat_tiny_max_w_ = 32;    // latency mode: windows up to this size run warp-per-window in the lat launch
 };
 
 // ---------------------------------------------------------------- search driver

@@ -289,6 +289,100 @@ __device__ __forceinline__ void warp_sum(long long& a, long long& b, int& c) {
     }
 }
 
+// One warp evaluates window q (w <= 32 R) alone: lane l owns points l + 32 r, all candidates from the warp's
+// shared-memory slice sx / sy (>= 32 R + 4 floats each).  Used by ksg_small_kernel (dense classes, 8 windows per
+// CTA) and by the latency kernel's tiny-window CTAs (one launch per round).
+template <int K1, int R, bool BL, bool V2>
+__device__ __forceinline__ void small_window_warp(const KsgLaunch& L, int q, float* sx, float* sy) {
+    const int lane = threadIdx.x & 31;
+    const KsgWin W = L.wins[q];
+    const int w = W.w;
+    const int wpad = (w + 3) & ~3;
+    const float* gx = L.pairs[W.pair].x + W.t0;
+    const float* gy = L.pairs[W.pair].y + W.t0;
+    for (int j = lane; j < wpad; j += 32) {  // a2: coalesced loads, +inf sentinels past w
+        sx[j] = j < w ? gx[j] : kInf;
+        sy[j] = j < w ? gy[j] : kInf;
+    }
+    __syncwarp();
+    float xi[R], yi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        xi[r] = i < w ? sx[i] : 0.0f;
+        yi[r] = i < w ? sy[i] : 0.0f;
+    }
+    float rk[R][K1];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < K1; ++m) rk[r][m] = kInf;
+    const float4* sx4 = reinterpret_cast<const float4*>(sx);
+    const float4* sy4 = reinterpret_cast<const float4*>(sy);
+    const int ng = wpad >> 2;
+    for (int g = 0; g < ng; ++g) knn_step<K1, R, BL>(xi, yi, rk, sx4[g], sy4[g]);
+    float eps[R], ex[R], ey[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) ex[r] = ey[r] = eps[r] = rk[r][K1 - 1];
+    if (V2) {  // KSG-2: d_x, d_y over kNN(i), one more pass in ascending j
+        int need[R], taken[R];
+        float mx[R], my[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            need[r] = ksg2_need<K1>(rk[r]);
+            taken[r] = 0;
+            mx[r] = my[r] = 0.0f;
+        }
+        for (int g = 0; g < ng; ++g) ksg2_step<R>(xi, yi, eps, need, taken, mx, my, sx4[g], sy4[g]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ex[r] = nextup(mx[r]);
+            ey[r] = nextup(my[r]);
+        }
+    }
+    unsigned cx[R], cy[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cx[r] = cy[r] = 0u;
+    if (L.knn_mode & 2) {
+        // a4, warp-ballot form (north star; SURVEY §8(a) a4 option 1, kept for the A/B): for each point i in
+        // turn (warp-uniform), lane l tests the candidates j = l + 32 c it holds in registers with the same
+        // predicate as acc_lt (sign bit of fl(|fl(x_i - x_j)| - e_i)); n(i) = sum of popc(ballot).  Measured
+        // slower than the per-lane form, so off by default (ISYCOS_KNN_MODE bit 1).
+        float xj[R], yj[R];
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            const int j = lane + 32 * c;
+            xj[c] = j < w ? sx[j] : kInf;  // +inf: never counted
+            yj[c] = j < w ? sy[j] : kInf;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            for (int l = 0; l < 32 && l + 32 * r < w; ++l) {  // warp-uniform bounds
+                const float xb = __shfl_sync(0xffffffffu, xi[r], l), yb = __shfl_sync(0xffffffffu, yi[r], l);
+                const float eb = __shfl_sync(0xffffffffu, ex[r], l), fb = __shfl_sync(0xffffffffu, ey[r], l);
+                unsigned nx = 0, ny = 0;
+#pragma unroll
+                for (int c = 0; c < R; ++c) {
+                    nx += __popc(__ballot_sync(0xffffffffu, (__float_as_uint(fabsf(xb - xj[c]) - eb) >> 31) != 0u));
+                    ny += __popc(__ballot_sync(0xffffffffu, (__float_as_uint(fabsf(yb - yj[c]) - fb) >> 31) != 0u));
+                }
+                if (lane == l) {
+                    cx[r] = nx;
+                    cy[r] = ny;
+                }
+            }
+        }
+    } else {
+        const unsigned two = (unsigned)L.two;
+        for (int g = 0; g < ng; ++g) count_step<R>(xi, yi, ex, ey, cx, cy, sx4[g], sy4[g], two);
+    }
+    long long sp = 0, sl = 0;
+    int z = 0;
+    point_terms<R, V2>(L, w, W.dbg_off, lane, 32, eps, cx, cy, sp, sl, z);
+    warp_sum(sp, sl, z);
+    if (lane == 0) finalize(L, w, sp, sl, z, &L.out[q]);
+}
+
 // ------------------------------------------------------------------ large windows: (window, i-tile) per CTA
 // a2 via cp.async.bulk of the 16-B aligned superset [a & ~3, ceil4(a + len)) into SMEM, completion on an
 // mbarrier; series buffers are 16-B aligned and padded to a multiple of 4 floats so the superset is in bounds.

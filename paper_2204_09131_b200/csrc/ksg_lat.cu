@@ -7,6 +7,7 @@
 // merge networks for k = 4, 8: after the xor-1/2/4 exchanges every lane holds the k smallest of the union over
 // j != i — the same multiset order statistic as one lane scanning everything), then the marginal counts are split the same
 // way and summed by shuffles.  The critical path per window drops ~8x; results are bit-identical.
+// Tiny windows (w <= 32) of the round ride in the same launch as extra CTAs, one warp per window.
 #include "ksg_device.cuh"
 
 namespace isy {
@@ -16,15 +17,28 @@ constexpr int kLatThreads = 256;
 constexpr int kLatP = 8;                              // lanes per point
 constexpr int kLatPts = kLatThreads / kLatP;          // points per CTA
 
+constexpr int kTinyCap = 36;                          // per-warp slice of a tiny window (w <= 32, +4 pad)
+
 template <int K1>
 __global__ void __launch_bounds__(kLatThreads)
-    ksg_lat_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items) {
-    __shared__ __align__(16) float sx[256];
-    __shared__ __align__(16) float sy[256];
+    ksg_lat_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items,
+                   const int32_t* __restrict__ tiny, int32_t n_tiny) {
+    __shared__ __align__(16) float sx[kSmallWarps * kTinyCap];  // >= 256
+    __shared__ __align__(16) float sy[kSmallWarps * kTinyCap];
     if (L.poison) {
         poison_smem(L, sx, sizeof(sx));
         poison_smem(L, sy, sizeof(sy));
         __syncthreads();
+    }
+    if ((int)blockIdx.x >= n_items) {
+        // tiny windows (w <= 32) of the same round: one warp per window, one point per lane (the small kernel's
+        // R = 1 body) — 8 lanes per point would leave most lanes idle and pay the list merge for a few candidates;
+        // sharing the launch keeps one latency-mode launch per round
+        const int warp = threadIdx.x >> 5;
+        const int idx = ((int)blockIdx.x - n_items) * kSmallWarps + warp;
+        if (idx >= n_tiny) return;  // warp-uniform; no block barrier on this path
+        small_window_warp<K1, 1, true, false>(L, tiny[idx], sx + warp * kTinyCap, sy + warp * kTinyCap);
+        return;
     }
     const KsgItem it = items[blockIdx.x];
     const int q = it.win;
@@ -82,8 +96,10 @@ __global__ void __launch_bounds__(kLatThreads)
 }
 
 template <int K1>
-cudaError_t lat_k(const KsgLaunch& L, const KsgItem* items, int32_t n, cudaStream_t st) {
-    ksg_lat_kernel<K1><<<n, kLatThreads, 0, st>>>(L, items, n);
+cudaError_t lat_k(const KsgLaunch& L, const KsgItem* items, int32_t n, const int32_t* tiny, int32_t n_tiny,
+                  cudaStream_t st) {
+    const int grid = n + (n_tiny + kSmallWarps - 1) / kSmallWarps;
+    ksg_lat_kernel<K1><<<grid, kLatThreads, 0, st>>>(L, items, n, tiny, n_tiny);
     return cudaGetLastError();
 }
 
@@ -91,10 +107,11 @@ cudaError_t lat_k(const KsgLaunch& L, const KsgItem* items, int32_t n, cudaStrea
 
 int lat_points_per_cta() { return kLatPts; }
 
-cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, cudaStream_t st) {
-    if (n_items <= 0) return cudaSuccess;
+cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, const int32_t* tiny,
+                           int32_t n_tiny, cudaStream_t st) {
+    if (n_items <= 0 && n_tiny <= 0) return cudaSuccess;
     if (L.variant != 0) return cudaErrorInvalidValue;  // KSG-2 latency windows take the tile kernel (R = 1)
-    ISY_K_CASES(lat_k, L, items, n_items, st)
+    ISY_K_CASES(lat_k, L, items, n_items, tiny, n_tiny, st)
 }
 
 }  // namespace isy

@@ -84,15 +84,48 @@ struct SmallMap {
 struct FlatMap {
     static constexpr int kShift = 8;  // shard = t0 >> 8
     static constexpr uint32_t kBlock = 4096;
+    static constexpr size_t kMaxBlocks = size_t(1) << 16;  // concurrent mode: block table never reallocates
     std::vector<SmallMap> shards;
     std::vector<std::unique_ptr<Entry[]>> blocks;
     uint32_t size = 0;
+    // Concurrent mode (one pair's climbs advanced on several host threads): a lock per shard guards its table,
+    // one lock the arena; shards and the block table are sized up front, so neither vector reallocates while
+    // another thread reads it.  Entries never move, so a returned Entry* stays valid without a lock.
+    std::unique_ptr<std::mutex[]> shard_mu;
+    std::mutex arena_mu;
 
+    void make_concurrent(int64_t n_samples) {
+        shards.resize((size_t)(n_samples >> kShift) + 2);
+        shard_mu.reset(new std::mutex[shards.size()]);
+        blocks.reserve(kMaxBlocks);
+    }
     Entry& at(uint32_t i) { return blocks[i / kBlock][i % kBlock]; }
     const Entry& at(uint32_t i) const { return blocks[i / kBlock][i % kBlock]; }
     std::pair<Entry*, bool> try_emplace(uint64_t k) {
         const size_t sh = (size_t)(key_t0(k) >> kShift);
+        if (shard_mu) {
+            std::lock_guard<std::mutex> lk(shard_mu[sh]);
+            return emplace_in(sh, k);
+        }
         if (sh >= shards.size()) shards.resize(sh + 1);
+        return emplace_in(sh, k);
+    }
+    Entry* find(uint64_t k) {
+        const size_t sh = (size_t)(key_t0(k) >> kShift);
+        if (sh >= shards.size()) return nullptr;
+        if (shard_mu) {
+            std::lock_guard<std::mutex> lk(shard_mu[sh]);
+            return find_in(sh, k);
+        }
+        return find_in(sh, k);
+    }
+    template <typename F>
+    void for_each(F&& f) const {
+        for (uint32_t i = 0; i < size; ++i) f(at(i));
+    }
+
+private:
+    std::pair<Entry*, bool> emplace_in(size_t sh, uint64_t k) {
         SmallMap& m = shards[sh];
         if ((m.count + 1) * 2 > m.tab.size()) m.grow();
         uint32_t i = SmallMap::hash(k) & m.mask;
@@ -100,17 +133,25 @@ struct FlatMap {
             if (m.tab[i].key == k) return {&at(m.tab[i].idx), false};
             i = (i + 1) & m.mask;
         }
-        if (size % kBlock == 0) blocks.emplace_back(new Entry[kBlock]);
-        const uint32_t idx = size++;
+        uint32_t idx;
+        if (shard_mu) {
+            std::lock_guard<std::mutex> lk(arena_mu);
+            if (size % kBlock == 0) {
+                if (blocks.size() == kMaxBlocks) std::abort();  // 2^28 entries of one pair: never reached
+                blocks.emplace_back(new Entry[kBlock]);
+            }
+            idx = size++;
+        } else {
+            if (size % kBlock == 0) blocks.emplace_back(new Entry[kBlock]);
+            idx = size++;
+        }
         m.tab[i] = SmallMap::Slot{k, idx};
         ++m.count;
         Entry& e = at(idx);
         e.key = k;
         return {&e, true};
     }
-    Entry* find(uint64_t k) {
-        const size_t sh = (size_t)(key_t0(k) >> kShift);
-        if (sh >= shards.size()) return nullptr;
+    Entry* find_in(size_t sh, uint64_t k) {
         SmallMap& m = shards[sh];
         if (m.tab.empty()) return nullptr;
         uint32_t i = SmallMap::hash(k) & m.mask;
@@ -120,15 +161,20 @@ struct FlatMap {
         }
         return nullptr;
     }
-    template <typename F>
-    void for_each(F&& f) const {
-        for (uint32_t i = 0; i < size; ++i) f(at(i));
-    }
 };
 
 struct PairCache {
     FlatMap map;
     std::vector<Entry*> pending;  // requested, not yet staged (entries never move)
+    std::mutex pending_mu;        // concurrent mode only
+    void add_pending(Entry* e) {
+        if (map.shard_mu) {
+            std::lock_guard<std::mutex> lk(pending_mu);
+            pending.push_back(e);
+        } else {
+            pending.push_back(e);
+        }
+    }
 };
 
 // t_w ~ w log w per MI request: Alg. 3's deterministic runtime proxy (DESIGN reading R24)
@@ -168,7 +214,7 @@ struct View {
         const uint64_t k = wkey(t0, t1);
         auto r = c->map.try_emplace(k);
         if (r.second) {
-            c->pending.push_back(r.first);
+            c->add_pending(r.first);
             return nullptr;
         }
         if (!r.first->ready) return nullptr;
@@ -178,7 +224,7 @@ struct View {
     void want(int64_t t0, int64_t t1) {
         const uint64_t k = wkey(t0, t1);
         auto r = c->map.try_emplace(k);
-        if (r.second) c->pending.push_back(r.first);
+        if (r.second) c->add_pending(r.first);
     }
     const Eval* peek(int64_t t0, int64_t t1) {  // no request, no consumption
         Entry* e = c->map.find(wkey(t0, t1));
@@ -637,11 +683,24 @@ struct BuJob {
     // chain alternate); advance(g) advances group g's climbs (g < 0: all) plus the chain bookkeeping.
     int group_of(int64_t l) const { return (int)((l / P->s_min) & 1); }
 
+    // set by the driver when this job's pair is the only one advancing (its cache is then in concurrent mode):
+    // the climbs of a group advance on the host pool (each climb touches only its own state and the cache)
+    std::function<void(int, const std::function<void(int)>&)> par_for;
+
     void advance(int g = -1) {
         if (done) return;
-        for (auto& kv : climbs)
-            if (g < 0 || group_of(kv.first) == g)
-                kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first), ring_for(kv.first));
+        if (par_for && cache->map.shard_mu) {
+            std::vector<std::pair<int64_t, Climb*>> cl;
+            for (auto& kv : climbs)
+                if (g < 0 || group_of(kv.first) == g) cl.push_back({kv.first, &kv.second});
+            par_for((int)cl.size(), [&](int i) {
+                cl[i].second->advance(*P, cache, pair_id, hi, cap_for(cl[i].first), ring_for(cl[i].first));
+            });
+        } else {
+            for (auto& kv : climbs)
+                if (g < 0 || group_of(kv.first) == g)
+                    kv.second.advance(*P, cache, pair_id, hi, cap_for(kv.first), ring_for(kv.first));
+        }
         ensure_lookahead();
         for (;;) {
             if (chain + P->s_min > hi) {
@@ -1035,7 +1094,12 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
     std::vector<AutoState> autos;
     int n_threads = P.host_threads;
     if (n_threads <= 0) n_threads = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
-    if (n_pairs <= 1 && P.method != 4) n_threads = 1;  // one pair: nothing to spread
+    // one pair: its BU climbs may spread over the pool instead (ISYCOS_PAR_CLIMBS=1; measured 2x slower on
+    // configs[1] — per-round dispatch and shard-lock traffic exceed the ~25 us of climb work per round — so off)
+    bool par_climbs = false;
+    if (const char* pc = std::getenv("ISYCOS_PAR_CLIMBS"))
+        par_climbs = std::atoi(pc) != 0 && n_pairs == 1 && P.method != 4 && (P.method & 2) && P.n_chunks <= 1;
+    if (n_pairs <= 1 && P.method != 4 && !par_climbs) n_threads = 1;  // one pair: nothing to spread
     HostPool pool(n_threads);
     Reaper reaper(P, chunk_sel);
     const int32_t aM = P.auto_M > 0 ? P.auto_M : 20, am = P.auto_m > 0 ? P.auto_m : 6;
@@ -1206,6 +1270,11 @@ Status run_search(Engine* eng, const std::vector<PairPtrs>& pair_ptrs, const std
                 for (auto& j : pw->td) {
                     j.cache = &pw->cache;
                     j.init();
+                }
+                if (par_climbs && pool.size() > 1) {
+                    pw->cache.map.make_concurrent(n);
+                    for (auto& j : pw->bu)
+                        j.par_for = [&pool](int cnt, const std::function<void(int)>& f) { pool.run(cnt, f); };
                 }
                 for (auto& j : pw->bu) {
                     j.cache = &pw->cache;

@@ -84,3 +84,16 @@ def test_auto_selection_multi_pair(hz, orc):
     pairs = [(a, b, 40 + i) for i, (a, b) in enumerate(wl.pairs)]
     res, st = check(hz, orc, wl, pairs=pairs, label="cfg4 auto", s_max=1024, method=4, auto_M=5, auto_m=2)
     assert st["auto_td"] + st["auto_bu"] == len(pairs)
+
+
+@pytest.mark.parametrize("method", [2, 3])
+def test_parallel_climbs_opt_in(hz, orc, method, monkeypatch):
+    """ISYCOS_PAR_CLIMBS=1: one pair's BU climbs advance on the host pool over a window cache in concurrent mode
+    (a lock per shard, one for the arena and the pending list).  Off by default (measured slower on configs[1]);
+    the results and counters must still equal the oracle's."""
+    monkeypatch.setenv("ISYCOS_PAR_CLIMBS", "1")
+    monkeypatch.setenv("ISYCOS_HOST_THREADS", "8")
+    for noise in (False, True):
+        check(hz, orc, datagen.cfg1(), method=method, noise=noise, label=f"par m{method} n{noise}")
+    wl = datagen.cfg2()
+    check(hz, orc, wl, series=[s[:12_000] for s in wl.series], method=method, label="par cfg2 prefix", s_max=2048)
