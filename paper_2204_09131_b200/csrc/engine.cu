@@ -135,6 +135,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_LAT_WINDOWS")) lat_windows_ = std::atoll(m);
     if (const char* m = std::getenv("ISYCOS_LAT_KEEP_SMALL_R")) lat_keep_small_R_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_TINY_MAX_W")) lat_tiny_max_w_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_COL_MIN_W")) col_min_w_ = std::max(kColW + 1, std::atoi(m));
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_SORTED_PPC"))
@@ -592,10 +593,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
                                        (int64_t)sorted.size() * (int64_t)sizeof(KsgInc) + 192);
         if (!s.ok()) return s;
     }
-    // scratch per sorted point: P2 (8) | OX (4) | YS (4) | TX (4) | TI (4) | TY (4)
-    // scratch per sorted point: P2 (8) | OX | YS | TX | TI | TY | EPS (4 each) | CNT (8); then the NEXT-3 block keys
+    // scratch per sorted point: P2 (8) | OX | YS | TX | TI | TY | EPS (4 each) | CNT (8) | CY (8); then the NEXT-3 block keys
     // BX (8) | BY (4)
-    const int64_t blk_base = (spts * 40 + 15) & ~int64_t(15);
+    const int64_t blk_base = (spts * 48 + 15) & ~int64_t(15);  // + CY (8): box-assisted columns
     const int64_t scratch_need = blk_base + blk_store * 12;
     if (spts > 0 && S.sscratch_cap < scratch_need) {
         const int64_t c = std::max<int64_t>(scratch_need, S.sscratch_cap * 2);
@@ -729,7 +729,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     L.fused_n2 = fused_n2;
     L.scan_unified = scan_unified_;
     L.poison = poison_;
-    L.pad4_ = 0;
+    L.col_min_w = col_min_w_;
     if (poison_) {  // every byte the kernels read must have been written in this batch
         const int pb = (int)(poison_ & 0xffu);
         if (S.sscratch) ISY_CK(cudaMemsetAsync(S.sscratch, pb, S.sscratch_cap, st));
@@ -851,6 +851,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         unsigned* BY = reinterpret_cast<unsigned*>(S.sscratch + blk_base + blk_store * 8);
         float* EPS = reinterpret_cast<float*>(S.sscratch + spts * 28);
         int2* CNT = reinterpret_cast<int2*>(S.sscratch + spts * 32);
+        float2* CY = reinterpret_cast<float2*>(S.sscratch + spts * 40);
+        bool cols = false;  // any window of the throughput batch on the box-assisted phase A
+        for (int32_t q : sorted) cols = cols || wins[q].w >= col_min_w_;
         const KsgInc* dinc = inc_windows ? reinterpret_cast<const KsgInc*>(dbase + off_inc) : nullptr;
         if (inc_windows) {  // work ticket + per-window finished-CTA counters, zeroed for this launch
             const int64_t need = 1 + (int64_t)sorted.size();
@@ -868,7 +871,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             }
             return launch_sorted(L, dsl, dso, dsg, (int32_t)n_segs, dmb, (int32_t)n_mblocks, P2, OX, YS, TX, TI, TY,
                                  W2, dsi, (int32_t)n_sitems, sg, dsb, dbk, (int32_t)blks.size(), blk_beta_max, BX, BY,
-                                 dinc, EPS, CNT, lv_off.data(), n_lv, inc_d_max, inc_windows ? S.sync : nullptr);
+                                 dinc, EPS, CNT, lv_off.data(), n_lv, inc_d_max, inc_windows ? S.sync : nullptr,
+                                 cols ? CY : nullptr);
         });
         if (!r.ok()) return r;
     }

@@ -91,7 +91,7 @@ struct KsgLaunch {           // arguments shared by every KSG kernel of a batch
     int32_t fused_n2;        // fused path: shared-memory layout stride (max next-pow2 window size of the batch)
     int32_t scan_unified;    // sorted-path phase A: 0 both sides per iteration (default), 1 one side per iteration
     uint32_t poison;         // T5 check (ISYCOS_POISON=<byte>): kernels fill their shared memory with this pattern first
-    int32_t pad4_;
+    int32_t col_min_w;       // throughput scan: windows this large search the k-NN by y-sorted columns (box-assisted)
 };
 
 // Size classes.  Small: one warp per window, R = points per lane.
@@ -104,6 +104,7 @@ inline int small_class_R(int w) {        // 1,2,4,8 for w <= 256; 0 => tile kern
 inline int tile_R(int w) { return w <= 2 * kTileThreads ? 2 : 4; }  // points per thread of the tile kernel
 constexpr int kSortedPts = 1024;         // max points per CTA of the sorted-path scan kernel (4 warps)
 constexpr int kSortedMaxW = 8192;        // sorted path: segment sorted in one CTA's SMEM (XL: runs + merge)
+constexpr int kColW = 32;                // box-assisted phase A: x-sorted positions per column (sorted by y)
 constexpr int kMergePts = 256;           // elements per CTA of the XL rank merge
 constexpr int kScanB = 8;                // sorted-path scan: candidates per block and side (= sentinels per end)
 constexpr int kFusedMaxW = 4096;         // fused sort+scan path (latency mode): windows up to this size
@@ -126,7 +127,7 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_items, cudaStream_t st, const KsgSegB* segb, const KsgBlk* blks,
                           int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY, const KsgInc* inc,
                           float* EPS, int2* CNT, const int32_t* lv_off, int n_lv, int inc_d_max,
-                          unsigned* sync);
+                          unsigned* sync, float2* CY);
 constexpr int kIncChain = 16;  // NEXT-3 incremental chains: a window scanned from scratch every this many
 constexpr int kIncMaxD = 1024; // NEXT-3 incremental chains: grid steps up to this (two blocks staged in SMEM)
 // small windows on the sorted path: one warp per window, E = 2, 4, 8 keys per lane (w <= 32 E)
@@ -296,6 +297,7 @@ private:
     int64_t lat_windows_ = 148 * 4;  // small classes with fewer windows run in latency mode (tile R=1)
     int32_t lat_keep_small_R_ = 0;   // brute small classes with R <= this stay warp-per-window even when sparse
     int32_t lat_tiny_max_w_ = 32;    // latency mode: windows up to this size run warp-per-window in the lat launch
+    int32_t col_min_w_ = 1 << 30;    // throughput scan: box-assisted phase A for windows >= this (ISYCOS_COL_MIN_W)
 };
 
 // ---------------------------------------------------------------- search driver

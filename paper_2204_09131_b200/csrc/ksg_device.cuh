@@ -944,6 +944,113 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
     }
 }
 
+// Phase A, box-assisted form (the paper's box-assisted k-NN, made exact): the window's x-sorted
+// positions form columns of kColW; CY holds each column's points (y, x) sorted by y.  A point first takes every
+// other point of its own column (in x order, blocks of 8 through the merge network, itself excluded), then visits
+// the other columns outward in order of their x-distance to it:
+//   * a column left of it whose largest x has fl(x_i - x) >= r (or right of it whose smallest x has
+//     fl(x - x_i) >= r) holds no point with d < r, nor does any column beyond it on that side: the side stops;
+//   * inside a column only the y-interval {j : |fl(y_i - y_j)| < r} can hold a point with d < r (the predicate is
+//     monotone on the y-sorted column, as in phase B): one binary search for its start, then a walk while
+//     fl(y_j - y_i) < r with the current (shrinking) r.
+// Every j with d_ij < eps lies in a visited column and inside that column's walked interval, so the top list ends
+// as the k smallest d over j != i — the same order statistic as the outward scan.  Stops for phase B: positions up
+// to the last position of the left stop column, and from the first of the right one, have |dx| >= r >= eps.
+template <int K1>
+__device__ __forceinline__ void sorted_phase_a_cols(const float2* P2, const float2* CY, int w, int cta0, int wb,
+                                                    int we, float* eps_s, unsigned long long& steps,
+                                                    int2* stop_s) {
+    constexpr int K = K1 - 1;
+    constexpr int C = kColW;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int kcur = wb + lane;
+    bool act = kcur < we;
+    int next = wb + 32;
+    float xi = 0.f, yi = 0.f;
+    int m = 0, cl = 0, cr = 0, blk = 0;  // own-column block still to visit (blk < C / 8), else columns
+    float rk[K];
+    auto start = [&](int ml) {
+        m = cta0 + ml;
+        const float2 me = P2[m];
+        xi = me.x;
+        yi = me.y;
+#pragma unroll
+        for (int t = 0; t < K; ++t) rk[t] = kInf;
+        const int col = m / C;
+        cl = col - 1;
+        cr = col + 1;
+        blk = 0;
+    };
+    if (act) start(kcur);
+    while (__any_sync(0xffffffffu, act)) {
+        bool fin = false;
+        if (act) {
+            if (blk < C / 8) {
+                // own column, one block of 8 in x order per iteration (itself and positions past w: +inf)
+                const int c0 = (m / C) * C + blk * 8;
+                float d[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int pj = c0 + u;
+                    const float2 c = pj < w ? P2[pj] : make_float2(kInf, 0.0f);
+                    const float dd = fmaxf(fabsf(xi - c.x), fabsf(yi - c.y));
+                    d[u] = (pj == m || pj >= w) ? kInf : dd;
+                }
+                float mn = d[0];
+#pragma unroll
+                for (int u = 1; u < 8; ++u) mn = fminf(mn, d[u]);
+                if (mn < rk[K - 1]) topk_merge8<K>(rk, d);
+                steps += (unsigned long long)max(0, min(8, w - c0) - ((m >= c0 && m < c0 + 8) ? 1 : 0));
+                ++blk;
+            } else {
+                const float r = rk[K - 1];
+                const float dl = cl >= 0 ? xi - P2[cl * C + C - 1].x : kInf;  // x-sorted: >= 0
+                const float dr = cr * C < w ? P2[cr * C].x - xi : kInf;
+                if (!(dl < r) && !(dr < r)) {
+                    fin = true;
+                } else {
+                    const int c = dl <= dr ? cl : cr;
+                    if (dl <= dr) --cl; else ++cr;
+                    const float2* col = CY + c * C;
+                    const int len = min(C, w - c * C);
+                    int lo = 0, n = len;  // first j with fl(y_i - y_j) < r (y ascending: false...true)
+                    while (n > 0) {
+                        const int h = n >> 1;
+                        if (!(yi - col[lo + h].x < r)) { lo += h + 1; n -= h + 1; } else n = h;
+                        ++steps;
+                    }
+                    for (int j = lo; j < len; ++j) {
+                        const float2 e = col[j];  // (y, x)
+                        if (!(e.x - yi < rk[K - 1])) break;
+                        ++steps;
+                        const float dd = fmaxf(fabsf(xi - e.y), fabsf(yi - e.x));
+                        if (dd < rk[K - 1]) topk_insert<K>(rk, dd);
+                    }
+                }
+            }
+            if (fin) {
+                eps_s[m - cta0] = rk[K - 1];
+                // phase B brackets: st.x + 2 = first position that may have |dx| < eps, st.y - 1 = one past the last
+                if (stop_s) stop_s[m - cta0] = make_int2(cl >= 0 ? cl * C + C - 2 : -2, cr * C < w ? cr * C + 1 : w + 1);
+            }
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, fin);
+        if (fm) {
+            if (fin) {
+                const int idx = next + __popc(fm & lt_mask);
+                if (idx < we) {
+                    kcur = idx;
+                    start(idx);
+                } else {
+                    act = false;
+                }
+            }
+            next += __popc(fm);
+        }
+    }
+}
+
 // Phase B for one point at sorted position m (a4, a5): interval counts by binary search with the
 // identical predicates, digamma / log terms, debug outputs.
 // [xlo, xhi] brackets the x-interval's ends (KSG-1: from phase A's stopping points; else [0, w]).
@@ -1111,7 +1218,8 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
                                             const unsigned long long* BX = nullptr, uint16_t* wl_s = nullptr,
                                             float* inc_sb = nullptr, const unsigned* BY = nullptr,
                                             const int2* cnt_prev = nullptr, int2* cnt_out = nullptr,
-                                            unsigned* done = nullptr, int b_self = 0) {
+                                            unsigned* done = nullptr, int b_self = 0,
+                                            const float2* CY = nullptr) {
     const int nwarps = blockDim.x >> 5;
     const int kPerWarp = (cta_n + nwarps - 1) / nwarps;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1175,6 +1283,8 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
         __syncwarp();
         sorted_phase_a<K1>(P2, w, cta0, 0, cnt, eps_s, steps, stop_s, L.scan_unified != 0, wl);
         wl_cnt = cnt;
+    } else if (CY && w >= L.col_min_w) {
+        sorted_phase_a_cols<K1>(P2, CY, w, cta0, wb, we, eps_s, steps, stop_s);
     } else {
         sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s, L.scan_unified != 0);
     }

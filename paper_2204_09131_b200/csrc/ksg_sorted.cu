@@ -201,6 +201,30 @@ __global__ void rank_merge_kernel(const KsgLaunch L, const int32_t* __restrict__
     YS[o + ry] = vy;
 }
 
+// Box-assisted phase A (sorted_phase_a_cols): each scan item's columns of kColW consecutive x-sorted points, sorted
+// by y into CY as (y, x) — one warp per column (a 32-key register bitonic sort, keys y with the lane as payload).
+__global__ void __launch_bounds__(kSortedThreads)
+    column_sort_kernel(const KsgLaunch L, const int32_t* __restrict__ list, const int64_t* __restrict__ soff,
+                       const float2* __restrict__ P2g, float2* __restrict__ CYg, const KsgItem* __restrict__ items) {
+    static_assert(kColW == 32, "one warp per column");
+    const KsgItem it = items[blockIdx.x];
+    const int b = it.win;
+    const int w = L.wins[list[b]].w;
+    if (w < L.col_min_w) return;  // block-uniform
+    const int64_t o = soff[b];
+    const int n = min(L.sorted_ppc, w - it.i0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int c0 = it.i0 + warp * kColW; c0 < it.i0 + n; c0 += nw * kColW) {
+        const int p = c0 + lane;
+        const float2 v = p < w ? P2g[o + p] : make_float2(0.0f, 0.0f);
+        unsigned long long key[1] = {p < w ? ((unsigned long long)sortable(v.y) << 32) | (unsigned)lane : ~0ull};
+        warp_sort<unsigned long long, 1>(key, lane);
+        const int src = (int)(key[0] & 31u);
+        const float vx = __shfl_sync(0xffffffffu, v.x, src), vy = __shfl_sync(0xffffffffu, v.y, src);
+        if (p < w) CYg[o + p] = make_float2(vy, vx);
+    }
+}
+
 // first index in [lo, hi) where pred is false, for pred true...true false...false
 // left side: smallest j in [0, m] with fl(v - s[j]) < eps (pred false...true)
 template <int K1, bool V2>
@@ -209,7 +233,7 @@ __global__ void __launch_bounds__(kSortedThreads)
                       const float2* __restrict__ P2g, const int32_t* __restrict__ OXg, const float* __restrict__ YSg,
                       const KsgItem* __restrict__ items, const KsgInc* __restrict__ inc, float* __restrict__ EPS,
                       const unsigned long long* __restrict__ BX, const unsigned* __restrict__ BY,
-                      int2* __restrict__ CNT, unsigned* __restrict__ sync) {
+                      int2* __restrict__ CNT, unsigned* __restrict__ sync, const float2* __restrict__ CYg) {
     const int ppc = L.sorted_ppc;  // points per CTA (runtime: 256 for latency, 1024 for throughput)
     __shared__ float eps_s[kSortedPts];
     __shared__ int2 stop_s[kSortedPts];
@@ -238,14 +262,14 @@ __global__ void __launch_bounds__(kSortedThreads)
                         stop_s, chain && ic->level > 0 ? ic : nullptr,
                         chain && ic->level > 0 ? EPS + ic->eps_prev : nullptr, chain ? EPS + o : nullptr, BX, wl_s,
                         inc_sb, BY, chain && ic->level > 0 ? CNT + ic->eps_prev : nullptr, chain ? CNT + o : nullptr,
-                        sync ? sync + 1 : nullptr, b);
+                        sync ? sync + 1 : nullptr, b, CYg ? CYg + o : nullptr);
 }
 
 template <int K1>
 cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* soff, const float2* P2,
                      const int32_t* OX, const float* YS, const KsgItem* items, int32_t n_items, cudaStream_t st,
                      const KsgInc* inc, float* EPS, const unsigned long long* BX, const unsigned* BY, int2* CNT,
-                     const int32_t* lv_off, int n_lv, int inc_d_max, unsigned* sync) {
+                     const int32_t* lv_off, int n_lv, int inc_d_max, unsigned* sync, const float2* CY) {
     // NEXT-3 chains: one launch over the level-ordered items; a level-j window's CTAs wait (per window) for the
     // level-(j-1) predecessor's CTAs, which took earlier work tickets (no per-level launch tails)
     (void)lv_off;
@@ -254,10 +278,10 @@ cudaError_t sorted_k(const KsgLaunch& L, const int32_t* list, const int64_t* sof
     unsigned* sy = chains ? sync : nullptr;
     if (L.variant == 1)
         sorted_knn_kernel<K1, true><<<n_items, kSortedThreads, smem, st>>>(L, list, soff, P2, OX, YS, items, inc, EPS,
-                                                                           BX, BY, CNT, sy);
+                                                                           BX, BY, CNT, sy, CY);
     else
         sorted_knn_kernel<K1, false><<<n_items, kSortedThreads, smem, st>>>(L, list, soff, P2, OX, YS, items, inc, EPS,
-                                                                            BX, BY, CNT, sy);
+                                                                            BX, BY, CNT, sy, CY);
     return cudaGetLastError();
 }
 }  // namespace
@@ -268,7 +292,7 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
                           int32_t n_items, cudaStream_t st, const KsgSegB* segb, const KsgBlk* blks,
                           int32_t n_blks, int blk_beta_max, unsigned long long* BX, unsigned* BY, const KsgInc* inc,
                           float* EPS, int2* CNT, const int32_t* lv_off, int n_lv, int inc_d_max,
-                          unsigned* sync) {
+                          unsigned* sync, float2* CY) {
     static_assert(kSortedPts % (kSortedThreads / 32) == 0, "scan CTA size");
     if (n_segs <= 0) return cudaSuccess;
     {
@@ -296,8 +320,13 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
+    if (CY) {  // box-assisted phase A for windows >= L.col_min_w: their y-sorted columns
+        column_sort_kernel<<<n_items, kSortedThreads, 0, st>>>(L, list, soff, P2, CY, items);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     ISY_K_CASES(sorted_k, L, list, soff, P2, OX, YS, items, n_items, st, inc, EPS, BX, BY, CNT, lv_off, n_lv, inc_d_max,
-                sync)
+                sync, CY)
 }
 
 
