@@ -968,7 +968,7 @@ __device__ __forceinline__ void sorted_phase_a_cols(const float2* P2, const floa
     bool act = kcur < we;
     int next = wb + 32;
     float xi = 0.f, yi = 0.f;
-    int m = 0, cl = 0, cr = 0, blk = 0;  // own-column block still to visit (blk < C / 8), else columns
+    int m = 0, cl = 0, cr = 0, blk = 0;  // own-column blocks visited (C / 8 of them), then the other columns
     float rk[K];
     auto start = [&](int ml) {
         m = cta0 + ml;
@@ -982,50 +982,74 @@ __device__ __forceinline__ void sorted_phase_a_cols(const float2* P2, const floa
         cr = col + 1;
         blk = 0;
     };
+    // one block of 8 own-column candidates in x order (itself and positions past w: +inf)
+    auto own_block = [&](int c0) {
+        float d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int pj = c0 + u;
+            const float2 c = pj < w ? P2[pj] : make_float2(kInf, 0.0f);
+            const float dd = fmaxf(fabsf(xi - c.x), fabsf(yi - c.y));
+            d[u] = (pj == m || pj >= w) ? kInf : dd;
+        }
+        float mn = d[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) mn = fminf(mn, d[u]);
+        if (mn < rk[K - 1]) topk_merge8<K>(rk, d);
+        steps += (unsigned long long)max(0, min(8, w - c0) - ((m >= c0 && m < c0 + 8) ? 1 : 0));
+    };
+    // walk column `col` (y ascending) from lo while fl(y_j - y_i) < r
+    auto walk = [&](const float2* col, int lo, int len) {
+        for (int j = lo; j < len; ++j) {
+            const float2 e = col[j];  // (y, x)
+            if (!(e.x - yi < rk[K - 1])) break;
+            ++steps;
+            const float dd = fmaxf(fabsf(xi - e.y), fabsf(yi - e.x));
+            if (dd < rk[K - 1]) topk_insert<K>(rk, dd);
+        }
+    };
     if (act) start(kcur);
     while (__any_sync(0xffffffffu, act)) {
         bool fin = false;
         if (act) {
-            if (blk < C / 8) {
-                // own column, one block of 8 in x order per iteration (itself and positions past w: +inf)
+            if (blk < C / 8) {  // two own-column blocks per iteration (16 independent loads)
                 const int c0 = (m / C) * C + blk * 8;
-                float d[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int pj = c0 + u;
-                    const float2 c = pj < w ? P2[pj] : make_float2(kInf, 0.0f);
-                    const float dd = fmaxf(fabsf(xi - c.x), fabsf(yi - c.y));
-                    d[u] = (pj == m || pj >= w) ? kInf : dd;
-                }
-                float mn = d[0];
-#pragma unroll
-                for (int u = 1; u < 8; ++u) mn = fminf(mn, d[u]);
-                if (mn < rk[K - 1]) topk_merge8<K>(rk, d);
-                steps += (unsigned long long)max(0, min(8, w - c0) - ((m >= c0 && m < c0 + 8) ? 1 : 0));
-                ++blk;
+                own_block(c0);
+                own_block(c0 + 8);
+                blk += 2;
             } else {
+                // the next column on each side within r of the point, both per iteration: their binary searches
+                // run in lockstep so the two chains of dependent loads overlap
                 const float r = rk[K - 1];
                 const float dl = cl >= 0 ? xi - P2[cl * C + C - 1].x : kInf;  // x-sorted: >= 0
                 const float dr = cr * C < w ? P2[cr * C].x - xi : kInf;
-                if (!(dl < r) && !(dr < r)) {
+                const bool gl = dl < r, gr = dr < r;
+                if (!gl && !gr) {
                     fin = true;
                 } else {
-                    const int c = dl <= dr ? cl : cr;
-                    if (dl <= dr) --cl; else ++cr;
-                    const float2* col = CY + c * C;
-                    const int len = min(C, w - c * C);
-                    int lo = 0, n = len;  // first j with fl(y_i - y_j) < r (y ascending: false...true)
-                    while (n > 0) {
-                        const int h = n >> 1;
-                        if (!(yi - col[lo + h].x < r)) { lo += h + 1; n -= h + 1; } else n = h;
-                        ++steps;
+                    const float2* colL = CY + (gl ? cl : 0) * C;
+                    const float2* colR = CY + (gr ? cr : 0) * C;
+                    const int lenL = gl ? min(C, w - cl * C) : 0, lenR = gr ? min(C, w - cr * C) : 0;
+                    int l0 = 0, n0 = lenL, l1 = 0, n1 = lenR;  // first j with fl(y_i - y_j) < r, per column
+                    while ((n0 | n1) > 0) {
+                        if (n0 > 0) {
+                            const int h = n0 >> 1;
+                            if (!(yi - colL[l0 + h].x < r)) { l0 += h + 1; n0 -= h + 1; } else n0 = h;
+                            ++steps;
+                        }
+                        if (n1 > 0) {
+                            const int h = n1 >> 1;
+                            if (!(yi - colR[l1 + h].x < r)) { l1 += h + 1; n1 -= h + 1; } else n1 = h;
+                            ++steps;
+                        }
                     }
-                    for (int j = lo; j < len; ++j) {
-                        const float2 e = col[j];  // (y, x)
-                        if (!(e.x - yi < rk[K - 1])) break;
-                        ++steps;
-                        const float dd = fmaxf(fabsf(xi - e.y), fabsf(yi - e.x));
-                        if (dd < rk[K - 1]) topk_insert<K>(rk, dd);
+                    if (gl) {
+                        walk(colL, l0, lenL);
+                        --cl;
+                    }
+                    if (gr) {
+                        walk(colR, l1, lenR);
+                        ++cr;
                     }
                 }
             }
