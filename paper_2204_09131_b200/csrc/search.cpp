@@ -750,6 +750,7 @@ struct BuJob {
 class HostPool {
 public:
     explicit HostPool(int n) {
+        if (const char* sp = std::getenv("ISYCOS_POOL_SPIN")) spin_max_ = std::max(0, std::atoi(sp));
         for (int i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
     }
     ~HostPool() {
@@ -794,7 +795,7 @@ private:
         uint64_t seen = 0;  // gen_ starts at 0 (a thread may start after the first run() began)
         for (;;) {
             uint64_t g = gen_.load(std::memory_order_acquire);
-            for (int spin = 0; g == seen && spin < 20000; ++spin) {
+            for (int spin = 0; g == seen && spin < spin_max_; ++spin) {
                 std::this_thread::yield();
                 g = gen_.load(std::memory_order_acquire);
             }
@@ -819,6 +820,7 @@ private:
     std::atomic<uint64_t> gen_{0};
     std::atomic<bool> stop_{false};
     int total_ = 0;
+    int spin_max_ = 20000;  // yields before a worker sleeps (ISYCOS_POOL_SPIN)
 };
 
 // Asynchronous submit (ISYCOS_ASYNC_SUBMIT, default on): one thread runs Engine::submit (binning, packing,
