@@ -136,6 +136,9 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_LAT_KEEP_SMALL_R")) lat_keep_small_R_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_LAT_TINY_MAX_W")) lat_tiny_max_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_COL_MIN_W")) col_min_w_ = std::max(kColW + 1, std::atoi(m));
+    if (const char* m = std::getenv("ISYCOS_LAT_LANES4_MAX_W")) lat_lanes4_max_w_ = std::atoi(m);
+    bin_threads_ = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+    if (const char* m = std::getenv("ISYCOS_BIN_THREADS")) bin_threads_ = std::max(1, std::atoi(m));
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
     if (const char* m = std::getenv("ISYCOS_WSORTED_MIN_W")) wsorted_min_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_SORTED_PPC"))
@@ -285,7 +288,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     // classes.  Large batches (TD layer starts: up to 10^7 windows, memory-bound single-threaded) split both
     // passes into contiguous chunks on host threads; the chunks' class lists are concatenated in chunk order,
     // so every list is in ascending window order exactly as in the serial pass.
-    const int n_chunks = n >= (int64_t)1 << 18 ? (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    const int n_chunks = n >= (int64_t)1 << 18 ? bin_threads_ : 1;
     auto par = [&](auto&& fn) {
         if (n_chunks == 1) {
             fn(0, (int64_t)0, n);
@@ -411,7 +414,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
     auto& lat_tiny = bins_.lat_tiny;  // w <= lat_tiny_max_w_: a warp per window inside the latency launch
     lat.clear();
     lat_tiny.clear();
-    const int lat_pts = lat_points_per_cta();
+
     auto to_latency = [&](std::vector<int32_t>& v) {
         for (int32_t q : v) {
             const int w = wins[q].w;
@@ -426,7 +429,8 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             }
             if (lat_split_on_ && variant == 0 && w <= 256) {  // 8 lanes per point (KSG-1)
                 lat.push_back(q);
-                n_items += (w + lat_pts - 1) / lat_pts;
+                const int lp = lat_points_per_cta(lat_lanes(w));
+                n_items += (w + lp - 1) / lp;
                 continue;
             }
             tile[2].push_back(q);
@@ -672,7 +676,9 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         item_off_lat = c;
         for (int32_t q : lat) {
             const int w = wins[q].w;
-            for (int i0 = 0; i0 < w; i0 += lat_pts) ip[c++] = KsgItem{q, i0};
+            const int lp = lat_points_per_cta(lat_lanes(w));
+            const int32_t fl = lat_item_flag(lat_lanes(w));
+            for (int i0 = 0; i0 < w; i0 += lp) ip[c++] = KsgItem{q, i0 | fl};
         }
         n_litems = c - item_off_lat;
         KsgItem* sp = reinterpret_cast<KsgItem*>(S.hstage + off_sitems);

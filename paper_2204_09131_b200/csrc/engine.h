@@ -116,7 +116,8 @@ cudaError_t launch_ksg_tile(const KsgLaunch& L, const KsgItem* items, int32_t n_
 // latency mode, KSG-1, w <= 256: 8 lanes per point (ksg_lat.cu); items {window, first point}, 32 points each
 cudaError_t launch_ksg_lat(const KsgLaunch& L, const KsgItem* items, int32_t n_items, const int32_t* tiny,
                            int32_t n_tiny, cudaStream_t st);
-int lat_points_per_cta();
+int lat_points_per_cta(int lanes);      // latency kernel: points per CTA with `lanes` (4 or 8) lanes per point
+int32_t lat_item_flag(int lanes);        // KsgItem.i0 flag selecting the lanes per point
 // sorted path: sort kernel over segments {list pos, start}, XL rank merge over blocks {list pos, start},
 // then the scan kernel over `items` {list pos, first point}
 // NEXT-3: blocks {pair, t, beta} are sorted first into BX (x keys) / BY (y keys); segments with segb[i].beta > 0
@@ -298,6 +299,9 @@ private:
     int32_t lat_keep_small_R_ = 0;   // brute small classes with R <= this stay warp-per-window even when sparse
     int32_t lat_tiny_max_w_ = 32;    // latency mode: windows up to this size run warp-per-window in the lat launch
     int32_t col_min_w_ = 1 << 30;    // throughput scan: box-assisted phase A for windows >= this (ISYCOS_COL_MIN_W)
+    int32_t lat_lanes4_max_w_ = 128; // latency kernel: 4 lanes per point up to this window size, else 8
+    int bin_threads_ = 1;            // host threads of a large batch's binning (ISYCOS_BIN_THREADS)
+    int lat_lanes(int w) const { return w <= lat_lanes4_max_w_ ? 4 : 8; }
 };
 
 // ---------------------------------------------------------------- search driver
