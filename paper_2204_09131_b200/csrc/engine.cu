@@ -137,6 +137,7 @@ Status Engine::init(int dev) {
     if (const char* m = std::getenv("ISYCOS_LAT_TINY_MAX_W")) lat_tiny_max_w_ = std::atoi(m);
     if (const char* m = std::getenv("ISYCOS_COL_MIN_W")) col_min_w_ = std::max(kColW + 1, std::atoi(m));
     if (const char* m = std::getenv("ISYCOS_LAT_LANES4_MAX_W")) lat_lanes4_max_w_ = std::atoi(m);
+    if (const char* m = std::getenv("ISYCOS_WS_GROUP")) ws_group_ = std::atoi(m);
     bin_threads_ = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
     if (const char* m = std::getenv("ISYCOS_BIN_THREADS")) bin_threads_ = std::max(1, std::atoi(m));
     if (const char* m = std::getenv("ISYCOS_FUSED")) fused_on_ = std::atoi(m) != 0;
@@ -836,7 +837,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
         if (wsorted[e].empty()) continue;
         const int32_t* wlp = reinterpret_cast<const int32_t*>(dbase + off_wlist) + wlist_off[e];
         const int32_t cnt = (int32_t)wsorted[e].size();
-        Status r = launch(0, 1, [&](cudaStream_t sg) { return launch_wsorted(L, wlp, cnt, 2 << e, sg); });
+        Status r = launch(0, 1, [&](cudaStream_t sg) { return launch_wsorted(L, wlp, cnt, 2 << e, ws_group(cnt), sg); });
         if (!r.ok()) return r;
     }
     if (!sorted.empty()) {

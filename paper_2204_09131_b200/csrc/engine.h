@@ -132,7 +132,7 @@ cudaError_t launch_sorted(const KsgLaunch& L, const int32_t* list, const int64_t
 constexpr int kIncChain = 16;  // NEXT-3 incremental chains: a window scanned from scratch every this many
 constexpr int kIncMaxD = 1024; // NEXT-3 incremental chains: grid steps up to this (two blocks staged in SMEM)
 // small windows on the sorted path: one warp per window, E = 2, 4, 8 keys per lane (w <= 32 E)
-cudaError_t launch_wsorted(const KsgLaunch& L, const int32_t* list, int32_t n, int E, cudaStream_t st);
+cudaError_t launch_wsorted(const KsgLaunch& L, const int32_t* list, int32_t n, int E, int G, cudaStream_t st);
 // fused latency path: items {list pos, slice start}; slices of fused_ppc(w, gmax) points
 cudaError_t launch_fused(const KsgLaunch& L, const int32_t* list, const KsgItem* items, int32_t n_items, int gmax,
                          cudaStream_t st);
@@ -301,7 +301,16 @@ private:
     int32_t col_min_w_ = 1 << 30;    // throughput scan: box-assisted phase A for windows >= this (ISYCOS_COL_MIN_W)
     int32_t lat_lanes4_max_w_ = 128; // latency kernel: 4 lanes per point up to this window size, else 8
     int bin_threads_ = 1;            // host threads of a large batch's binning (ISYCOS_BIN_THREADS)
+    int32_t ws_group_ = 0;           // warp-sorted kernel: warps per window (ISYCOS_WS_GROUP = 1, 2, 4; 0 = by batch size)
     int lat_lanes(int w) const { return w <= lat_lanes4_max_w_ ? 4 : 8; }
+    // warps per window of a warp-sorted launch of n windows: the most (<= 4) that keep n G warps within one
+    // wave of 40 resident warps per SM (E = 8's shared-memory limit), so a sparse round's windows finish G
+    // times sooner; a full batch keeps one warp per window
+    int ws_group(int64_t n) const {
+        if (ws_group_ == 1 || ws_group_ == 2 || ws_group_ == 4) return ws_group_;
+        const int64_t cap = 148 * 40;
+        return n * 4 <= cap ? 4 : n * 2 <= cap ? 2 : 1;
+    }
 };
 
 // ---------------------------------------------------------------- search driver
