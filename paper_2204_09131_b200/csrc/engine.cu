@@ -371,7 +371,7 @@ Status Engine::submit(int si, const PairPtrs* pairs, int32_t n_pairs, const KsgW
             } else if (use_sorted && w >= sorted_min_w_) {
                 B.sorted.push_back((int32_t)i);
                 B.soff.push_back(B.spts + kScanB);  // kScanB sentinel entries on either side of the window's region
-                B.spts += w + 2 * kScanB;
+                B.spts += (w + 2 * kScanB + 1) & ~1;  // even offsets: phase A loads 16-B aligned pairs of P2 entries
                 B.n_segs += (w + kSortedMaxW - 1) / kSortedMaxW;
                 if (w > kSortedMaxW) B.n_mblocks += (w + kMergePts - 1) / kMergePts;
                 int n2 = 1;

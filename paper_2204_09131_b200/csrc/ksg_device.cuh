@@ -809,7 +809,11 @@ __device__ __forceinline__ void topk_merge_sorted(float (&a)[K], const float (&b
 // P2 must carry sentinels: P2[-kScanB..-1] = (-inf, 0), P2[w..w+kScanB-1] = (+inf, 0) (no bounds checks).
 // Warp-local work queue: a lane that finishes its point takes the next one (ballot + popc), so warps do
 // not idle on their slowest lane (per-point scan lengths vary several-fold with the local density ratio).
-template <int K1>
+// PAIRS (two-sided form only): candidates loaded as 16-byte pairs from aligned blocks (see below); for P2 in global
+// memory at large w, where the lanes' blocks lie far apart (measured: w = 16,384 -9 %, 4,096 -4.5 %; shared memory
+// and w <= 1,024 slightly slower, so those keep 8-byte loads).
+constexpr int kPairsMinW = 2048;
+template <int K1, bool PAIRS = false>
 __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0, int wb, int we, float* eps_s,
                                                unsigned long long& steps, int2* stop_s = nullptr,
                                                bool unified = true, const uint16_t* wl = nullptr) {
@@ -824,7 +828,8 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
     float xi = 0.f, yi = 0.f;
     int lj = 0, rj = 0;  // next unvisited index on each side
     bool lact = false, ract = false;
-    constexpr int K = K1 - 1;  // the k smallest over j != i (the scan never visits self)
+    bool lself = false, rself = false;  // two-sided form: the side's first block holds self (masked)
+    constexpr int K = K1 - 1;  // the k smallest over j != i (self's d = 0 is never merged)
     float rk[K];
     auto start = [&](int ml) {
         const int m = cta0 + ml;
@@ -835,6 +840,20 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
         for (int t = 0; t < K; ++t) rk[t] = kInf;
         lj = m - 1;
         rj = m + 1;
+        lself = rself = false;
+        if (PAIRS && !unified) {
+            // aligned blocks: left [lj - 7, lj] with lj odd, right [rj, rj + 7] with rj even, so every block is four
+            // 16-byte pairs (P2 + even index is 16-byte aligned); the side whose first block would start one entry
+            // short takes self into it instead, and self's distance there is replaced by +inf
+            if (!(lj & 1)) {
+                lj = m;
+                lself = true;
+            }
+            if (rj & 1) {
+                rj = m;
+                rself = true;
+            }
+        }
         lact = true;  // the sentinels end a side
         ract = true;
     };
@@ -894,6 +913,51 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                 if (stop_s) stop_s[mloc] = make_int2(lj, rj);
             }
         } else if (act) {
+          if constexpr (PAIRS) {
+            // One 16-byte load per pair of candidates: the lanes' blocks lie scattered over the window, and the
+            // L1 data pipe serves a warp load roughly per distinct line touched, so pairs halve its wavefronts
+            // (8-byte loads: 5.4 wavefronts per request, the scan's bound at w = 16,384).
+            if (lact) {
+                float d[B], far = 0.f;
+#pragma unroll
+                for (int h = 0; h < B / 2; ++h) {
+                    // (P2[lj - 2h - 1], P2[lj - 2h]); P2[-B..-1] = (-inf, 0) sentinels: d = far = +inf
+                    const float4 c = *reinterpret_cast<const float4*>(P2 + (lj - 2 * h - 1));
+                    const float dxa = xi - c.z;  // >= 0: ascending order
+                    const float dxb = xi - c.x;
+                    d[2 * h] = fmaxf(dxa, fabsf(yi - c.w));
+                    d[2 * h + 1] = fmaxf(dxb, fabsf(yi - c.y));
+                    far = dxb;
+                }
+                if (lself) {  // d[0] is self's 0 (position m)
+                    d[0] = kInf;
+                    lself = false;
+                }
+                visit(d);
+                lj -= B;
+                lact = far < rk[K - 1];
+            }
+            if (ract) {
+                float d[B], far = 0.f;
+#pragma unroll
+                for (int h = 0; h < B / 2; ++h) {
+                    // (P2[rj + 2h], P2[rj + 2h + 1]); P2[w..w+B-1] = (+inf, 0) sentinels
+                    const float4 c = *reinterpret_cast<const float4*>(P2 + (rj + 2 * h));
+                    const float dxa = c.x - xi;
+                    const float dxb = c.z - xi;
+                    d[2 * h] = fmaxf(dxa, fabsf(yi - c.y));
+                    d[2 * h + 1] = fmaxf(dxb, fabsf(yi - c.w));
+                    far = dxb;
+                }
+                if (rself) {  // d[0] is self's 0 (position m)
+                    d[0] = kInf;
+                    rself = false;
+                }
+                visit(d);
+                rj += B;
+                ract = far < rk[K - 1];
+            }
+          } else {
             if (lact) {
                 float d[B], far = 0.f;
 #pragma unroll
@@ -920,6 +984,7 @@ __device__ __forceinline__ void sorted_phase_a(const float2* P2, int w, int cta0
                 rj += B;
                 ract = far < rk[K - 1];
             }
+          }
             if (!lact && !ract) {
                 fin = true;
                 steps += visited();
@@ -1252,6 +1317,8 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
     unsigned long long steps = 0;
     unsigned reused = 0;
     int wl_cnt = -1;  // >= 0: incremental window, this warp's scan list length
+    // phase A's 16-byte pair loads: P2 in global memory (the throughput scan's scratch) and large windows
+    const bool pairs = w >= kPairsMinW && !__isShared(P2);
     if (inc && eps_prev && cnt_prev && stop_s && !V2) {
         // incremental window: radii carried over where the removed / inserted blocks cannot change them; the
         // remaining points (and the newly inserted ones) form this warp's scan list
@@ -1305,10 +1372,15 @@ __device__ __forceinline__ void sorted_scan(const KsgLaunch& L, int q, int w, in
             cnt += __popc(bm);
         }
         __syncwarp();
-        sorted_phase_a<K1>(P2, w, cta0, 0, cnt, eps_s, steps, stop_s, L.scan_unified != 0, wl);
+        if (pairs)
+            sorted_phase_a<K1, true>(P2, w, cta0, 0, cnt, eps_s, steps, stop_s, L.scan_unified != 0, wl);
+        else
+            sorted_phase_a<K1>(P2, w, cta0, 0, cnt, eps_s, steps, stop_s, L.scan_unified != 0, wl);
         wl_cnt = cnt;
     } else if (CY && w >= L.col_min_w) {
         sorted_phase_a_cols<K1>(P2, CY, w, cta0, wb, we, eps_s, steps, stop_s);
+    } else if (pairs) {
+        sorted_phase_a<K1, true>(P2, w, cta0, wb, we, eps_s, steps, stop_s, L.scan_unified != 0);
     } else {
         sorted_phase_a<K1>(P2, w, cta0, wb, we, eps_s, steps, stop_s, L.scan_unified != 0);
     }

@@ -330,3 +330,18 @@ def test_maximum_window_and_empty_batch(isy, orc):
     with pytest.raises(isy.IsycosError) as e:
         isy.isycos_mi_batch(x, y, [(0, w + 1)], 4)
     assert e.value.code == -2
+
+
+@pytest.mark.parametrize("k", [1, 4, 8])
+def test_pair_loads_odd_layouts(isy, orc, k):
+    """Phase A's 16-byte pair loads (throughput scan, w >= 2,048): aligned blocks with self masked in the first
+    block of one side, so both parities of every position are exercised; odd window sizes before and after the
+    large ones give odd scratch offsets (rounded up to even by the engine), plus a tied series."""
+    wl = datagen.cfg2(n=40_000)
+    x, y = wl.series
+    sizes = [257, 999, 2049, 3001, 4095, 2048, 8191, 8193, 12289, 301, 2051]
+    W = [(3 + 7 * i, 3 + 7 * i + w) for i, w in enumerate(sizes)] + [(len(x) - 4097, len(x))]
+    check_windows(isy, orc, x, y, W, k, debug=True, label=f"pairs k={k}", unfused=True)
+    st = datagen.Stream(21, 2)
+    xi = np.floor(st.uniform(len(x)) * 9).astype(np.float32)
+    check_windows(isy, orc, xi, y, W, k, debug=True, label=f"pairs ties k={k}", unfused=True)
