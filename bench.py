@@ -388,13 +388,22 @@ def main():
 
     import torch
 
+    # ISYCOS_BENCH_DRYRUN=1: a code-path check of the N > 1 flow on a box with fewer GPUs than ranks (ranks share
+    # a GPU, gloo on the host for the collectives; the ranks' kernels never wait on one another).  Its line is
+    # marked "dry_run" and is never a scaling number.
+    dry_run = world > 1 and os.environ.get("ISYCOS_BENCH_DRYRUN") == "1"
+    if dry_run:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) in the log
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dry_run:
+            dist.init_process_group("gloo")
+        else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) in the log
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2204_09131_b200 import build
 
     if rank == 0:
@@ -498,7 +507,7 @@ def main():
     def agg(v, op):
         if not dist:
             return v
-        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cpu" if dry_run else "cuda")
         dist.all_reduce(t, op=op)
         return t.item()
 
@@ -568,6 +577,8 @@ def main():
             "host_ms_per_step_rank0": host_ms / args.steps,
             "clocks": clocks,
         }
+        if dry_run:
+            line["dry_run"] = "ranks share one GPU, gloo collectives: a code-path check, not a measurement"
         if world == 1 and not args.no_cpu_baseline and multi_pair:
             cores, model = cpu_info()
             pairs = batch_pairs(wl, 0, cores, 1)[:cores]

@@ -70,8 +70,13 @@ __device__ __forceinline__ void lat_points(const KsgLaunch& L, int q, const KsgW
 
 constexpr int kTinyCap = 36;                          // per-warp slice of a tiny window (w <= 32, +4 pad)
 
+#ifdef ISY_LAT_MINB  // A/B knob: resident CTAs per SM the register allocation must allow (measured)
+#define ISY_LAT_BOUNDS __launch_bounds__(kLatThreads, ISY_LAT_MINB)
+#else
+#define ISY_LAT_BOUNDS __launch_bounds__(kLatThreads)
+#endif
 template <int K1>
-__global__ void __launch_bounds__(kLatThreads)
+__global__ void ISY_LAT_BOUNDS
     ksg_lat_kernel(const KsgLaunch L, const KsgItem* __restrict__ items, int32_t n_items,
                    const int32_t* __restrict__ tiny, int32_t n_tiny) {
     __shared__ __align__(16) float sx[kSmallWarps * kTinyCap];  // >= 256
